@@ -1,0 +1,213 @@
+/*
+ * minife.h — C ABI of the B200-native MiniFE CG hot path (arxiv 1505.08023).
+ *
+ * The library assembles and solves the FE system of the paper's problem statement
+ * (steady-state heat conduction on the unit cube, trilinear hex elements, u = 1 on
+ * the plane x = 1 and u = 0 on the other faces) with unpreconditioned CG ("conjugate
+ * gradient(CG) method without preprocessing"), entirely in hand-written sm_100a CUDA
+ * kernels.  Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; C0..C8 / G1..G20 =
+ * readings in DESIGN.md §3.  SURVEY.md §8(b) is the contract this header implements.
+ *
+ * Conventions (all entry points):
+ *   - Every int-returning call returns MINIFE_OK (0) or one of the MINIFE_E* codes below; the
+ *     library never aborts and never prints.  minife_strerror() maps a code to a static
+ *     string; minife_last_error() returns the ctx's last detailed message.
+ *   - A minife_ctx is not thread-safe: drive it from one host thread.
+ *   - Host pointers are caller-owned; the library never retains them past the call.
+ *   - Device pointers (the *_device calls) are caller-owned device memory on the ctx's device.
+ *   - Global node/row ids are x-fastest: id = ix + (nx+1)*(iy + (ny+1)*iz) (Fig 3.6).
+ *   - All arithmetic is binary64, round-to-nearest-even, no FMA contraction, subnormals kept.
+ */
+#ifndef MINIFE_H
+#define MINIFE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------- */
+#define MINIFE_OK 0
+#define MINIFE_EINVAL 1      /* invalid argument (bad size, NULL, buffer too small, ...) */
+#define MINIFE_ESTATE 2      /* call not valid in the ctx's state (e.g. solve before assemble) */
+#define MINIFE_ECUDA 3       /* a CUDA runtime call failed */
+#define MINIFE_ENCCL 4       /* an NCCL call failed */
+#define MINIFE_ENOMEM 5      /* device or host allocation failed */
+#define MINIFE_ENOTSPD 6     /* CG met pAp < 0, or pAp == 0 with rr != 0 */
+#define MINIFE_EDIVERGED 7   /* CG met a non-finite pAp or rr */
+#define MINIFE_ENODEV 8      /* no CUDA device (or fewer than requested) */
+
+/* ---- context modes ---------------------------------------------------------------------- */
+#define MINIFE_MODE_SINGLE 0   /* one process, one GPU, one part */
+#define MINIFE_MODE_VIRTUAL 1  /* one process, one GPU, p RCB parts ("virtual ranks") */
+#define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1, NCCL comms */
+#define MINIFE_MODE_RANK 3     /* SPMD: this process is rank r of w (torchrun), NCCL comm */
+
+typedef struct minife_ctx minife_ctx;
+
+/* Per-part (per-rank) plan, host-computed from the RCB partition (G15). */
+typedef struct minife_part_info {
+    int32_t rank, world;
+    int32_t box[6];           /* element box lo_x,lo_y,lo_z, hi_x,hi_y,hi_z (half-open)  */
+    int32_t own[6];           /* owned node box lo_x,lo_y,lo_z, hi_x,hi_y,hi_z (inclusive) */
+    int32_t n_neighbors;      /* ranks this part exchanges halo values with              */
+    int32_t device;
+    int64_t rows;             /* owned nodes = local rows (ascending global id)     */
+    int64_t externals;        /* halo slots, ordered (owner rank, global id)       */
+    int64_t nnz;              /* stored entries of the local rows (27-point pattern)      */
+    int64_t slices;           /* SELL-32 slices = ceil(rows/32)                           */
+    int64_t sell_entries;     /* sum over slices of 32*width (incl. padding)              */
+    int64_t send_total;       /* values this part sends per halo exchange                 */
+} minife_part_info;
+
+typedef struct minife_info {
+    int32_t nx, ny, nz;       /* elements per axis (nodes = n+1, G1)                */
+    int32_t mode;             /* MINIFE_MODE_*                                            */
+    int32_t nparts;           /* parts held by THIS ctx (1 in SINGLE and RANK mode)       */
+    int32_t rank, world;      /* RANK mode: this rank / world; otherwise 0 / nparts       */
+    int32_t assembled;        /* 1 after a successful minife_assemble                     */
+    int64_t rows, nnz;        /* GLOBAL counts: prod(N_a), prod(3N_a - 2) (§8(a))          */
+    int64_t local_rows;       /* rows held by this ctx (all parts)                        */
+    int64_t local_nnz;
+    int64_t max_part_rows, max_part_nnz, max_part_externals;
+    int64_t sell_entries;     /* held by this ctx                                         */
+    int64_t device_bytes;     /* device memory held by this ctx                           */
+} minife_info;
+
+typedef struct minife_cg_result {
+    int32_t status;           /* MINIFE_OK, MINIFE_ENOTSPD or MINIFE_EDIVERGED             */
+    int32_t iterations;       /* completed CG iterations                                  */
+    int32_t converged;        /* 1 iff a stop test fired (tol, rr == 0); 0 at the cap      */
+    int32_t max_iters;
+    double norm_b;            /* hist[0] = sqrt(dot(b,b))                                 */
+    double final_rel_residual;/* hist[iterations] / hist[0] (0 if norm_b == 0)            */
+    double seconds;           /* device time of the solve, CUDA events on the ctx stream  */
+    double flops;             /* algorithmic: iterations * (2 nnz + 10 rows), global      */
+    double bytes;             /* algorithmic HBM bytes of this ctx's kernels */
+} minife_cg_result;
+
+/* Per-kernel-class device times from minife_cg_profile (milliseconds, summed over launches). */
+typedef struct minife_kernel_times {
+    double spmv_ms;           /* K1: SpMV + pAp epilogue (a2)                             */
+    double update_xr_ms;      /* K6: x/r update + rr (a3 finalise, a4)                    */
+    double update_p_ms;       /* K7: p update (a5 finalise, a6)                           */
+    double comm_ms;           /* halo + accumulator reductions (a1, a3/a5 all-reduce)     */
+    int32_t spmv_launches, update_xr_launches, update_p_launches, iterations;
+} minife_kernel_times;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+
+/* Elements per axis nx,ny,nz >= 1 on the unit cube; ngpu >= 1 devices 0..ngpu-1
+ * of this process.  ngpu == 1 -> MINIFE_MODE_SINGLE, ngpu > 1 -> MINIFE_MODE_MULTI (RCB over
+ * ngpu parts, NCCL comms from ncclCommInitAll).  Computes the RCB plan and allocates every
+ * device buffer.  *out is set only on success.
+ * Errors: MINIFE_EINVAL (n < 1, ngpu < 1, out == NULL, RCB leaf without elements),
+ * MINIFE_ENODEV (ngpu > visible devices), MINIFE_ENOMEM, MINIFE_ECUDA, MINIFE_ENCCL. */
+int minife_create(int nx, int ny, int nz, int ngpu, minife_ctx **out);
+
+/* p RCB parts ("virtual ranks") on device 0 of this process: the exact multi-rank data
+ * layout, halo plans and reductions, with device-local copies as the transport.
+ * Errors as minife_create. */
+int minife_create_virtual(int nx, int ny, int nz, int nparts, minife_ctx **out);
+
+/* SPMD: NCCL unique id (128 bytes) to broadcast from rank 0 to all ranks. */
+int minife_nccl_unique_id(void *uid128);
+
+/* SPMD: this process is `rank` of `world` and drives CUDA device `device`; uid128 is rank
+ * 0's minife_nccl_unique_id.  Collective: every rank must call it.  Errors as
+ * minife_create, plus MINIFE_EINVAL for rank/world out of range. */
+int minife_create_rank(int nx, int ny, int nz, int rank, int world, int device,
+                       const void *uid128, minife_ctx **out);
+
+/* Frees every device/host resource and NCCL comm of the ctx.  NULL-safe. */
+void minife_destroy(minife_ctx *ctx);
+
+/* Run all subsequent device work of a SINGLE/RANK ctx on `stream` (a cudaStream_t, may be a
+ * torch stream).  NULL restores the ctx's own stream.  Invalidates captured graphs.
+ * Errors: MINIFE_EINVAL (ctx NULL), MINIFE_ESTATE (mode VIRTUAL/MULTI). */
+int minife_set_stream(minife_ctx *ctx, void *stream);
+
+const char *minife_strerror(int status);
+const char *minife_last_error(const minife_ctx *ctx);
+
+/* ---- the hot path ---------------------------------------------------------------------- */
+
+/* Structure -> SELL-32 (a0.2), element operator (a0.3, C1), gather-assembly (a0.4, C2) and
+ * Dirichlet elimination (a0.5, C3) on the device, for every part.  Idempotent.
+ * Errors: MINIFE_EINVAL (ctx NULL), MINIFE_ECUDA. */
+int minife_assemble(minife_ctx *ctx);
+
+/* Unpreconditioned CG (C6): x0 = 0, r0 = b, p0 = r0; at most max_iters
+ * iterations; stops when hist[k] <= tol*hist[0] or rr == 0.  tol == 0 runs exactly
+ * max_iters (benchmark mode).  Dots are exactly rounded (C5), so the result is independent
+ * of the partition and bit-identical to the oracle.  Blocks until the solve has finished.
+ * `res` may be NULL.  Returns MINIFE_OK, MINIFE_ENOTSPD or MINIFE_EDIVERGED (also stored in
+ * res->status); the cap reached is MINIFE_OK with converged = 0.
+ * Errors: MINIFE_ESTATE (not assembled), MINIFE_EINVAL (max_iters < 1, tol < 0 or NaN),
+ * MINIFE_ECUDA, MINIFE_ENCCL. */
+int minife_cg_solve(minife_ctx *ctx, int max_iters, double tol, minife_cg_result *res);
+
+/* Same iteration sequence as minife_cg_solve, launched without a graph and bracketed by CUDA
+ * events per kernel class, to attribute device time (Fig 2.2 analogue).  Leaves the solution
+ * state valid.  Errors as minife_cg_solve. */
+int minife_cg_profile(minife_ctx *ctx, int max_iters, minife_kernel_times *out);
+
+/* y = A x for the assembled, Dirichlet-imposed A (C4).  SINGLE/VIRTUAL/MULTI: x, y are host
+ * arrays of `rows` doubles in global id order.  RANK: x, y hold this rank's owned rows in
+ * ascending global id (minife_get_owned_ids); the halo is exchanged with the other ranks.
+ * Errors: MINIFE_ESTATE (not assembled), MINIFE_EINVAL (NULL), MINIFE_ECUDA, MINIFE_ENCCL. */
+int minife_spmv(minife_ctx *ctx, const double *x, double *y);
+
+/* SINGLE only: y = A x on device arrays of `rows` doubles, launched on `stream` (NULL = the
+ * ctx stream); asynchronous.  Errors: MINIFE_ESTATE (other modes, not assembled),
+ * MINIFE_EINVAL (NULL pointers), MINIFE_ECUDA. */
+int minife_spmv_device(minife_ctx *ctx, const double *d_x, double *d_y, void *stream);
+
+/* ---- getters --------------------------------------------------------------------------- */
+
+int minife_get_info(const minife_ctx *ctx, minife_info *out);
+int minife_get_part_info(const minife_ctx *ctx, int part, minife_part_info *out);
+
+/* Canonical global CSR of the assembled system (rows in global id order, columns ascending,
+ * structural zeros kept): row_ptr[rows+1], col[nnz], val[nnz].  RANK mode: this rank's
+ * owned rows only (row_ptr[local_rows+1]), global column ids.  Errors: MINIFE_ESTATE,
+ * MINIFE_EINVAL, MINIFE_ECUDA. */
+int minife_export_csr(minife_ctx *ctx, int64_t *row_ptr, int64_t *col, double *val);
+
+/* Rows `gids[0..n)` of the assembled system (any size, for sampled parity): cols/vals are
+ * n*27 arrays (row i at [27*i]), lens[i] = its length.  Rows not held by this ctx give
+ * lens[i] = -1.  Errors: MINIFE_ESTATE, MINIFE_EINVAL, MINIFE_ECUDA. */
+int minife_export_rows(minife_ctx *ctx, int64_t n, const int64_t *gids, int64_t *cols,
+                       double *vals, int32_t *lens);
+
+/* b, x (after cg_solve) in global id order (RANK: owned rows, ascending global id). */
+int minife_get_rhs(minife_ctx *ctx, double *b);
+int minife_get_solution(minife_ctx *ctx, double *x);
+
+/* Residual-norm history hist[0..iterations] of the last solve (hist[0] = ||b||).  cap is the
+ * capacity of h; *n receives iterations+1.  MINIFE_EINVAL if cap < iterations+1. */
+int minife_get_history(minife_ctx *ctx, double *h, int cap, int *n);
+
+/* RANK mode: global ids of this rank's owned rows, ascending (local_rows entries). */
+int minife_get_owned_ids(const minife_ctx *ctx, int64_t *gids);
+
+/* ---- host-only plan queries (no GPU needed) -------------------------------------------- */
+
+/* RCB plan of part `rank` of `world` for an nx*ny*nz mesh (G15): fills `out` except nnz,
+ * slices, sell_entries computed from closed forms.  Errors: MINIFE_EINVAL. */
+int minife_plan(int nx, int ny, int nz, int world, int rank, minife_part_info *out);
+
+/* The halo lists of that part: ext_gids[externals] in slot order; per neighbor (ascending
+ * rank) nbr[k], recv_cnt[k], send_cnt[k]; send_idx[send_total] = local row indices to send,
+ * concatenated by neighbor.  Any pointer may be NULL.  Errors: MINIFE_EINVAL. */
+int minife_plan_lists(int nx, int ny, int nz, int world, int rank, int64_t *ext_gids,
+                      int32_t *nbr, int64_t *recv_cnt, int64_t *send_cnt, int32_t *send_idx);
+
+/* Library version string. */
+const char *minife_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

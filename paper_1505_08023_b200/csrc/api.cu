@@ -1,0 +1,1157 @@
+// api.cu — the C ABI of include/minife.h: context, plans, device buffers, graph-captured CG
+// driver, NCCL / virtual-rank transports, parity getters.  Host code; every numeric step of
+// the method runs in kernels.cu.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/minife.h"
+#include "exact.cuh"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace minife;
+
+#define MINIFE_VERSION "minife-b200 0.1.0 (sm_100a)"
+
+namespace {
+
+struct Part {
+    int dev = 0;
+    Plan plan;
+    int64_t rows = 0, ncols = 0, nslices = 0, entries = 0, nnz = 0;
+    std::vector<int64_t> h_slice_off;
+    int64_t *d_slice_off = nullptr;
+    uint8_t *d_row_len = nullptr, *d_width = nullptr;
+    int32_t *d_col = nullptr;
+    double *d_val = nullptr;
+    double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
+    double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
+    unsigned long long *d_acc = nullptr;          // [0, ACC_WORDS) pAp, [ACC_WORDS, 2*) rr
+    CgState *d_st = nullptr;
+    double *d_hist = nullptr, *d_rr = nullptr;
+    int hist_cap = 0;
+    int64_t *d_ext_gid = nullptr;
+    int32_t *d_ext_slot = nullptr;
+    int32_t *d_send_idx = nullptr;
+    double *d_sendbuf = nullptr;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    int grid_spmv = 1, grid_upd = 1;
+    size_t bytes = 0;
+    unsigned long long *acc_pAp() const { return d_acc; }
+    unsigned long long *acc_rr() const { return d_acc + ACC_WORDS; }
+};
+
+struct DevGuard {
+    int prev = 0;
+    bool ok = false;
+    explicit DevGuard(int dev) {
+        ok = cudaGetDevice(&prev) == cudaSuccess;
+        cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        if (ok) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+
+// ----------------------------------------------------------------------------------------
+// NCCL is resolved at run time (dlopen), never linked: the process may already hold torch's
+// NCCL (a newer libnccl.so.2 than the system one) and two copies must not be mixed.  Order:
+// an already-loaded libnccl.so.2 (RTLD_NOLOAD), then $MINIFE_NCCL_LIB (the binding points it
+// at the torch wheel's copy), then the default search path.
+// ----------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommInitAll)(ncclComm_t *, int, const int *);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    const char *(*GetErrorString)(ncclResult_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t);
+};
+
+const NcclApi *nccl() {
+    static NcclApi api;
+    static int state = 0;   // 0 untried, 1 ok, -1 failed
+    if (state) return state > 0 ? &api : nullptr;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char *env = getenv("MINIFE_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        state = -1;
+        return nullptr;
+    }
+    bool ok = true;
+    auto sym = [&](const char *n) {
+        void *f = dlsym(h, n);
+        if (!f) ok = false;
+        return f;
+    };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommInitAll = (decltype(api.CommInitAll))sym("ncclCommInitAll");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+    api.Send = (decltype(api.Send))sym("ncclSend");
+    api.Recv = (decltype(api.Recv))sym("ncclRecv");
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    state = ok ? 1 : -1;
+    return ok ? &api : nullptr;
+}
+}  // namespace
+
+struct minife_ctx {
+    Mesh mesh{};
+    int mode = MINIFE_MODE_SINGLE;
+    int world = 1, rank = 0;
+    std::vector<Part> parts;
+    cudaStream_t user_stream = nullptr;
+    bool assembled = false;
+    std::string err;
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    int g_iters = -1;
+    double g_tol = -1.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // last solve
+    int last_iters = 0;
+    bool solved = false;
+};
+
+static void set_err(minife_ctx *c, const char *fmt, ...) {
+    if (!c) return;
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+}
+
+#define CUDA_TRY(ctx, call)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            set_err(ctx, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+            return e_ == cudaErrorMemoryAllocation ? MINIFE_ENOMEM : MINIFE_ECUDA;            \
+        }                                                                                     \
+    } while (0)
+
+#define NCCL_TRY(ctx, call)                                                                   \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) {                                                              \
+            set_err(ctx, "%s: %s (%s:%d)", #call, nccl()->GetErrorString(r_), __FILE__,       \
+                    __LINE__);                                                                \
+            return MINIFE_ENCCL;                                                              \
+        }                                                                                     \
+    } while (0)
+
+#define TRY(call)                                                                             \
+    do {                                                                                      \
+        int s_ = (call);                                                                      \
+        if (s_ != MINIFE_OK) return s_;                                                       \
+    } while (0)
+
+static cudaStream_t stream_of(minife_ctx *c, Part &p) {
+    if (c->user_stream && (c->mode == MINIFE_MODE_SINGLE || c->mode == MINIFE_MODE_RANK))
+        return c->user_stream;
+    return p.stream;
+}
+
+template <class T>
+static int dalloc(minife_ctx *c, Part &p, T **ptr, size_t n) {
+    if (n == 0) n = 1;
+    CUDA_TRY(c, cudaMalloc((void **)ptr, n * sizeof(T)));
+    p.bytes += n * sizeof(T);
+    return MINIFE_OK;
+}
+
+static void free_part(Part &p) {
+    DevGuard g(p.dev);
+    void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width, p.d_col,     p.d_val,    p.d_b,
+                    p.d_x,         p.d_r,       p.d_p,     p.d_Ap,      p.d_xin,    p.d_yout,
+                    p.d_acc,       p.d_st,      p.d_hist,  p.d_rr,      p.d_ext_gid,
+                    p.d_ext_slot,  p.d_send_idx, p.d_sendbuf};
+    for (void *b : bufs)
+        if (b) cudaFree(b);
+    if (p.comm) nccl()->CommDestroy(p.comm);
+    if (p.stream) cudaStreamDestroy(p.stream);
+}
+
+// ----------------------------------------------------------------------------------------
+// creation
+// ----------------------------------------------------------------------------------------
+
+static int alloc_hist(minife_ctx *c, Part &p, int cap) {
+    DevGuard g(p.dev);
+    if (p.d_hist) cudaFree(p.d_hist);
+    if (p.d_rr) cudaFree(p.d_rr);
+    p.d_hist = p.d_rr = nullptr;
+    CUDA_TRY(c, cudaMalloc((void **)&p.d_hist, sizeof(double) * cap));
+    CUDA_TRY(c, cudaMalloc((void **)&p.d_rr, sizeof(double) * cap));
+    p.hist_cap = cap;
+    return MINIFE_OK;
+}
+
+static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
+    p.dev = dev;
+    p.plan = plan;
+    DevGuard g(dev);
+    p.rows = plan.n_owned;
+    p.ncols = plan.n_owned + plan.n_ext;
+    p.nslices = (p.rows + 31) / 32;
+    p.nnz = plan.local_nnz();
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
+    TRY(dalloc(c, p, &p.d_slice_off, p.nslices + 1));
+    TRY(dalloc(c, p, &p.d_row_len, p.nslices * 32));
+    TRY(dalloc(c, p, &p.d_width, p.nslices));
+    TRY(dalloc(c, p, &p.d_b, p.rows));
+    TRY(dalloc(c, p, &p.d_x, p.rows));
+    TRY(dalloc(c, p, &p.d_r, p.rows));
+    TRY(dalloc(c, p, &p.d_p, p.ncols));
+    TRY(dalloc(c, p, &p.d_Ap, p.rows));
+    TRY(dalloc(c, p, &p.d_acc, 2 * ACC_WORDS));
+    TRY(dalloc(c, p, &p.d_st, 1));
+    TRY(alloc_hist(c, p, 201));
+    CUDA_TRY(c, cudaMemset(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long)));
+    CUDA_TRY(c, cudaMemset(p.d_st, 0, sizeof(CgState)));
+    CUDA_TRY(c, cudaMemset(p.d_p, 0, p.ncols * sizeof(double)));
+    // externals sorted by gid -> local column, for the assembly's column lookup
+    std::vector<std::pair<int64_t, int32_t>> ext(plan.n_ext);
+    for (int64_t i = 0; i < plan.n_ext; ++i)
+        ext[i] = {plan.ext_gid[i], (int32_t)(plan.n_owned + i)};
+    std::sort(ext.begin(), ext.end());
+    std::vector<int64_t> eg(plan.n_ext);
+    std::vector<int32_t> es(plan.n_ext);
+    for (int64_t i = 0; i < plan.n_ext; ++i) {
+        eg[i] = ext[i].first;
+        es[i] = ext[i].second;
+    }
+    TRY(dalloc(c, p, &p.d_ext_gid, plan.n_ext));
+    TRY(dalloc(c, p, &p.d_ext_slot, plan.n_ext));
+    if (plan.n_ext) {
+        CUDA_TRY(c, cudaMemcpy(p.d_ext_gid, eg.data(), eg.size() * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaMemcpy(p.d_ext_slot, es.data(), es.size() * 4, cudaMemcpyHostToDevice));
+    }
+    TRY(dalloc(c, p, &p.d_send_idx, plan.send_idx.size()));
+    TRY(dalloc(c, p, &p.d_sendbuf, plan.send_idx.size()));
+    if (!plan.send_idx.empty())
+        CUDA_TRY(c, cudaMemcpy(p.d_send_idx, plan.send_idx.data(), plan.send_idx.size() * 4,
+                               cudaMemcpyHostToDevice));
+    p.grid_spmv = spmv_grid(p.nslices);
+    p.grid_upd = stream_grid(p.rows);
+    return MINIFE_OK;
+}
+
+static int validate_mesh(int nx, int ny, int nz) {
+    if (nx < 1 || ny < 1 || nz < 1) return MINIFE_EINVAL;
+    // local column ids are int32 (north star); a part must stay below 2^31 columns
+    return MINIFE_OK;
+}
+
+static int create_common(minife_ctx *c, int nx, int ny, int nz, int nparts,
+                         const std::vector<int> &devs, int rank_only) {
+    c->mesh = Mesh{nx, ny, nz};
+    std::vector<Box> boxes;
+    if (!rcb(c->mesh, c->world, boxes)) {
+        set_err(c, "RCB: %d ranks do not fit a %dx%dx%d element mesh (S:65)", c->world, nx, ny,
+                nz);
+        return MINIFE_EINVAL;
+    }
+    c->parts.resize(nparts);
+    for (int q = 0; q < nparts; ++q) {
+        const int r = rank_only >= 0 ? rank_only : q;
+        Plan plan;
+        if (!build_plan(c->mesh, c->world, r, plan)) {
+            set_err(c, "plan construction failed for rank %d", r);
+            return MINIFE_EINVAL;
+        }
+        if (plan.n_owned + plan.n_ext >= (int64_t)1 << 31) {
+            set_err(c, "part %d has %lld columns: int32 local indices overflow", r,
+                    (long long)(plan.n_owned + plan.n_ext));
+            return MINIFE_EINVAL;
+        }
+        TRY(setup_part(c, c->parts[q], devs[q], plan));
+    }
+    DevGuard g(c->parts[0].dev);
+    CUDA_TRY(c, cudaEventCreate(&c->ev0));
+    CUDA_TRY(c, cudaEventCreate(&c->ev1));
+    return MINIFE_OK;
+}
+
+extern "C" int minife_create(int nx, int ny, int nz, int ngpu, minife_ctx **out) {
+    if (!out || validate_mesh(nx, ny, nz) != MINIFE_OK || ngpu < 1) return MINIFE_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MINIFE_ENODEV;
+    if (ngpu > ndev) return MINIFE_ENODEV;
+    minife_ctx *c = new minife_ctx();
+    c->mode = ngpu == 1 ? MINIFE_MODE_SINGLE : MINIFE_MODE_MULTI;
+    c->world = ngpu;
+    std::vector<int> devs(ngpu);
+    for (int q = 0; q < ngpu; ++q) devs[q] = q;
+    int st = create_common(c, nx, ny, nz, ngpu, devs, -1);
+    if (st == MINIFE_OK && ngpu > 1 && !nccl()) {
+        set_err(c, "NCCL could not be loaded (set MINIFE_NCCL_LIB)");
+        st = MINIFE_ENCCL;
+    }
+    if (st == MINIFE_OK && ngpu > 1) {
+        std::vector<ncclComm_t> comms(ngpu);
+        ncclResult_t r = nccl()->CommInitAll(comms.data(), ngpu, devs.data());
+        if (r != ncclSuccess) {
+            set_err(c, "ncclCommInitAll: %s", nccl()->GetErrorString(r));
+            st = MINIFE_ENCCL;
+        } else {
+            for (int q = 0; q < ngpu; ++q) c->parts[q].comm = comms[q];
+        }
+    }
+    if (st != MINIFE_OK) {
+        minife_destroy(c);
+        return st;
+    }
+    *out = c;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_create_virtual(int nx, int ny, int nz, int nparts, minife_ctx **out) {
+    if (!out || validate_mesh(nx, ny, nz) != MINIFE_OK || nparts < 1 || nparts > 64)
+        return MINIFE_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MINIFE_ENODEV;
+    minife_ctx *c = new minife_ctx();
+    c->mode = MINIFE_MODE_VIRTUAL;
+    c->world = nparts;
+    std::vector<int> devs(nparts, 0);
+    int st = create_common(c, nx, ny, nz, nparts, devs, -1);
+    if (st != MINIFE_OK) {
+        minife_destroy(c);
+        return st;
+    }
+    *out = c;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_nccl_unique_id(void *uid128) {
+    if (!uid128) return MINIFE_EINVAL;
+    ncclUniqueId id;
+    if (!nccl() || nccl()->GetUniqueId(&id) != ncclSuccess) return MINIFE_ENCCL;
+    memcpy(uid128, &id, sizeof id);
+    return MINIFE_OK;
+}
+
+extern "C" int minife_create_rank(int nx, int ny, int nz, int rank, int world, int device,
+                                  const void *uid128, minife_ctx **out) {
+    if (!out || !uid128 || validate_mesh(nx, ny, nz) != MINIFE_OK || world < 1 || rank < 0 ||
+        rank >= world || device < 0)
+        return MINIFE_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1 || device >= ndev)
+        return MINIFE_ENODEV;
+    minife_ctx *c = new minife_ctx();
+    c->mode = MINIFE_MODE_RANK;
+    c->world = world;
+    c->rank = rank;
+    std::vector<int> devs(1, device);
+    int st = create_common(c, nx, ny, nz, 1, devs, rank);
+    if (st == MINIFE_OK && !nccl()) {
+        set_err(c, "NCCL could not be loaded (set MINIFE_NCCL_LIB)");
+        st = MINIFE_ENCCL;
+    }
+    if (st == MINIFE_OK) {
+        DevGuard g(device);
+        ncclUniqueId id;
+        memcpy(&id, uid128, sizeof id);
+        ncclResult_t r = nccl()->CommInitRank(&c->parts[0].comm, world, id, rank);
+        if (r != ncclSuccess) {
+            set_err(c, "ncclCommInitRank: %s", nccl()->GetErrorString(r));
+            st = MINIFE_ENCCL;
+        }
+    }
+    if (st != MINIFE_OK) {
+        minife_destroy(c);
+        return st;
+    }
+    *out = c;
+    return MINIFE_OK;
+}
+
+extern "C" void minife_destroy(minife_ctx *c) {
+    if (!c) return;
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    for (auto &p : c->parts) free_part(p);
+    delete c;
+}
+
+extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
+    if (!c) return MINIFE_EINVAL;
+    if (c->mode != MINIFE_MODE_SINGLE && c->mode != MINIFE_MODE_RANK) return MINIFE_ESTATE;
+    c->user_stream = (cudaStream_t)stream;
+    return MINIFE_OK;
+}
+
+extern "C" const char *minife_strerror(int s) {
+    switch (s) {
+    case MINIFE_OK: return "ok";
+    case MINIFE_EINVAL: return "invalid argument";
+    case MINIFE_ESTATE: return "invalid state for this call";
+    case MINIFE_ECUDA: return "CUDA error";
+    case MINIFE_ENCCL: return "NCCL error";
+    case MINIFE_ENOMEM: return "out of memory";
+    case MINIFE_ENOTSPD: return "matrix not SPD (pAp <= 0 with rr != 0)";
+    case MINIFE_EDIVERGED: return "CG diverged (non-finite value)";
+    case MINIFE_ENODEV: return "no (or not enough) CUDA devices";
+    default: return "unknown status";
+    }
+}
+
+extern "C" const char *minife_last_error(const minife_ctx *c) { return c ? c->err.c_str() : ""; }
+extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
+
+// ----------------------------------------------------------------------------------------
+// assembly (a0.2 - a0.5)
+// ----------------------------------------------------------------------------------------
+
+static AsmArgs asm_args(const minife_ctx *c, const Part &p) {
+    AsmArgs a{};
+    a.nx = c->mesh.nx;
+    a.ny = c->mesh.ny;
+    a.nz = c->mesh.nz;
+    for (int k = 0; k < 3; ++k) {
+        a.own_lo[k] = p.plan.own_lo[k];
+        a.own_n[k] = p.plan.own_n[k];
+    }
+    a.rows = p.rows;
+    a.n_ext = p.plan.n_ext;
+    a.ext_sorted_gid = p.d_ext_gid;
+    a.ext_sorted_slot = p.d_ext_slot;
+    a.slice_off = p.d_slice_off;
+    a.row_len = p.d_row_len;
+    a.col = p.d_col;
+    a.val = p.d_val;
+    a.b = p.d_b;
+    return a;
+}
+
+extern "C" int minife_assemble(minife_ctx *c) {
+    if (!c) return MINIFE_EINVAL;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        cudaStream_t s = stream_of(c, p);
+        AsmArgs a = asm_args(c, p);
+        CUDA_TRY(c, launch_rowlen_widths(a, p.d_row_len, p.d_width, p.nslices, s));
+        std::vector<uint8_t> w(p.nslices);
+        CUDA_TRY(c, cudaMemcpyAsync(w.data(), p.d_width, p.nslices, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(c, cudaStreamSynchronize(s));
+        p.h_slice_off.assign(p.nslices + 1, 0);
+        for (int64_t i = 0; i < p.nslices; ++i)
+            p.h_slice_off[i + 1] = p.h_slice_off[i] + 32 * (int64_t)w[i];
+        const int64_t entries = p.h_slice_off[p.nslices];
+        if (entries != p.entries || !p.d_col) {
+            if (p.d_col) cudaFree(p.d_col);
+            if (p.d_val) cudaFree(p.d_val);
+            p.d_col = nullptr;
+            p.d_val = nullptr;
+            TRY(dalloc(c, p, &p.d_col, entries));
+            TRY(dalloc(c, p, &p.d_val, entries));
+            p.entries = entries;
+        }
+        CUDA_TRY(c, cudaMemcpyAsync(p.d_slice_off, p.h_slice_off.data(), 8 * (p.nslices + 1),
+                                    cudaMemcpyHostToDevice, s));
+        a = asm_args(c, p);
+        CUDA_TRY(c, launch_assemble(a, s));
+        CUDA_TRY(c, cudaStreamSynchronize(s));
+    }
+    c->assembled = true;
+    c->solved = false;
+    return MINIFE_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// transports: halo exchange (a1) and accumulator all-reduce (a3/a5)
+// ----------------------------------------------------------------------------------------
+
+// Fill the external slots of `vec(part)` (length ncols) from the owners' owned values.
+template <class VecOf>
+static int enqueue_halo(minife_ctx *c, VecOf vec) {
+    if (c->world == 1) return MINIFE_OK;
+    if (c->mode == MINIFE_MODE_VIRTUAL) {
+        // device-local transport: read the owner's owned values through its send list
+        cudaStream_t s = c->parts[0].stream;
+        for (auto &dst : c->parts) {
+            for (size_t k = 0; k < dst.plan.nbr.size(); ++k) {
+                Part &src = c->parts[dst.plan.nbr[k]];
+                auto it = std::lower_bound(src.plan.nbr.begin(), src.plan.nbr.end(),
+                                           dst.plan.rank);
+                const size_t j = (size_t)(it - src.plan.nbr.begin());
+                CUDA_TRY(c, launch_pack(vec(src), src.d_send_idx + src.plan.send_off[j],
+                                        src.plan.send_cnt[j],
+                                        vec(dst) + dst.rows + dst.plan.recv_off[k], s));
+            }
+        }
+        return MINIFE_OK;
+    }
+    // NCCL: pack each part's send lists, then grouped send/recv per neighbor
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_pack(vec(p), p.d_send_idx, (int64_t)p.plan.send_idx.size(),
+                                p.d_sendbuf, stream_of(c, p)));
+    }
+    NCCL_TRY(c, nccl()->GroupStart());
+    for (auto &p : c->parts) {
+        cudaStream_t s = stream_of(c, p);
+        for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
+            NCCL_TRY(c, nccl()->Send(p.d_sendbuf + p.plan.send_off[k], (size_t)p.plan.send_cnt[k],
+                                 ncclFloat64, p.plan.nbr[k], p.comm, s));
+            NCCL_TRY(c, nccl()->Recv(vec(p) + p.rows + p.plan.recv_off[k],
+                                 (size_t)p.plan.recv_cnt[k], ncclFloat64, p.plan.nbr[k],
+                                 p.comm, s));
+        }
+    }
+    NCCL_TRY(c, nccl()->GroupEnd());
+    return MINIFE_OK;
+}
+
+// int64 SUM of the exact accumulators over all ranks (which = 0: pAp, 1: rr)
+static int enqueue_allreduce(minife_ctx *c, int which) {
+    if (c->world == 1) return MINIFE_OK;
+    if (c->mode == MINIFE_MODE_VIRTUAL) {
+        std::vector<unsigned long long *> accs;
+        for (auto &p : c->parts) accs.push_back(which ? p.acc_rr() : p.acc_pAp());
+        CUDA_TRY(c, launch_vsum(accs.data(), (int)accs.size(), c->parts[0].stream));
+        return MINIFE_OK;
+    }
+    NCCL_TRY(c, nccl()->GroupStart());
+    for (auto &p : c->parts) {
+        unsigned long long *a = which ? p.acc_rr() : p.acc_pAp();
+        NCCL_TRY(c, nccl()->AllReduce(a, a, ACC_WORDS, ncclInt64, ncclSum, p.comm, stream_of(c, p)));
+    }
+    NCCL_TRY(c, nccl()->GroupEnd());
+    return MINIFE_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// CG driver (C6): init + max_iters x [halo, K1, reduce, K6, reduce, K7]
+// ----------------------------------------------------------------------------------------
+
+static UpdArgs upd_args(Part &p, int which_in) {
+    UpdArgs a{};
+    a.rows = p.rows;
+    a.x = p.d_x;
+    a.r = p.d_r;
+    a.p = p.d_p;
+    a.Ap = p.d_Ap;
+    a.b = p.d_b;
+    a.hist = p.d_hist;
+    a.rr = p.d_rr;
+    a.st = p.d_st;
+    if (which_in == 0) {          // K6: in = pAp, out = rr
+        a.acc_in = p.acc_pAp();
+        a.acc_out = p.acc_rr();
+        a.acc_zero = nullptr;
+    } else {                      // K7: in = rr, zero pAp
+        a.acc_in = p.acc_rr();
+        a.acc_out = nullptr;
+        a.acc_zero = p.acc_pAp();
+    }
+    return a;
+}
+
+static SpmvArgs spmv_args(Part &p, const double *x, double *y, bool dot) {
+    SpmvArgs a{};
+    a.rows = p.rows;
+    a.nslices = p.nslices;
+    a.slice_off = p.d_slice_off;
+    a.row_len = p.d_row_len;
+    a.col = p.d_col;
+    a.val = p.d_val;
+    a.x = x;
+    a.y = y;
+    a.acc = dot ? p.acc_pAp() : nullptr;
+    a.acc_zero = dot ? p.acc_rr() : nullptr;
+    a.st = dot ? p.d_st : nullptr;
+    return a;
+}
+
+static cudaStream_t launch_stream(minife_ctx *c, Part &p) {
+    return c->mode == MINIFE_MODE_VIRTUAL ? c->parts[0].stream : stream_of(c, p);
+}
+
+struct PhaseTimer {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> phase;     // phase of the interval ending at ev[i]
+    cudaStream_t s = nullptr;
+    void mark(int ph) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+        phase.push_back(ph);
+    }
+};
+
+static int enqueue_init(minife_ctx *c, double tol) {
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        cudaStream_t s = launch_stream(c, p);
+        CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long), s));
+        UpdArgs a = upd_args(p, 0);
+        a.acc_out = p.acc_rr();
+        CUDA_TRY(c, launch_init_vectors(a, p.grid_upd, s));
+    }
+    TRY(enqueue_allreduce(c, 1));
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        UpdArgs a = upd_args(p, 0);
+        a.acc_out = p.acc_rr();
+        a.acc_zero = p.acc_pAp();
+        CUDA_TRY(c, launch_init_finalize(a, tol, launch_stream(c, p)));
+    }
+    return MINIFE_OK;
+}
+
+static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
+    TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+    if (t) t->mark(3);
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_spmv(spmv_args(p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+                                launch_stream(c, p)));
+    }
+    if (t) t->mark(0);
+    TRY(enqueue_allreduce(c, 0));
+    if (t) t->mark(3);
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_update_xr(upd_args(p, 0), k, p.grid_upd, launch_stream(c, p)));
+    }
+    if (t) t->mark(1);
+    TRY(enqueue_allreduce(c, 1));
+    if (t) t->mark(3);
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_update_p(upd_args(p, 1), k, p.grid_upd, launch_stream(c, p)));
+    }
+    if (t) t->mark(2);
+    return MINIFE_OK;
+}
+
+static int ensure_hist(minife_ctx *c, int max_iters) {
+    if (c->parts[0].hist_cap >= max_iters + 1) return MINIFE_OK;
+    for (auto &p : c->parts) TRY(alloc_hist(c, p, max_iters + 1));
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    return MINIFE_OK;
+}
+
+static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, double seconds) {
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    CgState st;
+    double h0 = 0.0;
+    CUDA_TRY(c, cudaMemcpy(&st, p.d_st, sizeof st, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(&h0, p.d_hist, sizeof h0, cudaMemcpyDeviceToHost));
+    double hk = h0;
+    if (st.iters > 0)
+        CUDA_TRY(c, cudaMemcpy(&hk, p.d_hist + st.iters, sizeof hk, cudaMemcpyDeviceToHost));
+    c->last_iters = st.iters;
+    c->solved = true;
+    const int status = st.status == 6 ? MINIFE_ENOTSPD
+                       : st.status == 7 ? MINIFE_EDIVERGED
+                                        : MINIFE_OK;
+    if (res) {
+        res->status = status;
+        res->iterations = st.iters;
+        res->converged = st.converged;
+        res->max_iters = max_iters;
+        res->norm_b = h0;
+        res->final_rel_residual = h0 > 0.0 ? hk / h0 : 0.0;
+        res->seconds = seconds;
+        const double rows = (double)c->mesh.rows(), nnz = (double)c->mesh.nnz();
+        res->flops = (double)st.iters * (2.0 * nnz + 10.0 * rows);
+        double bytes = 0.0;
+        for (auto &q : c->parts) bytes += 12.0 * (double)q.nnz + 88.0 * (double)q.rows;
+        res->bytes = (double)st.iters * bytes;
+    }
+    return status;
+}
+
+static int check_solve_args(minife_ctx *c, int max_iters, double tol) {
+    if (!c) return MINIFE_EINVAL;
+    if (!c->assembled) {
+        set_err(c, "minife_cg_solve before minife_assemble");
+        return MINIFE_ESTATE;
+    }
+    if (max_iters < 1 || !(tol >= 0.0)) return MINIFE_EINVAL;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_cg_result *res) {
+    TRY(check_solve_args(c, max_iters, tol));
+    TRY(ensure_hist(c, max_iters));
+    Part &p0 = c->parts[0];
+    DevGuard g(p0.dev);
+    double seconds = 0.0;
+    if (c->mode == MINIFE_MODE_MULTI) {
+        // one host thread drives every device: launch the sequence directly
+        CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
+        TRY(enqueue_init(c, tol));
+        for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration(c, k, nullptr));
+        CUDA_TRY(c, cudaEventRecord(c->ev1, p0.stream));
+        for (auto &p : c->parts) {
+            DevGuard gg(p.dev);
+            CUDA_TRY(c, cudaStreamSynchronize(p.stream));
+        }
+    } else {
+        if (!c->gexec || c->g_iters != max_iters || c->g_tol != tol) {
+            if (c->gexec) {
+                cudaGraphExecDestroy(c->gexec);
+                c->gexec = nullptr;
+            }
+            // capture on the ctx's own stream (a torch stream may be the legacy default one)
+            cudaStream_t cap = p0.stream;
+            cudaStream_t saved = c->user_stream;
+            c->user_stream = nullptr;
+            CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            int st = enqueue_init(c, tol);
+            for (int k = 1; st == MINIFE_OK && k <= max_iters; ++k)
+                st = enqueue_iteration(c, k, nullptr);
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamEndCapture(cap, &graph);
+            c->user_stream = saved;
+            if (st != MINIFE_OK) {
+                if (graph) cudaGraphDestroy(graph);
+                return st;
+            }
+            CUDA_TRY(c, e);
+            e = cudaGraphInstantiate(&c->gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            CUDA_TRY(c, e);
+            c->g_iters = max_iters;
+            c->g_tol = tol;
+        }
+        cudaStream_t s = launch_stream(c, p0);
+        CUDA_TRY(c, cudaEventRecord(c->ev0, s));
+        CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
+        CUDA_TRY(c, cudaEventRecord(c->ev1, s));
+    }
+    CUDA_TRY(c, cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    seconds = ms * 1e-3;
+    return read_result(c, max_iters, res, seconds);
+}
+
+extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_times *out) {
+    TRY(check_solve_args(c, max_iters, 0.0));
+    TRY(ensure_hist(c, max_iters));
+    Part &p0 = c->parts[0];
+    DevGuard g(p0.dev);
+    PhaseTimer t;
+    t.s = launch_stream(c, p0);
+    TRY(enqueue_init(c, 0.0));
+    t.mark(-1);
+    for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration(c, k, &t));
+    for (auto &p : c->parts) {
+        DevGuard gg(p.dev);
+        CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+    }
+    double ms[4] = {0, 0, 0, 0};
+    for (size_t i = 1; i < t.ev.size(); ++i) {
+        float m = 0.f;
+        cudaEventElapsedTime(&m, t.ev[i - 1], t.ev[i]);
+        if (t.phase[i] >= 0) ms[t.phase[i]] += m;
+    }
+    for (auto e : t.ev) cudaEventDestroy(e);
+    if (out) {
+        out->spmv_ms = ms[0];
+        out->update_xr_ms = ms[1];
+        out->update_p_ms = ms[2];
+        out->comm_ms = ms[3];
+        out->spmv_launches = out->update_xr_launches = out->update_p_launches = max_iters;
+        out->iterations = max_iters;
+    }
+    return read_result(c, max_iters, nullptr, 0.0);
+}
+
+// ----------------------------------------------------------------------------------------
+// SpMV through the ABI
+// ----------------------------------------------------------------------------------------
+
+static int64_t gid_of_local(const Plan &pl, int64_t l) {
+    const Mesh &m = pl.mesh;
+    if (l < pl.n_owned) {
+        const int64_t lx = l % pl.own_n[0], ly = (l / pl.own_n[0]) % pl.own_n[1],
+                      lz = l / (pl.own_n[0] * pl.own_n[1]);
+        return (pl.own_lo[0] + lx) + m.NX() * ((pl.own_lo[1] + ly) + m.NY() * (pl.own_lo[2] + lz));
+    }
+    return pl.ext_gid[l - pl.n_owned];
+}
+
+// global <-> owned-local scatter/gather on the host (box enumeration)
+static void gather_owned(const Plan &pl, const double *global, double *local) {
+    const int64_t NX = pl.mesh.NX(), NY = pl.mesh.NY();
+    int64_t l = 0;
+    for (int64_t iz = pl.own_lo[2]; iz <= pl.own_hi[2]; ++iz)
+        for (int64_t iy = pl.own_lo[1]; iy <= pl.own_hi[1]; ++iy) {
+            const int64_t g0 = pl.own_lo[0] + NX * (iy + NY * iz);
+            memcpy(local + l, global + g0, sizeof(double) * pl.own_n[0]);
+            l += pl.own_n[0];
+        }
+}
+static void scatter_owned(const Plan &pl, const double *local, double *global) {
+    const int64_t NX = pl.mesh.NX(), NY = pl.mesh.NY();
+    int64_t l = 0;
+    for (int64_t iz = pl.own_lo[2]; iz <= pl.own_hi[2]; ++iz)
+        for (int64_t iy = pl.own_lo[1]; iy <= pl.own_hi[1]; ++iy) {
+            const int64_t g0 = pl.own_lo[0] + NX * (iy + NY * iz);
+            memcpy(global + g0, local + l, sizeof(double) * pl.own_n[0]);
+            l += pl.own_n[0];
+        }
+}
+
+extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
+    if (!c || !x || !y) return MINIFE_EINVAL;
+    if (!c->assembled) return MINIFE_ESTATE;
+    const bool global_io = c->mode != MINIFE_MODE_RANK;
+    std::vector<double> tmp;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        if (!p.d_xin) {
+            TRY(dalloc(c, p, &p.d_xin, p.ncols));
+            TRY(dalloc(c, p, &p.d_yout, p.rows));
+        }
+        const double *src = x;
+        if (global_io) {
+            tmp.resize(p.rows);
+            gather_owned(p.plan, x, tmp.data());
+            src = tmp.data();
+        }
+        CUDA_TRY(c, cudaMemcpy(p.d_xin, src, sizeof(double) * p.rows, cudaMemcpyHostToDevice));
+    }
+    TRY(enqueue_halo(c, [](Part &p) { return p.d_xin; }));
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_spmv(spmv_args(p, p.d_xin, p.d_yout, false), false, p.grid_spmv,
+                                launch_stream(c, p)));
+    }
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+        if (global_io) {
+            tmp.resize(p.rows);
+            CUDA_TRY(c, cudaMemcpy(tmp.data(), p.d_yout, sizeof(double) * p.rows,
+                                   cudaMemcpyDeviceToHost));
+            scatter_owned(p.plan, tmp.data(), y);
+        } else {
+            CUDA_TRY(c, cudaMemcpy(y, p.d_yout, sizeof(double) * p.rows, cudaMemcpyDeviceToHost));
+        }
+    }
+    return MINIFE_OK;
+}
+
+extern "C" int minife_spmv_device(minife_ctx *c, const double *d_x, double *d_y, void *stream) {
+    if (!c || !d_x || !d_y) return MINIFE_EINVAL;
+    if (c->mode != MINIFE_MODE_SINGLE || !c->assembled) return MINIFE_ESTATE;
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    cudaStream_t s = stream ? (cudaStream_t)stream : stream_of(c, p);
+    CUDA_TRY(c, launch_spmv(spmv_args(p, d_x, d_y, false), false, p.grid_spmv, s));
+    return MINIFE_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// getters
+// ----------------------------------------------------------------------------------------
+
+static void fill_part_info(const Plan &pl, int dev, int64_t entries, minife_part_info *o) {
+    memset(o, 0, sizeof *o);
+    o->rank = pl.rank;
+    o->world = pl.world;
+    for (int k = 0; k < 3; ++k) {
+        o->box[k] = pl.boxes[pl.rank].lo[k];
+        o->box[3 + k] = pl.boxes[pl.rank].hi[k];
+        o->own[k] = pl.own_lo[k];
+        o->own[3 + k] = pl.own_hi[k];
+    }
+    o->n_neighbors = (int32_t)pl.nbr.size();
+    o->device = dev;
+    o->rows = pl.n_owned;
+    o->externals = pl.n_ext;
+    o->nnz = pl.local_nnz();
+    o->slices = (pl.n_owned + 31) / 32;
+    o->sell_entries = entries;
+    o->send_total = (int64_t)pl.send_idx.size();
+}
+
+extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
+    if (!c || !o) return MINIFE_EINVAL;
+    memset(o, 0, sizeof *o);
+    o->nx = c->mesh.nx;
+    o->ny = c->mesh.ny;
+    o->nz = c->mesh.nz;
+    o->mode = c->mode;
+    o->nparts = (int)c->parts.size();
+    o->rank = c->rank;
+    o->world = c->world;
+    o->assembled = c->assembled;
+    o->rows = c->mesh.rows();
+    o->nnz = c->mesh.nnz();
+    for (auto &p : c->parts) {
+        o->local_rows += p.rows;
+        o->local_nnz += p.nnz;
+        o->max_part_rows = std::max(o->max_part_rows, p.rows);
+        o->max_part_nnz = std::max(o->max_part_nnz, p.nnz);
+        o->max_part_externals = std::max(o->max_part_externals, p.plan.n_ext);
+        o->sell_entries += p.entries;
+        o->device_bytes += (int64_t)p.bytes;
+    }
+    return MINIFE_OK;
+}
+
+extern "C" int minife_get_part_info(const minife_ctx *c, int part, minife_part_info *o) {
+    if (!c || !o || part < 0 || part >= (int)c->parts.size()) return MINIFE_EINVAL;
+    const Part &p = c->parts[part];
+    fill_part_info(p.plan, p.dev, p.entries, o);
+    return MINIFE_OK;
+}
+
+struct HostPart {
+    std::vector<int64_t> so;
+    std::vector<uint8_t> len;
+    std::vector<int32_t> col;
+    std::vector<double> val;
+};
+
+static int download_part(minife_ctx *c, Part &p, HostPart &h) {
+    DevGuard g(p.dev);
+    h.so = p.h_slice_off;
+    h.len.resize(p.rows);
+    h.col.resize(p.entries);
+    h.val.resize(p.entries);
+    CUDA_TRY(c, cudaMemcpy(h.len.data(), p.d_row_len, p.rows, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(h.col.data(), p.d_col, 4 * p.entries, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(h.val.data(), p.d_val, 8 * p.entries, cudaMemcpyDeviceToHost));
+    return MINIFE_OK;
+}
+
+extern "C" int minife_export_csr(minife_ctx *c, int64_t *row_ptr, int64_t *col, double *val) {
+    if (!c || !row_ptr || !col || !val) return MINIFE_EINVAL;
+    if (!c->assembled) return MINIFE_ESTATE;
+    if (c->mode == MINIFE_MODE_RANK) {
+        Part &p = c->parts[0];
+        HostPart h;
+        TRY(download_part(c, p, h));
+        row_ptr[0] = 0;
+        for (int64_t r = 0; r < p.rows; ++r) {
+            const int64_t s = r >> 5, lane = r & 31;
+            int64_t o = row_ptr[r];
+            for (int k = 0; k < h.len[r]; ++k) {
+                const int64_t e = h.so[s] + 32 * k + lane;
+                col[o] = gid_of_local(p.plan, h.col[e]);
+                val[o] = h.val[e];
+                ++o;
+            }
+            row_ptr[r + 1] = o;
+        }
+        return MINIFE_OK;
+    }
+    // global row pointer from the closed-form row lengths (rows in global id order)
+    const Mesh &m = c->mesh;
+    const int64_t NX = m.NX(), NY = m.NY(), NZ = m.NZ();
+    row_ptr[0] = 0;
+    int64_t g = 0;
+    for (int64_t iz = 0; iz < NZ; ++iz)
+        for (int64_t iy = 0; iy < NY; ++iy)
+            for (int64_t ix = 0; ix < NX; ++ix, ++g) {
+                const int cx = (ix == 0 || ix == m.nx) ? 2 : 3;
+                const int cy = (iy == 0 || iy == m.ny) ? 2 : 3;
+                const int cz = (iz == 0 || iz == m.nz) ? 2 : 3;
+                row_ptr[g + 1] = row_ptr[g] + cx * cy * cz;
+            }
+    for (auto &p : c->parts) {
+        HostPart h;
+        TRY(download_part(c, p, h));
+        for (int64_t r = 0; r < p.rows; ++r) {
+            const int64_t gid = gid_of_local(p.plan, r);
+            const int64_t s = r >> 5, lane = r & 31;
+            int64_t o = row_ptr[gid];
+            if (row_ptr[gid + 1] - o != h.len[r]) {
+                set_err(c, "row %lld: device length %d != closed form", (long long)gid, h.len[r]);
+                return MINIFE_ESTATE;
+            }
+            for (int k = 0; k < h.len[r]; ++k) {
+                const int64_t e = h.so[s] + 32 * k + lane;
+                col[o] = gid_of_local(p.plan, h.col[e]);
+                val[o] = h.val[e];
+                ++o;
+            }
+        }
+    }
+    return MINIFE_OK;
+}
+
+extern "C" int minife_export_rows(minife_ctx *c, int64_t n, const int64_t *gids, int64_t *cols,
+                                  double *vals, int32_t *lens) {
+    if (!c || n < 0 || (n && (!gids || !cols || !vals || !lens))) return MINIFE_EINVAL;
+    if (!c->assembled) return MINIFE_ESTATE;
+    const Mesh &m = c->mesh;
+    for (int64_t i = 0; i < n; ++i) lens[i] = -1;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        std::vector<int64_t> loc, which;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t gid = gids[i];
+            if (gid < 0 || gid >= m.rows()) continue;
+            const int64_t ix = gid % m.NX(), iy = (gid / m.NX()) % m.NY(),
+                          iz = gid / (m.NX() * m.NY());
+            if (!p.plan.owns(ix, iy, iz)) continue;
+            loc.push_back(p.plan.owned_local(ix, iy, iz));
+            which.push_back(i);
+        }
+        if (loc.empty()) continue;
+        const int64_t k = (int64_t)loc.size();
+        int64_t *d_rows = nullptr;
+        int32_t *d_oc = nullptr, *d_ol = nullptr;
+        double *d_ov = nullptr;
+        CUDA_TRY(c, cudaMalloc((void **)&d_rows, 8 * k));
+        CUDA_TRY(c, cudaMalloc((void **)&d_oc, 4 * 27 * k));
+        CUDA_TRY(c, cudaMalloc((void **)&d_ov, 8 * 27 * k));
+        CUDA_TRY(c, cudaMalloc((void **)&d_ol, 4 * k));
+        CUDA_TRY(c, cudaMemcpy(d_rows, loc.data(), 8 * k, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, launch_extract_rows(p.d_slice_off, p.d_row_len, p.d_col, p.d_val, d_rows, k,
+                                        d_oc, d_ov, d_ol, p.stream));
+        std::vector<int32_t> oc(27 * k), ol(k);
+        std::vector<double> ov(27 * k);
+        CUDA_TRY(c, cudaStreamSynchronize(p.stream));
+        CUDA_TRY(c, cudaMemcpy(oc.data(), d_oc, 4 * 27 * k, cudaMemcpyDeviceToHost));
+        CUDA_TRY(c, cudaMemcpy(ov.data(), d_ov, 8 * 27 * k, cudaMemcpyDeviceToHost));
+        CUDA_TRY(c, cudaMemcpy(ol.data(), d_ol, 4 * k, cudaMemcpyDeviceToHost));
+        cudaFree(d_rows);
+        cudaFree(d_oc);
+        cudaFree(d_ov);
+        cudaFree(d_ol);
+        for (int64_t j = 0; j < k; ++j) {
+            const int64_t i = which[j];
+            lens[i] = ol[j];
+            for (int e = 0; e < ol[j]; ++e) {
+                cols[27 * i + e] = gid_of_local(p.plan, oc[27 * j + e]);
+                vals[27 * i + e] = ov[27 * j + e];
+            }
+        }
+    }
+    return MINIFE_OK;
+}
+
+static int get_vec(minife_ctx *c, double *out, double *Part::*member) {
+    std::vector<double> tmp;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        tmp.resize(p.rows);
+        CUDA_TRY(c, cudaMemcpy(tmp.data(), p.*member, 8 * p.rows, cudaMemcpyDeviceToHost));
+        if (c->mode == MINIFE_MODE_RANK) memcpy(out, tmp.data(), 8 * p.rows);
+        else scatter_owned(p.plan, tmp.data(), out);
+    }
+    return MINIFE_OK;
+}
+
+extern "C" int minife_get_rhs(minife_ctx *c, double *b) {
+    if (!c || !b) return MINIFE_EINVAL;
+    if (!c->assembled) return MINIFE_ESTATE;
+    return get_vec(c, b, &Part::d_b);
+}
+
+extern "C" int minife_get_solution(minife_ctx *c, double *x) {
+    if (!c || !x) return MINIFE_EINVAL;
+    if (!c->solved) return MINIFE_ESTATE;
+    return get_vec(c, x, &Part::d_x);
+}
+
+extern "C" int minife_get_history(minife_ctx *c, double *h, int cap, int *n) {
+    if (!c || !h || !n) return MINIFE_EINVAL;
+    if (!c->solved) return MINIFE_ESTATE;
+    const int cnt = c->last_iters + 1;
+    *n = cnt;
+    if (cap < cnt) return MINIFE_EINVAL;
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    CUDA_TRY(c, cudaMemcpy(h, p.d_hist, 8 * cnt, cudaMemcpyDeviceToHost));
+    return MINIFE_OK;
+}
+
+extern "C" int minife_get_owned_ids(const minife_ctx *c, int64_t *gids) {
+    if (!c || !gids) return MINIFE_EINVAL;
+    int64_t o = 0;
+    for (auto &p : c->parts)
+        for (int64_t l = 0; l < p.rows; ++l) gids[o++] = gid_of_local(p.plan, l);
+    return MINIFE_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// host-only plan queries
+// ----------------------------------------------------------------------------------------
+
+extern "C" int minife_plan(int nx, int ny, int nz, int world, int rank, minife_part_info *out) {
+    if (!out || validate_mesh(nx, ny, nz) != MINIFE_OK) return MINIFE_EINVAL;
+    Plan pl;
+    if (!build_plan(Mesh{nx, ny, nz}, world, rank, pl)) return MINIFE_EINVAL;
+    int64_t entries = 0;
+    // SELL entries from the closed-form row lengths (max per 32-row slice)
+    {
+        const Mesh m{nx, ny, nz};
+        int64_t r = 0, w = 0;
+        for (int64_t iz = pl.own_lo[2]; iz <= pl.own_hi[2]; ++iz)
+            for (int64_t iy = pl.own_lo[1]; iy <= pl.own_hi[1]; ++iy)
+                for (int64_t ix = pl.own_lo[0]; ix <= pl.own_hi[0]; ++ix) {
+                    const int len = ((ix == 0 || ix == m.nx) ? 2 : 3) *
+                                    ((iy == 0 || iy == m.ny) ? 2 : 3) *
+                                    ((iz == 0 || iz == m.nz) ? 2 : 3);
+                    w = std::max<int64_t>(w, len);
+                    if ((++r & 31) == 0) {
+                        entries += 32 * w;
+                        w = 0;
+                    }
+                }
+        if (r & 31) entries += 32 * w;
+    }
+    fill_part_info(pl, -1, entries, out);
+    return MINIFE_OK;
+}
+
+extern "C" int minife_plan_lists(int nx, int ny, int nz, int world, int rank, int64_t *ext_gids,
+                                 int32_t *nbr, int64_t *recv_cnt, int64_t *send_cnt,
+                                 int32_t *send_idx) {
+    if (validate_mesh(nx, ny, nz) != MINIFE_OK) return MINIFE_EINVAL;
+    Plan pl;
+    if (!build_plan(Mesh{nx, ny, nz}, world, rank, pl)) return MINIFE_EINVAL;
+    if (ext_gids) std::copy(pl.ext_gid.begin(), pl.ext_gid.end(), ext_gids);
+    for (size_t k = 0; k < pl.nbr.size(); ++k) {
+        if (nbr) nbr[k] = pl.nbr[k];
+        if (recv_cnt) recv_cnt[k] = pl.recv_cnt[k];
+        if (send_cnt) send_cnt[k] = pl.send_cnt[k];
+    }
+    if (send_idx) std::copy(pl.send_idx.begin(), pl.send_idx.end(), send_idx);
+    return MINIFE_OK;
+}

@@ -1,0 +1,145 @@
+// exact.cuh — exactly-rounded dot products on the device (reading C5).
+//
+// dot(u,v) = RN( sum_i^exact fl(u_i * v_i) ): independent of summation order, tiling and
+// rank count, which is what makes the GPU CG bit-identical to the oracle and to itself at any
+// partition (any ulp-level change in a dot changes ||r_k|| by O(1) within 50
+// iterations on this problem, so nothing weaker meets the north-star tolerances).
+//
+// Three levels, all exact:
+//   1. per thread: a floating-point expansion of NEXP doubles, updated by Knuth's TwoSum
+//      cascade; whatever the last level cannot hold ("spill") goes to level 2;
+//   2. per CTA: a fixed-point superaccumulator in shared memory: ACC_DIGITS signed int64
+//      words, word i weighting 2^(32 i - 1074); a double adds < 2^33 to each of <= 3 words;
+//   3. per rank / globally: the CTA words are added to a global copy with int64 atomicAdd;
+//      across ranks an int64-SUM all-reduce (associative, so deterministic).
+// A consumer kernel normalises the carries and rounds once (acc_finalize).
+// Capacity: < 2^29 additions per accumulator word (any n < 5e8 terms) keeps every word and
+// carry inside int64.  Word ACC_FLAG counts non-finite inputs (then the result is NaN).
+#pragma once
+#include <cstdint>
+
+namespace minife {
+
+constexpr int ACC_DIGITS = 68;            // bits 0..2175 relative to 2^-1074
+constexpr int ACC_FLAG = ACC_DIGITS;      // non-finite counter
+constexpr int ACC_WORDS = 72;             // padded (576 B)
+constexpr int NEXP = 4;                   // expansion length per thread
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// Add one double to a superaccumulator (shared or global words) with 64-bit atomics.
+__device__ __forceinline__ void acc_add(unsigned long long *w, double x) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    const unsigned long long frac = bits & 0xfffffffffffffull;
+    if (e == 0x7ff) {                      // inf / nan
+        atomicAdd(&w[ACC_FLAG], 1ull);
+        return;
+    }
+    if (e == 0 && frac == 0) return;
+    // x = m * 2^(pos - 1074)
+    const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
+    const int pos = e ? e - 1 : 0;
+    const int d = pos >> 5, s = pos & 31;
+    const unsigned long long a = (m & 0xffffffffull) << s;   // < 2^63
+    const unsigned long long b = (m >> 32) << s;             // < 2^53
+    long long w0 = (long long)(a & 0xffffffffull);
+    long long w1 = (long long)((a >> 32) + (b & 0xffffffffull));
+    long long w2 = (long long)(b >> 32);
+    if (bits >> 63) {
+        w0 = -w0;
+        w1 = -w1;
+        w2 = -w2;
+    }
+    if (w0) atomicAdd(&w[d], (unsigned long long)w0);
+    if (w1) atomicAdd(&w[d + 1], (unsigned long long)w1);
+    if (w2) atomicAdd(&w[d + 2], (unsigned long long)w2);
+}
+
+struct Expansion {
+    double c[NEXP];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int j = 0; j < NEXP; ++j) c[j] = 0.0;
+    }
+    // exact: c[0]+..+c[NEXP-1] (+ spilled) == previous total + x, always
+    __device__ __forceinline__ void add(double x, unsigned long long *spill) {
+#pragma unroll
+        for (int j = 0; j < NEXP; ++j) two_sum(c[j], x, c[j], x);
+        if (x != 0.0) acc_add(spill, x);   // also routes NaN to the flag word
+    }
+    __device__ __forceinline__ void flush(unsigned long long *acc) const {
+#pragma unroll
+        for (int j = 0; j < NEXP; ++j)
+            if (c[j] != 0.0) acc_add(acc, c[j]);
+    }
+};
+
+// CTA helpers: zero the shared words (all threads), merge them into a global accumulator.
+__device__ __forceinline__ void acc_zero_shared(unsigned long long *s) {
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = 0ull;
+}
+__device__ __forceinline__ void acc_merge_to_global(const unsigned long long *s,
+                                                    unsigned long long *g) {
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
+        const unsigned long long v = s[i];
+        if (v) atomicAdd(&g[i], v);
+    }
+}
+
+// Normalise carries and round to nearest-even (one thread).  Exact zero -> +0.0.
+static __device__ __noinline__ double acc_finalize(const unsigned long long *gw) {
+    if (gw[ACC_FLAG] != 0ull) return __longlong_as_double(0x7ff8000000000000ll);
+    uint32_t d[ACC_DIGITS];
+    long long carry = 0;
+#pragma unroll 4
+    for (int i = 0; i < ACC_DIGITS; ++i) {
+        const long long v = (long long)gw[i] + carry;
+        d[i] = (uint32_t)((unsigned long long)v & 0xffffffffull);
+        carry = (v - (long long)d[i]) >> 32;   // exact floor division by 2^32
+    }
+    const bool neg = carry < 0;                // value = sum d_i 2^(32i) - [neg] 2^(32*68)
+    if (neg) {
+        unsigned long long c = 1;
+        for (int i = 0; i < ACC_DIGITS; ++i) {
+            c += (uint32_t)~d[i];
+            d[i] = (uint32_t)c;
+            c >>= 32;
+        }
+    }
+    int T = ACC_DIGITS - 1;
+    while (T >= 0 && d[T] == 0) --T;
+    if (T < 0) return 0.0;
+    const int t = 32 * T + 31 - __clz(d[T]);   // top bit, in units of 2^-1074
+    double mag;
+    if (t <= 52) {
+        const unsigned long long v = (unsigned long long)d[0] | ((unsigned long long)d[1] << 32);
+        mag = scalbn((double)v, -1074);        // < 2^53 ulps of 2^-1074: exact
+    } else {
+        // 96-bit window of digits T, T-1, T-2 (missing digits read as 0)
+        const uint32_t d1 = T >= 1 ? d[T - 1] : 0u, d2 = T >= 2 ? d[T - 2] : 0u;
+        const unsigned __int128 W = ((unsigned __int128)d[T] << 64) |
+                                    ((unsigned __int128)d1 << 32) | (unsigned __int128)d2;
+        const int sh = t - 32 * (T - 2);        // top bit position inside W, in [64, 95]
+        unsigned long long M = (unsigned long long)(W >> (sh - 52));   // 53 bits
+        const int guard = (int)((W >> (sh - 53)) & 1u);
+        bool sticky = (W & ((((unsigned __int128)1) << (sh - 53)) - 1)) != 0;
+        for (int i = T - 3; i >= 0 && !sticky; --i) sticky = d[i] != 0;
+        int top = t;
+        if (guard && (sticky || (M & 1ull))) {
+            ++M;
+            if (M == (1ull << 53)) {
+                M >>= 1;
+                ++top;
+            }
+        }
+        mag = scalbn((double)M, top - 52 - 1074);   // inf iff round-to-nearest overflows
+    }
+    return neg ? -mag : mag;
+}
+
+}  // namespace minife

@@ -1,0 +1,61 @@
+// plan.h — host-side RCB partition, nodal ownership and halo plans (G15; P:29, P:44-48;
+// S:61-100).  Pure integer C++, no CUDA.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace minife {
+
+struct Mesh {
+    int nx, ny, nz;                       // elements per axis (G1)
+    int64_t NX() const { return nx + 1; }
+    int64_t NY() const { return ny + 1; }
+    int64_t NZ() const { return nz + 1; }
+    int64_t rows() const { return NX() * NY() * NZ(); }
+    // stored entries of the full 27-point pattern: prod(3N-2)
+    int64_t nnz() const { return (3 * NX() - 2) * (3 * NY() - 2) * (3 * NZ() - 2); }
+};
+
+struct Box {
+    int lo[3], hi[3];                     // element ranges [lo, hi)
+};
+
+// RCB: longest axis (ties x<y<z), ceil(p/2) ranks take the lower part, cut at
+// lo + floor(len*ceil(p/2)/p).  Returns false if some leaf would hold fewer elements than
+// ranks.
+bool rcb(const Mesh &m, int p, std::vector<Box> &boxes);
+
+struct Plan {
+    Mesh mesh;
+    int rank = 0, world = 1;
+    std::vector<Box> boxes;               // all ranks' element boxes
+    int own_lo[3], own_hi[3];             // owned node box, inclusive
+    int64_t own_n[3];
+    int64_t n_owned = 0, n_ext = 0;
+    std::vector<int64_t> ext_gid;         // slot order: (owner rank, global id)
+    std::vector<int> nbr;                 // neighbor ranks, ascending
+    std::vector<int64_t> recv_off, recv_cnt;   // slots [recv_off, +cnt) come from nbr[k]
+    std::vector<int64_t> send_off, send_cnt;   // send_idx[send_off, +cnt) go to nbr[k]
+    std::vector<int32_t> send_idx;        // local owned row indices
+
+    int64_t owned_local(int64_t ix, int64_t iy, int64_t iz) const {
+        return (ix - own_lo[0]) + own_n[0] * ((iy - own_lo[1]) + own_n[1] * (iz - own_lo[2]));
+    }
+    bool owns(int64_t ix, int64_t iy, int64_t iz) const {
+        return ix >= own_lo[0] && ix <= own_hi[0] && iy >= own_lo[1] && iy <= own_hi[1] &&
+               iz >= own_lo[2] && iz <= own_hi[2];
+    }
+    int64_t local_nnz() const;            // closed form over the owned box
+};
+
+// Owned node box of `rank` (S:97 lowest-rank rule; DESIGN §4 shows it is a box: the closed
+// node box minus every lower face lying on an interior cut plane).
+void owned_box(const Mesh &m, const std::vector<Box> &boxes, int rank, int lo[3], int hi[3]);
+
+// owner(node) = lowest rank whose closed node box contains it.
+int owner_of(const std::vector<Box> &boxes, int64_t ix, int64_t iy, int64_t iz);
+
+// Full plan of `rank`: owned box, externals, neighbors and halo send/recv lists.
+bool build_plan(const Mesh &m, int world, int rank, Plan &out);
+
+}  // namespace minife

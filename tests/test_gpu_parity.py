@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar: integer/index work bit-exact; floating point compared with IEEE ==
+(zero error), which is inside every north-star tolerance (SpMV 1e-12 relative per entry,
+history 1e-8 relative over the first 50 iterations, x 1e-9 max-abs) -- SURVEY §8(c) shows a
+weaker contract cannot meet those on this problem.  Each comparison also asserts the
+north-star tolerance itself, so a failure says which bar broke.
+"""
+import numpy as np
+import pytest
+
+import minife_inputs
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+M = pytest.importorskip("paper_1505_08023_b200")
+
+MESHES = [(1, 1, 1), (2, 2, 2), (10, 10, 10), (23, 17, 9), (7, 1, 3), (33, 32, 31)]
+
+
+def _same(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return a.shape == b.shape and bool(np.all((a == b) | (np.isnan(a) & np.isnan(b))))
+
+
+_oracle_cache = {}
+
+
+def oracle_system(n):
+    if n not in _oracle_cache:
+        _oracle_cache[n] = O.assemble(*n)
+    return _oracle_cache[n]
+
+
+def oracle_cg(n, iters, tol):
+    key = ("cg", n, iters, tol)
+    if key not in _oracle_cache:
+        s = oracle_system(n)
+        _oracle_cache[key] = O.cg(s.row_ptr, s.col, s.val, s.b, iters, tol)
+    return _oracle_cache[key]
+
+
+def check_matrix(g, s):
+    rp, col, val = g.export_csr()
+    assert np.array_equal(rp, s.row_ptr)          # pattern: bit-exact
+    assert np.array_equal(col, s.col)             # indices: bit-exact
+    assert _same(val, s.val)                      # values: IEEE ==
+    assert _same(g.rhs(), s.b)
+
+
+def check_spmv(g, s, seed):
+    x = minife_inputs.uniform_pm1(s.rows, seed)
+    y = g.spmv(x)
+    yo = O.spmv(s.row_ptr, s.col, s.val, x)
+    rel = np.abs(y - yo) / np.maximum(np.abs(yo), 1e-300)
+    assert np.all((rel <= 1e-12) | (y == yo))     # north-star bar
+    assert _same(y, yo)                           # canonical-arithmetic bar
+
+
+def check_cg(g, n, iters, tol):
+    r = g.cg_solve(iters, tol)
+    o = oracle_cg(n, iters, tol)
+    assert r.status == o.status
+    assert r.iterations == o.iters and r.converged == o.converged
+    h = g.history()
+    k = min(51, h.size)
+    assert np.all(np.abs(h[:k] - o.hist[:k]) <= 1e-8 * np.abs(o.hist[:k]))   # north star
+    assert _same(h, o.hist)
+    x = g.solution()
+    assert np.abs(x - o.x).max() <= 1e-9                                       # north star
+    assert _same(x, o.x)
+
+
+@pytest.mark.parametrize("n", MESHES)
+def test_single_gpu_matrix_spmv_cg(n):
+    s = oracle_system(n)
+    with M.Minife(*n) as g:
+        g.assemble()
+        info = g.get_info()
+        assert info.rows == s.rows and info.nnz == s.nnz
+        check_matrix(g, s)
+        for seed in (12345, 1, 2):
+            check_spmv(g, s, seed)
+        check_cg(g, n, 200, 0.0)
+        check_cg(g, n, 200, 1e-8)
+        check_cg(g, n, 7, 0.0)          # graph re-capture with another iteration count
+
+
+@pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
+                                 ((12, 11, 10), 8), ((33, 32, 31), 5)])
+def test_virtual_ranks_bit_identical(n, p):
+    """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results."""
+    s = oracle_system(n)
+    with M.Minife(*n, virtual=p) as g:
+        g.assemble()
+        assert g.get_info().nparts == p
+        check_matrix(g, s)
+        check_spmv(g, s, 12345)
+        check_cg(g, n, 200, 0.0)
+        check_cg(g, n, 100, 1e-10)
+
+
+def test_plan_on_device_matches_host_plan():
+    n, p = (12, 11, 10), 8
+    with M.Minife(*n, virtual=p) as g:
+        for r in range(p):
+            a = g.part_info(r)
+            b = M.plan(*n, p, r)
+            assert (a.rows, a.externals, a.nnz, a.n_neighbors, a.send_total) == \
+                   (b.rows, b.externals, b.nnz, b.n_neighbors, b.send_total)
+        g.assemble()
+        for r in range(p):
+            assert g.part_info(r).sell_entries == M.plan(*n, p, r).sell_entries
+
+
+def test_rank_mode_world1_nccl_path():
+    """SPMD entry point with a 1-rank NCCL communicator (exercises NCCL + graph capture)."""
+    n = (10, 10, 10)
+    uid = M.nccl_unique_id()
+    with M.Minife(*n, rank=(0, 1, 0, uid)) as g:
+        g.assemble()
+        check_matrix(g, oracle_system(n))
+        check_cg(g, n, 200, 0.0)
+
+
+def test_errors_and_states():
+    with M.Minife(4, 4, 4) as g:
+        with pytest.raises(M.MinifeError) as e:
+            g.cg_solve(10, 0.0)
+        assert e.value.status == M.MINIFE_ESTATE
+        g.assemble()
+        with pytest.raises(M.MinifeError):
+            g.cg_solve(0, 0.0)
+        with pytest.raises(M.MinifeError):
+            g.cg_solve(10, float("nan"))
+        with pytest.raises(M.MinifeError):
+            g.cg_solve(10, -1.0)
+        g.assemble()                      # idempotent
+        check_matrix(g, oracle_system((4, 4, 4)))
+
+
+def test_all_dirichlet_mesh_converges_in_one_iteration():
+    # 1x1x1: every node constrained -> A = I, b = v; CG stops at k = 1 with x = b
+    with M.Minife(1, 1, 1) as g:
+        g.assemble()
+        r = g.cg_solve(200, 0.0)
+        assert r.iterations == 1 and r.converged == 1
+        assert np.array_equal(g.solution(), g.rhs())
+
+
+def test_spmv_device_and_user_stream():
+    import torch
+    n = (16, 15, 14)
+    s = oracle_system(n)
+    x = minife_inputs.uniform_pm1(s.rows, 7)
+    yo = O.spmv(s.row_ptr, s.col, s.val, x)
+    with M.Minife(*n) as g:
+        g.assemble()
+        st = torch.cuda.Stream()
+        g.set_stream(st.cuda_stream)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        g.spmv_device(xd.data_ptr(), yd.data_ptr(), st.cuda_stream)
+        st.synchronize()
+        assert _same(yd.cpu().numpy(), yo)
+        check_cg(g, n, 50, 0.0)           # solve launched on the torch stream
+        g.set_stream(None)
+
+
+def test_profile_mode_matches_graph_mode():
+    n = (20, 20, 20)
+    with M.Minife(*n) as g:
+        g.assemble()
+        g.cg_solve(200, 0.0)
+        h1, x1 = g.history(), g.solution()
+        t = g.cg_profile(200)
+        assert t.spmv_ms > 0 and t.update_xr_ms > 0 and t.update_p_ms > 0
+        assert _same(g.history(), h1) and _same(g.solution(), x1)
+
+
+@pytest.mark.slow
+def test_100cubed_full_parity():
+    """configs[1] at full size: matrix, SpMV and the 200-iteration CG, element by element."""
+    n = (100, 100, 100)
+    s = oracle_system(n)
+    with M.Minife(*n) as g:
+        g.assemble()
+        check_matrix(g, s)
+        check_spmv(g, s, 12345)
+        check_cg(g, n, 200, 0.0)
+    _oracle_cache.clear()
+
+
+@pytest.mark.slow
+def test_300cubed_sampled_parity():
+    """configs[2] at full size, in the bench's launch configuration: sampled rows of A and y
+    against the oracle's per-row routine, and p-independence of the whole CG (P10)."""
+    n = (300, 300, 300)
+    rows = 301 ** 3
+    rng = np.random.default_rng(0)
+    gids = np.unique(np.concatenate([rng.integers(0, rows, 400),
+                                     [0, 1, 300, 301, rows // 2, rows - 1, rows - 302]]))
+    with M.Minife(*n) as g:
+        g.assemble()
+        cols, vals, lens = g.export_rows(gids)
+        x = minife_inputs.uniform_pm1(rows, 12345)
+        y = g.spmv(x)
+        for i, gid in enumerate(gids):
+            oc, ov, ob = O.row(*n, int(gid))
+            assert lens[i] == oc.size
+            assert np.array_equal(cols[i, :lens[i]], oc)
+            assert _same(vals[i, :lens[i]], ov)
+            yo = O.spmv(np.array([0, oc.size]), oc, ov, x)[0]
+            assert y[gid] == yo
+        r1 = g.cg_solve(200, 0.0)
+        h1 = g.history()
+        x1 = g.solution()
+    with M.Minife(*n, virtual=2) as g2:
+        g2.assemble()
+        r2 = g2.cg_solve(200, 0.0)
+        assert r2.iterations == r1.iterations == 200
+        assert _same(g2.history(), h1)
+        assert _same(g2.solution(), x1)
