@@ -44,6 +44,14 @@ extern "C" {
 #define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1, NCCL comms */
 #define MINIFE_MODE_RANK 3     /* SPMD: this process is rank r of w (torchrun), NCCL comm */
 
+/* ---- matrix storage formats ---------------------------------------------- */
+#define MINIFE_FMT_CRS 0       /* SELL-32, one int32 column per stored entry: the paper's CRS
+                                  (Fig 3.1) on the GPU; 12 B per entry              */
+#define MINIFE_FMT_SEG 1       /* SELL-32, 27 value slots per row + one int32 start column per
+                                  x-run ("non-zero segment") + a 27-bit presence mask: the
+                                  paper's BCRS (Fig 3.2) on the GPU; 8 B per entry
+                                  + 4 B per segment.  Default.                                */
+
 typedef struct minife_ctx minife_ctx;
 
 /* Per-part (per-rank) plan, host-computed from the RCB partition (G15). */
@@ -73,6 +81,9 @@ typedef struct minife_info {
     int64_t max_part_rows, max_part_nnz, max_part_externals;
     int64_t sell_entries;     /* held by this ctx                                         */
     int64_t device_bytes;     /* device memory held by this ctx                           */
+    int32_t format;           /* MINIFE_FMT_*                                             */
+    int32_t reserved;
+    int64_t local_nns;        /* non-zero segments (x-runs) of the rows held here */
 } minife_info;
 
 typedef struct minife_cg_result {
@@ -132,6 +143,11 @@ const char *minife_strerror(int status);
 const char *minife_last_error(const minife_ctx *ctx);
 
 /* ---- the hot path ---------------------------------------------------------------------- */
+
+/* Select the storage format used by the next minife_assemble (default MINIFE_FMT_SEG).  The
+ * ctx becomes unassembled.  Results are bit-identical in both formats (same values, same
+ * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
+int minife_set_format(minife_ctx *ctx, int format);
 
 /* Structure -> SELL-32 (a0.2), element operator (a0.3, C1), gather-assembly (a0.4, C2) and
  * Dirichlet elimination (a0.5, C3) on the device, for every part.  Idempotent.

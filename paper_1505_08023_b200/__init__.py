@@ -40,6 +40,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 MINIFE_OK, MINIFE_EINVAL, MINIFE_ESTATE, MINIFE_ECUDA, MINIFE_ENCCL = 0, 1, 2, 3, 4
 MINIFE_ENOMEM, MINIFE_ENOTSPD, MINIFE_EDIVERGED, MINIFE_ENODEV = 5, 6, 7, 8
 MODE_SINGLE, MODE_VIRTUAL, MODE_MULTI, MODE_RANK = 0, 1, 2, 3
+FMT_CRS, FMT_SEG = 0, 1
 
 
 class minife_part_info(ctypes.Structure):
@@ -60,7 +61,8 @@ class minife_info(ctypes.Structure):
                 ("local_rows", ctypes.c_int64), ("local_nnz", ctypes.c_int64),
                 ("max_part_rows", ctypes.c_int64), ("max_part_nnz", ctypes.c_int64),
                 ("max_part_externals", ctypes.c_int64), ("sell_entries", ctypes.c_int64),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("format", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("local_nns", ctypes.c_int64)]
 
 
 class minife_cg_result(ctypes.Structure):
@@ -95,6 +97,7 @@ SIGNATURES = {
     "minife_set_stream": (_I, [_P, _P]),
     "minife_strerror": (ctypes.c_char_p, [_I]),
     "minife_last_error": (ctypes.c_char_p, [_P]),
+    "minife_set_format": (_I, [_P, _I]),
     "minife_assemble": (_I, [_P]),
     "minife_cg_solve": (_I, [_P, _I, _D, ctypes.POINTER(minife_cg_result)]),
     "minife_cg_profile": (_I, [_P, _I, ctypes.POINTER(minife_kernel_times)]),
@@ -170,7 +173,7 @@ class Minife:
     """RAII wrapper: Minife(nx, ny, nz, ngpu=1 | virtual=p | rank=(r, w, dev, uid))."""
 
     def __init__(self, nx: int, ny: int, nz: int, ngpu: int = 1, virtual: int | None = None,
-                 rank: tuple | None = None):
+                 rank: tuple | None = None, fmt: int | None = None):
         h = ctypes.c_void_p()
         if rank is not None:
             r, w, dev, uid = rank
@@ -183,6 +186,8 @@ class Minife:
         if st != MINIFE_OK:
             raise MinifeError(st, "minife_create")
         self.h = h
+        if fmt is not None:
+            self._check(minife_set_format(self.h, fmt), "minife_set_format")
         self.info = self.get_info()
 
     # -- lifecycle -------------------------------------------------------------------------
@@ -226,6 +231,11 @@ class Minife:
     def set_stream(self, stream_handle: int | None):
         self._check(minife_set_stream(self.h, ctypes.c_void_p(stream_handle or 0)),
                     "minife_set_stream")
+
+    def set_format(self, fmt: int):
+        """FMT_SEG (default, the paper's BCRS on SELL-32) or FMT_CRS (one index per entry)."""
+        self._check(minife_set_format(self.h, fmt), "minife_set_format")
+        self.info = self.get_info()
 
     def assemble(self):
         self._check(minife_assemble(self.h), "minife_assemble")

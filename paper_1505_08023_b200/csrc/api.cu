@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,51 +20,7 @@
 
 using namespace minife;
 
-#define MINIFE_VERSION "minife-b200 0.1.0 (sm_100a)"
-
-namespace {
-
-struct Part {
-    int dev = 0;
-    Plan plan;
-    int64_t rows = 0, ncols = 0, nslices = 0, entries = 0, nnz = 0;
-    std::vector<int64_t> h_slice_off;
-    int64_t *d_slice_off = nullptr;
-    uint8_t *d_row_len = nullptr, *d_width = nullptr;
-    int32_t *d_col = nullptr;
-    double *d_val = nullptr;
-    double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
-    double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
-    unsigned long long *d_acc = nullptr;          // [0, ACC_WORDS) pAp, [ACC_WORDS, 2*) rr
-    CgState *d_st = nullptr;
-    double *d_hist = nullptr, *d_rr = nullptr;
-    int hist_cap = 0;
-    int64_t *d_ext_gid = nullptr;
-    int32_t *d_ext_slot = nullptr;
-    int32_t *d_send_idx = nullptr;
-    double *d_sendbuf = nullptr;
-    ncclComm_t comm = nullptr;
-    cudaStream_t stream = nullptr;
-    int grid_spmv = 1, grid_upd = 1;
-    size_t bytes = 0;
-    unsigned long long *acc_pAp() const { return d_acc; }
-    unsigned long long *acc_rr() const { return d_acc + ACC_WORDS; }
-};
-
-struct DevGuard {
-    int prev = 0;
-    bool ok = false;
-    explicit DevGuard(int dev) {
-        ok = cudaGetDevice(&prev) == cudaSuccess;
-        cudaSetDevice(dev);
-    }
-    ~DevGuard() {
-        if (ok) cudaSetDevice(prev);
-    }
-};
-
-}  // namespace
-
+#define MINIFE_VERSION "minife-b200 0.2.0 (sm_100a)"
 
 // ----------------------------------------------------------------------------------------
 // NCCL is resolved at run time (dlopen), never linked: the process may already hold torch's
@@ -117,11 +74,54 @@ const NcclApi *nccl() {
     state = ok ? 1 : -1;
     return ok ? &api : nullptr;
 }
+
+struct Part {
+    int dev = 0;
+    Plan plan;
+    int64_t rows = 0, ncols = 0, nslices = 0, entries = 0, nnz = 0, nns = 0;
+    std::vector<int64_t> h_slice_off;
+    // matrix (CRS: slice_off/row_len/col/val; SEG: seg/mask/val)
+    int64_t *d_slice_off = nullptr;
+    uint8_t *d_row_len = nullptr, *d_width = nullptr;
+    int32_t *d_col = nullptr, *d_seg = nullptr;
+    uint32_t *d_mask = nullptr;
+    double *d_val = nullptr;
+    // vectors: b, x, r, Ap in row (owned) order; p in column (extended-box) order
+    double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
+    double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
+    unsigned long long *d_acc = nullptr;          // [0, ACC_WORDS) pAp, [ACC_WORDS, 2*) rr
+    CgState *d_st = nullptr;
+    double *d_hist = nullptr, *d_rr = nullptr;
+    int hist_cap = 0;
+    // halo: send_col = extended columns of the send lists (neighbor order), recv_pos =
+    // extended column of each halo slot; wire buffers
+    int32_t *d_send_col = nullptr, *d_recv_pos = nullptr;
+    double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    int grid_spmv = 1, grid_upd = 1;
+    size_t bytes = 0, matrix_bytes = 0;
+    unsigned long long *acc_pAp() const { return d_acc; }
+    unsigned long long *acc_rr() const { return d_acc + ACC_WORDS; }
+};
+
+struct DevGuard {
+    int prev = 0;
+    bool ok = false;
+    explicit DevGuard(int dev) {
+        ok = cudaGetDevice(&prev) == cudaSuccess;
+        cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        if (ok) cudaSetDevice(prev);
+    }
+};
 }  // namespace
 
 struct minife_ctx {
     Mesh mesh{};
     int mode = MINIFE_MODE_SINGLE;
+    int fmt = MINIFE_FMT_SEG;
     int world = 1, rank = 0;
     std::vector<Part> parts;
     cudaStream_t user_stream = nullptr;
@@ -178,6 +178,11 @@ static cudaStream_t stream_of(minife_ctx *c, Part &p) {
     return p.stream;
 }
 
+// all parts of a VIRTUAL ctx share part 0's stream (one device, one ordered queue)
+static cudaStream_t launch_stream(minife_ctx *c, Part &p) {
+    return c->mode == MINIFE_MODE_VIRTUAL ? c->parts[0].stream : stream_of(c, p);
+}
+
 template <class T>
 static int dalloc(minife_ctx *c, Part &p, T **ptr, size_t n) {
     if (n == 0) n = 1;
@@ -186,16 +191,54 @@ static int dalloc(minife_ctx *c, Part &p, T **ptr, size_t n) {
     return MINIFE_OK;
 }
 
+template <class T>
+static void dfree(Part &p, T *&ptr, size_t n) {
+    if (!ptr) return;
+    cudaFree(ptr);
+    ptr = nullptr;
+    p.bytes -= (n ? n : 1) * sizeof(T);
+}
+
+static void free_matrix(Part &p) {
+    DevGuard g(p.dev);
+    for (void **b : {(void **)&p.d_col, (void **)&p.d_seg, (void **)&p.d_mask, (void **)&p.d_val}) {
+        if (*b) cudaFree(*b);
+        *b = nullptr;
+    }
+    p.bytes -= p.matrix_bytes;
+    p.matrix_bytes = 0;
+    p.entries = 0;
+}
+
 static void free_part(Part &p) {
     DevGuard g(p.dev);
-    void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width, p.d_col,     p.d_val,    p.d_b,
-                    p.d_x,         p.d_r,       p.d_p,     p.d_Ap,      p.d_xin,    p.d_yout,
-                    p.d_acc,       p.d_st,      p.d_hist,  p.d_rr,      p.d_ext_gid,
-                    p.d_ext_slot,  p.d_send_idx, p.d_sendbuf};
+    free_matrix(p);
+    void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width,   p.d_b,        p.d_x,
+                    p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,
+                    p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
+                    p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
     if (p.stream) cudaStreamDestroy(p.stream);
+}
+
+static Geom geom_of(const minife_ctx *c, const Part &p) {
+    Geom g{};
+    g.nx = c->mesh.nx;
+    g.ny = c->mesh.ny;
+    g.nz = c->mesh.nz;
+    for (int k = 0; k < 3; ++k) {
+        g.own_lo[k] = p.plan.own_lo[k];
+        g.own_n[k] = (int)p.plan.own_n[k];
+        g.ext_lo[k] = p.plan.ext_lo[k];
+        g.ext_n[k] = (int)p.plan.ext_n[k];
+        g.off[k] = p.plan.off[k];
+    }
+    g.rows = p.rows;
+    g.ncols = p.ncols;
+    g.ident = p.ncols == p.rows;
+    return g;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -204,11 +247,10 @@ static void free_part(Part &p) {
 
 static int alloc_hist(minife_ctx *c, Part &p, int cap) {
     DevGuard g(p.dev);
-    if (p.d_hist) cudaFree(p.d_hist);
-    if (p.d_rr) cudaFree(p.d_rr);
-    p.d_hist = p.d_rr = nullptr;
-    CUDA_TRY(c, cudaMalloc((void **)&p.d_hist, sizeof(double) * cap));
-    CUDA_TRY(c, cudaMalloc((void **)&p.d_rr, sizeof(double) * cap));
+    dfree(p, p.d_hist, p.hist_cap);
+    dfree(p, p.d_rr, p.hist_cap);
+    TRY(dalloc(c, p, &p.d_hist, cap));
+    TRY(dalloc(c, p, &p.d_rr, cap));
     p.hist_cap = cap;
     return MINIFE_OK;
 }
@@ -218,9 +260,10 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     p.plan = plan;
     DevGuard g(dev);
     p.rows = plan.n_owned;
-    p.ncols = plan.n_owned + plan.n_ext;
+    p.ncols = plan.n_cols;
     p.nslices = (p.rows + 31) / 32;
     p.nnz = plan.local_nnz();
+    p.nns = plan.local_nns();
     CUDA_TRY(c, cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
     TRY(dalloc(c, p, &p.d_slice_off, p.nslices + 1));
     TRY(dalloc(c, p, &p.d_row_len, p.nslices * 32));
@@ -236,36 +279,27 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     CUDA_TRY(c, cudaMemset(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long)));
     CUDA_TRY(c, cudaMemset(p.d_st, 0, sizeof(CgState)));
     CUDA_TRY(c, cudaMemset(p.d_p, 0, p.ncols * sizeof(double)));
-    // externals sorted by gid -> local column, for the assembly's column lookup
-    std::vector<std::pair<int64_t, int32_t>> ext(plan.n_ext);
-    for (int64_t i = 0; i < plan.n_ext; ++i)
-        ext[i] = {plan.ext_gid[i], (int32_t)(plan.n_owned + i)};
-    std::sort(ext.begin(), ext.end());
-    std::vector<int64_t> eg(plan.n_ext);
-    std::vector<int32_t> es(plan.n_ext);
-    for (int64_t i = 0; i < plan.n_ext; ++i) {
-        eg[i] = ext[i].first;
-        es[i] = ext[i].second;
-    }
-    TRY(dalloc(c, p, &p.d_ext_gid, plan.n_ext));
-    TRY(dalloc(c, p, &p.d_ext_slot, plan.n_ext));
-    if (plan.n_ext) {
-        CUDA_TRY(c, cudaMemcpy(p.d_ext_gid, eg.data(), eg.size() * 8, cudaMemcpyHostToDevice));
-        CUDA_TRY(c, cudaMemcpy(p.d_ext_slot, es.data(), es.size() * 4, cudaMemcpyHostToDevice));
-    }
-    TRY(dalloc(c, p, &p.d_send_idx, plan.send_idx.size()));
-    TRY(dalloc(c, p, &p.d_sendbuf, plan.send_idx.size()));
-    if (!plan.send_idx.empty())
-        CUDA_TRY(c, cudaMemcpy(p.d_send_idx, plan.send_idx.data(), plan.send_idx.size() * 4,
+    // halo index lists, as extended columns
+    std::vector<int32_t> send_col(plan.send_idx.size()), recv_pos(plan.n_ext);
+    for (size_t i = 0; i < plan.send_idx.size(); ++i)
+        send_col[i] = (int32_t)plan.row_to_col(plan.send_idx[i]);
+    for (int64_t i = 0; i < plan.n_ext; ++i) recv_pos[i] = (int32_t)plan.ext_pos[i];
+    TRY(dalloc(c, p, &p.d_send_col, send_col.size()));
+    TRY(dalloc(c, p, &p.d_sendbuf, send_col.size()));
+    TRY(dalloc(c, p, &p.d_recv_pos, recv_pos.size()));
+    TRY(dalloc(c, p, &p.d_recvbuf, recv_pos.size()));
+    if (!send_col.empty())
+        CUDA_TRY(c, cudaMemcpy(p.d_send_col, send_col.data(), 4 * send_col.size(),
                                cudaMemcpyHostToDevice));
-    p.grid_spmv = spmv_grid(p.nslices);
+    if (!recv_pos.empty())
+        CUDA_TRY(c, cudaMemcpy(p.d_recv_pos, recv_pos.data(), 4 * recv_pos.size(),
+                               cudaMemcpyHostToDevice));
     p.grid_upd = stream_grid(p.rows);
     return MINIFE_OK;
 }
 
 static int validate_mesh(int nx, int ny, int nz) {
     if (nx < 1 || ny < 1 || nz < 1) return MINIFE_EINVAL;
-    // local column ids are int32 (north star); a part must stay below 2^31 columns
     return MINIFE_OK;
 }
 
@@ -286,9 +320,9 @@ static int create_common(minife_ctx *c, int nx, int ny, int nz, int nparts,
             set_err(c, "plan construction failed for rank %d", r);
             return MINIFE_EINVAL;
         }
-        if (plan.n_owned + plan.n_ext >= (int64_t)1 << 31) {
+        if (plan.n_cols >= ((int64_t)1 << 31) - 64) {
             set_err(c, "part %d has %lld columns: int32 local indices overflow", r,
-                    (long long)(plan.n_owned + plan.n_ext));
+                    (long long)plan.n_cols);
             return MINIFE_EINVAL;
         }
         TRY(setup_part(c, c->parts[q], devs[q], plan));
@@ -394,9 +428,15 @@ extern "C" int minife_create_rank(int nx, int ny, int nz, int rank, int world, i
     return MINIFE_OK;
 }
 
+static void drop_graph(minife_ctx *c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->g_iters = -1;
+}
+
 extern "C" void minife_destroy(minife_ctx *c) {
     if (!c) return;
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    drop_graph(c);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto &p : c->parts) free_part(p);
@@ -407,6 +447,18 @@ extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
     if (!c) return MINIFE_EINVAL;
     if (c->mode != MINIFE_MODE_SINGLE && c->mode != MINIFE_MODE_RANK) return MINIFE_ESTATE;
     c->user_stream = (cudaStream_t)stream;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_set_format(minife_ctx *c, int format) {
+    if (!c || (format != MINIFE_FMT_CRS && format != MINIFE_FMT_SEG)) return MINIFE_EINVAL;
+    if (format != c->fmt) {
+        c->fmt = format;
+        c->assembled = false;
+        c->solved = false;
+        drop_graph(c);
+        for (auto &p : c->parts) free_matrix(p);
+    }
     return MINIFE_OK;
 }
 
@@ -432,25 +484,18 @@ extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
 // assembly (a0.2 - a0.5)
 // ----------------------------------------------------------------------------------------
 
-static AsmArgs asm_args(const minife_ctx *c, const Part &p) {
-    AsmArgs a{};
-    a.nx = c->mesh.nx;
-    a.ny = c->mesh.ny;
-    a.nz = c->mesh.nz;
-    for (int k = 0; k < 3; ++k) {
-        a.own_lo[k] = p.plan.own_lo[k];
-        a.own_n[k] = p.plan.own_n[k];
-    }
-    a.rows = p.rows;
-    a.n_ext = p.plan.n_ext;
-    a.ext_sorted_gid = p.d_ext_gid;
-    a.ext_sorted_slot = p.d_ext_slot;
-    a.slice_off = p.d_slice_off;
-    a.row_len = p.d_row_len;
-    a.col = p.d_col;
-    a.val = p.d_val;
-    a.b = p.d_b;
-    return a;
+static Matrix matrix_of(const minife_ctx *c, const Part &p) {
+    Matrix m{};
+    m.fmt = c->fmt;
+    m.rows = p.rows;
+    m.nslices = p.nslices;
+    m.val = p.d_val;
+    m.slice_off = p.d_slice_off;
+    m.row_len = p.d_row_len;
+    m.col = p.d_col;
+    m.seg = p.d_seg;
+    m.mask = p.d_mask;
+    return m;
 }
 
 extern "C" int minife_assemble(minife_ctx *c) {
@@ -458,29 +503,55 @@ extern "C" int minife_assemble(minife_ctx *c) {
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         cudaStream_t s = stream_of(c, p);
-        AsmArgs a = asm_args(c, p);
-        CUDA_TRY(c, launch_rowlen_widths(a, p.d_row_len, p.d_width, p.nslices, s));
-        std::vector<uint8_t> w(p.nslices);
-        CUDA_TRY(c, cudaMemcpyAsync(w.data(), p.d_width, p.nslices, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(c, cudaStreamSynchronize(s));
-        p.h_slice_off.assign(p.nslices + 1, 0);
-        for (int64_t i = 0; i < p.nslices; ++i)
-            p.h_slice_off[i + 1] = p.h_slice_off[i] + 32 * (int64_t)w[i];
-        const int64_t entries = p.h_slice_off[p.nslices];
-        if (entries != p.entries || !p.d_col) {
-            if (p.d_col) cudaFree(p.d_col);
-            if (p.d_val) cudaFree(p.d_val);
-            p.d_col = nullptr;
-            p.d_val = nullptr;
-            TRY(dalloc(c, p, &p.d_col, entries));
-            TRY(dalloc(c, p, &p.d_val, entries));
-            p.entries = entries;
+        const Geom geo = geom_of(c, p);
+        AsmArgs a{};
+        a.g = geo;
+        a.fmt = c->fmt;
+        if (c->fmt == MINIFE_FMT_CRS) {
+            // slice widths on the device, offsets by a host prefix sum (8 B per 32 rows)
+            CUDA_TRY(c, launch_rowlen_widths(geo, p.d_row_len, p.d_width, p.nslices, s));
+            std::vector<uint8_t> w(p.nslices);
+            CUDA_TRY(c, cudaMemcpyAsync(w.data(), p.d_width, p.nslices, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c, cudaStreamSynchronize(s));
+            p.h_slice_off.assign(p.nslices + 1, 0);
+            for (int64_t i = 0; i < p.nslices; ++i)
+                p.h_slice_off[i + 1] = p.h_slice_off[i] + 32 * (int64_t)w[i];
+            const int64_t entries = p.h_slice_off[p.nslices];
+            if (entries != p.entries || !p.d_col) {
+                free_matrix(p);
+                TRY(dalloc(c, p, &p.d_col, entries));
+                TRY(dalloc(c, p, &p.d_val, entries));
+                p.matrix_bytes = 12 * (size_t)entries;
+                p.entries = entries;
+            }
+            CUDA_TRY(c, cudaMemcpyAsync(p.d_slice_off, p.h_slice_off.data(), 8 * (p.nslices + 1),
+                                        cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c, cudaStreamSynchronize(s));
+        } else {
+            const int64_t entries = 27 * 32 * p.nslices;
+            if (!p.d_seg) {
+                free_matrix(p);
+                TRY(dalloc(c, p, &p.d_val, entries));
+                TRY(dalloc(c, p, &p.d_seg, 9 * 32 * p.nslices));
+                TRY(dalloc(c, p, &p.d_mask, 32 * p.nslices));   // padded: whole-slice copies
+                p.matrix_bytes = 8 * (size_t)entries + 4 * (size_t)(9 * 32 * p.nslices) +
+                                 4 * (size_t)(32 * p.nslices);
+                p.entries = entries;
+            }
         }
-        CUDA_TRY(c, cudaMemcpyAsync(p.d_slice_off, p.h_slice_off.data(), 8 * (p.nslices + 1),
-                                    cudaMemcpyHostToDevice, s));
-        a = asm_args(c, p);
+        a.slice_off = p.d_slice_off;
+        a.row_len = p.d_row_len;
+        a.col = p.d_col;
+        a.seg = p.d_seg;
+        a.mask = p.d_mask;
+        a.val = p.d_val;
+        a.b = p.d_b;
         CUDA_TRY(c, launch_assemble(a, s));
-        CUDA_TRY(c, cudaStreamSynchronize(s));
+        p.grid_spmv = spmv_grid(p.nslices, c->fmt);
+    }
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaStreamSynchronize(stream_of(c, p)));
     }
     c->assembled = true;
     c->solved = false;
@@ -491,12 +562,13 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // transports: halo exchange (a1) and accumulator all-reduce (a3/a5)
 // ----------------------------------------------------------------------------------------
 
-// Fill the external slots of `vec(part)` (length ncols) from the owners' owned values.
+// Fill the halo (shell) columns of vec(part) from the owners' owned values.
 template <class VecOf>
 static int enqueue_halo(minife_ctx *c, VecOf vec) {
     if (c->world == 1) return MINIFE_OK;
     if (c->mode == MINIFE_MODE_VIRTUAL) {
-        // device-local transport: read the owner's owned values through its send list
+        // device-local transport: read the owner's columns through its send list, write the
+        // receiver's halo columns
         cudaStream_t s = c->parts[0].stream;
         for (auto &dst : c->parts) {
             for (size_t k = 0; k < dst.plan.nbr.size(); ++k) {
@@ -504,31 +576,37 @@ static int enqueue_halo(minife_ctx *c, VecOf vec) {
                 auto it = std::lower_bound(src.plan.nbr.begin(), src.plan.nbr.end(),
                                            dst.plan.rank);
                 const size_t j = (size_t)(it - src.plan.nbr.begin());
-                CUDA_TRY(c, launch_pack(vec(src), src.d_send_idx + src.plan.send_off[j],
-                                        src.plan.send_cnt[j],
-                                        vec(dst) + dst.rows + dst.plan.recv_off[k], s));
+                CUDA_TRY(c, launch_move(vec(src), src.d_send_col + src.plan.send_off[j], vec(dst),
+                                        dst.d_recv_pos + dst.plan.recv_off[k],
+                                        src.plan.send_cnt[j], s));
             }
         }
         return MINIFE_OK;
     }
-    // NCCL: pack each part's send lists, then grouped send/recv per neighbor
+    // NCCL: pack each part's send lists, grouped send/recv per neighbor, unpack the slots
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_pack(vec(p), p.d_send_idx, (int64_t)p.plan.send_idx.size(),
-                                p.d_sendbuf, stream_of(c, p)));
+        CUDA_TRY(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
+                                (int64_t)p.plan.send_idx.size(), stream_of(c, p)));
     }
     NCCL_TRY(c, nccl()->GroupStart());
     for (auto &p : c->parts) {
         cudaStream_t s = stream_of(c, p);
         for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
-            NCCL_TRY(c, nccl()->Send(p.d_sendbuf + p.plan.send_off[k], (size_t)p.plan.send_cnt[k],
-                                 ncclFloat64, p.plan.nbr[k], p.comm, s));
-            NCCL_TRY(c, nccl()->Recv(vec(p) + p.rows + p.plan.recv_off[k],
-                                 (size_t)p.plan.recv_cnt[k], ncclFloat64, p.plan.nbr[k],
-                                 p.comm, s));
+            NCCL_TRY(c, nccl()->Send(p.d_sendbuf + p.plan.send_off[k],
+                                     (size_t)p.plan.send_cnt[k], ncclFloat64, p.plan.nbr[k],
+                                     p.comm, s));
+            NCCL_TRY(c, nccl()->Recv(p.d_recvbuf + p.plan.recv_off[k],
+                                     (size_t)p.plan.recv_cnt[k], ncclFloat64, p.plan.nbr[k],
+                                     p.comm, s));
         }
     }
     NCCL_TRY(c, nccl()->GroupEnd());
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext,
+                                stream_of(c, p)));
+    }
     return MINIFE_OK;
 }
 
@@ -544,7 +622,8 @@ static int enqueue_allreduce(minife_ctx *c, int which) {
     NCCL_TRY(c, nccl()->GroupStart());
     for (auto &p : c->parts) {
         unsigned long long *a = which ? p.acc_rr() : p.acc_pAp();
-        NCCL_TRY(c, nccl()->AllReduce(a, a, ACC_WORDS, ncclInt64, ncclSum, p.comm, stream_of(c, p)));
+        NCCL_TRY(c, nccl()->AllReduce(a, a, ACC_WORDS, ncclInt64, ncclSum, p.comm,
+                                      stream_of(c, p)));
     }
     NCCL_TRY(c, nccl()->GroupEnd());
     return MINIFE_OK;
@@ -554,9 +633,9 @@ static int enqueue_allreduce(minife_ctx *c, int which) {
 // CG driver (C6): init + max_iters x [halo, K1, reduce, K6, reduce, K7]
 // ----------------------------------------------------------------------------------------
 
-static UpdArgs upd_args(Part &p, int which_in) {
+static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
     UpdArgs a{};
-    a.rows = p.rows;
+    a.g = geom_of(c, p);
     a.x = p.d_x;
     a.r = p.d_r;
     a.p = p.d_p;
@@ -577,24 +656,16 @@ static UpdArgs upd_args(Part &p, int which_in) {
     return a;
 }
 
-static SpmvArgs spmv_args(Part &p, const double *x, double *y, bool dot) {
+static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double *y, bool dot) {
     SpmvArgs a{};
-    a.rows = p.rows;
-    a.nslices = p.nslices;
-    a.slice_off = p.d_slice_off;
-    a.row_len = p.d_row_len;
-    a.col = p.d_col;
-    a.val = p.d_val;
+    a.m = matrix_of(c, p);
+    a.g = geom_of(c, p);
     a.x = x;
     a.y = y;
     a.acc = dot ? p.acc_pAp() : nullptr;
     a.acc_zero = dot ? p.acc_rr() : nullptr;
     a.st = dot ? p.d_st : nullptr;
     return a;
-}
-
-static cudaStream_t launch_stream(minife_ctx *c, Part &p) {
-    return c->mode == MINIFE_MODE_VIRTUAL ? c->parts[0].stream : stream_of(c, p);
 }
 
 struct PhaseTimer {
@@ -615,14 +686,14 @@ static int enqueue_init(minife_ctx *c, double tol) {
         DevGuard g(p.dev);
         cudaStream_t s = launch_stream(c, p);
         CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long), s));
-        UpdArgs a = upd_args(p, 0);
+        UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
         CUDA_TRY(c, launch_init_vectors(a, p.grid_upd, s));
     }
     TRY(enqueue_allreduce(c, 1));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        UpdArgs a = upd_args(p, 0);
+        UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
         a.acc_zero = p.acc_pAp();
         CUDA_TRY(c, launch_init_finalize(a, tol, launch_stream(c, p)));
@@ -635,7 +706,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+        CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
                                 launch_stream(c, p)));
     }
     if (t) t->mark(0);
@@ -643,14 +714,14 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_update_xr(upd_args(p, 0), k, p.grid_upd, launch_stream(c, p)));
+        CUDA_TRY(c, launch_update_xr(upd_args(c, p, 0), k, p.grid_upd, launch_stream(c, p)));
     }
     if (t) t->mark(1);
     TRY(enqueue_allreduce(c, 1));
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_update_p(upd_args(p, 1), k, p.grid_upd, launch_stream(c, p)));
+        CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
     }
     if (t) t->mark(2);
     return MINIFE_OK;
@@ -659,11 +730,14 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
 static int ensure_hist(minife_ctx *c, int max_iters) {
     if (c->parts[0].hist_cap >= max_iters + 1) return MINIFE_OK;
     for (auto &p : c->parts) TRY(alloc_hist(c, p, max_iters + 1));
-    if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
-    }
+    drop_graph(c);
     return MINIFE_OK;
+}
+
+static double spmv_alg_bytes(const minife_ctx *c, const Part &q) {
+    // CRS 12 nnz (+16 rows of x/y); segment format 8 nnz + 4 nns (+16 rows)
+    return c->fmt == MINIFE_FMT_CRS ? 12.0 * (double)q.nnz
+                                    : 8.0 * (double)q.nnz + 4.0 * (double)q.nns;
 }
 
 static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, double seconds) {
@@ -692,7 +766,7 @@ static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, doub
         const double rows = (double)c->mesh.rows(), nnz = (double)c->mesh.nnz();
         res->flops = (double)st.iters * (2.0 * nnz + 10.0 * rows);
         double bytes = 0.0;
-        for (auto &q : c->parts) bytes += 12.0 * (double)q.nnz + 88.0 * (double)q.rows;
+        for (auto &q : c->parts) bytes += spmv_alg_bytes(c, q) + 88.0 * (double)q.rows;
         res->bytes = (double)st.iters * bytes;
     }
     return status;
@@ -713,7 +787,6 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
     DevGuard g(p0.dev);
-    double seconds = 0.0;
     if (c->mode == MINIFE_MODE_MULTI) {
         // one host thread drives every device: launch the sequence directly
         CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
@@ -726,10 +799,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         }
     } else {
         if (!c->gexec || c->g_iters != max_iters || c->g_tol != tol) {
-            if (c->gexec) {
-                cudaGraphExecDestroy(c->gexec);
-                c->gexec = nullptr;
-            }
+            drop_graph(c);
             // capture on the ctx's own stream (a torch stream may be the legacy default one)
             cudaStream_t cap = p0.stream;
             cudaStream_t saved = c->user_stream;
@@ -760,8 +830,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     CUDA_TRY(c, cudaEventSynchronize(c->ev1));
     float ms = 0.f;
     CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    seconds = ms * 1e-3;
-    return read_result(c, max_iters, res, seconds);
+    return read_result(c, max_iters, res, ms * 1e-3);
 }
 
 extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_times *out) {
@@ -797,20 +866,17 @@ extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_tim
 }
 
 // ----------------------------------------------------------------------------------------
-// SpMV through the ABI
+// host <-> part index helpers
 // ----------------------------------------------------------------------------------------
 
-static int64_t gid_of_local(const Plan &pl, int64_t l) {
-    const Mesh &m = pl.mesh;
-    if (l < pl.n_owned) {
-        const int64_t lx = l % pl.own_n[0], ly = (l / pl.own_n[0]) % pl.own_n[1],
-                      lz = l / (pl.own_n[0] * pl.own_n[1]);
-        return (pl.own_lo[0] + lx) + m.NX() * ((pl.own_lo[1] + ly) + m.NY() * (pl.own_lo[2] + lz));
-    }
-    return pl.ext_gid[l - pl.n_owned];
+static int64_t gid_of_row(const Plan &pl, int64_t l) {
+    const int64_t lx = l % pl.own_n[0], ly = (l / pl.own_n[0]) % pl.own_n[1],
+                  lz = l / (pl.own_n[0] * pl.own_n[1]);
+    return (pl.own_lo[0] + lx) +
+           pl.mesh.NX() * ((pl.own_lo[1] + ly) + pl.mesh.NY() * (pl.own_lo[2] + lz));
 }
 
-// global <-> owned-local scatter/gather on the host (box enumeration)
+// global <-> owned-local scatter/gather on the host (box enumeration, x-lines contiguous)
 static void gather_owned(const Plan &pl, const double *global, double *local) {
     const int64_t NX = pl.mesh.NX(), NY = pl.mesh.NY();
     int64_t l = 0;
@@ -831,12 +897,27 @@ static void scatter_owned(const Plan &pl, const double *local, double *global) {
             l += pl.own_n[0];
         }
 }
+// owned-row-order values -> extended-box vector (halo columns left 0)
+static void rows_to_cols(const Plan &pl, const double *rowv, double *colv) {
+    int64_t l = 0;
+    for (int64_t lz = 0; lz < pl.own_n[2]; ++lz)
+        for (int64_t ly = 0; ly < pl.own_n[1]; ++ly) {
+            const int64_t c0 = pl.off[0] + pl.ext_n[0] * ((ly + pl.off[1]) +
+                                                          pl.ext_n[1] * (lz + pl.off[2]));
+            memcpy(colv + c0, rowv + l, sizeof(double) * pl.own_n[0]);
+            l += pl.own_n[0];
+        }
+}
+
+// ----------------------------------------------------------------------------------------
+// SpMV through the ABI
+// ----------------------------------------------------------------------------------------
 
 extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
     if (!c || !x || !y) return MINIFE_EINVAL;
     if (!c->assembled) return MINIFE_ESTATE;
     const bool global_io = c->mode != MINIFE_MODE_RANK;
-    std::vector<double> tmp;
+    std::vector<double> tmp, colv;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         if (!p.d_xin) {
@@ -844,23 +925,30 @@ extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
             TRY(dalloc(c, p, &p.d_yout, p.rows));
         }
         const double *src = x;
-        if (global_io) {
+        if (global_io && !(c->parts.size() == 1 && p.ncols == p.rows)) {
             tmp.resize(p.rows);
             gather_owned(p.plan, x, tmp.data());
             src = tmp.data();
         }
-        CUDA_TRY(c, cudaMemcpy(p.d_xin, src, sizeof(double) * p.rows, cudaMemcpyHostToDevice));
+        if (p.ncols == p.rows) {
+            CUDA_TRY(c, cudaMemcpy(p.d_xin, src, sizeof(double) * p.rows, cudaMemcpyHostToDevice));
+        } else {
+            colv.assign(p.ncols, 0.0);
+            rows_to_cols(p.plan, src, colv.data());
+            CUDA_TRY(c, cudaMemcpy(p.d_xin, colv.data(), sizeof(double) * p.ncols,
+                                   cudaMemcpyHostToDevice));
+        }
     }
     TRY(enqueue_halo(c, [](Part &p) { return p.d_xin; }));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(p, p.d_xin, p.d_yout, false), false, p.grid_spmv,
+        CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_xin, p.d_yout, false), false, p.grid_spmv,
                                 launch_stream(c, p)));
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
-        if (global_io) {
+        if (global_io && !(c->parts.size() == 1 && p.ncols == p.rows)) {
             tmp.resize(p.rows);
             CUDA_TRY(c, cudaMemcpy(tmp.data(), p.d_yout, sizeof(double) * p.rows,
                                    cudaMemcpyDeviceToHost));
@@ -878,7 +966,7 @@ extern "C" int minife_spmv_device(minife_ctx *c, const double *d_x, double *d_y,
     Part &p = c->parts[0];
     DevGuard g(p.dev);
     cudaStream_t s = stream ? (cudaStream_t)stream : stream_of(c, p);
-    CUDA_TRY(c, launch_spmv(spmv_args(p, d_x, d_y, false), false, p.grid_spmv, s));
+    CUDA_TRY(c, launch_spmv(spmv_args(c, p, d_x, d_y, false), false, p.grid_spmv, s));
     return MINIFE_OK;
 }
 
@@ -919,9 +1007,11 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
     o->assembled = c->assembled;
     o->rows = c->mesh.rows();
     o->nnz = c->mesh.nnz();
+    o->format = c->fmt;
     for (auto &p : c->parts) {
         o->local_rows += p.rows;
         o->local_nnz += p.nnz;
+        o->local_nns += p.nns;
         o->max_part_rows = std::max(o->max_part_rows, p.rows);
         o->max_part_nnz = std::max(o->max_part_nnz, p.nnz);
         o->max_part_externals = std::max(o->max_part_externals, p.plan.n_ext);
@@ -938,74 +1028,92 @@ extern "C" int minife_get_part_info(const minife_ctx *c, int part, minife_part_i
     return MINIFE_OK;
 }
 
-struct HostPart {
-    std::vector<int64_t> so;
-    std::vector<uint8_t> len;
-    std::vector<int32_t> col;
-    std::vector<double> val;
-};
-
-static int download_part(minife_ctx *c, Part &p, HostPart &h) {
+// rows [r0, r0+n) of one part -> (extended column, value) lists via the device extractor
+static int extract_part_rows(minife_ctx *c, Part &p, const std::vector<int64_t> &loc,
+                             std::vector<int32_t> &oc, std::vector<double> &ov,
+                             std::vector<int32_t> &ol) {
     DevGuard g(p.dev);
-    h.so = p.h_slice_off;
-    h.len.resize(p.rows);
-    h.col.resize(p.entries);
-    h.val.resize(p.entries);
-    CUDA_TRY(c, cudaMemcpy(h.len.data(), p.d_row_len, p.rows, cudaMemcpyDeviceToHost));
-    CUDA_TRY(c, cudaMemcpy(h.col.data(), p.d_col, 4 * p.entries, cudaMemcpyDeviceToHost));
-    CUDA_TRY(c, cudaMemcpy(h.val.data(), p.d_val, 8 * p.entries, cudaMemcpyDeviceToHost));
-    return MINIFE_OK;
+    const int64_t k = (int64_t)loc.size();
+    oc.assign(27 * k, 0);
+    ov.assign(27 * k, 0.0);
+    ol.assign(k, 0);
+    if (!k) return MINIFE_OK;
+    const int64_t chunk = 1 << 22;
+    int64_t *d_rows = nullptr;
+    int32_t *d_oc = nullptr, *d_ol = nullptr;
+    double *d_ov = nullptr;
+    const int64_t cap = std::min(k, chunk);
+    CUDA_TRY(c, cudaMalloc((void **)&d_rows, 8 * cap));
+    CUDA_TRY(c, cudaMalloc((void **)&d_oc, 4 * 27 * cap));
+    CUDA_TRY(c, cudaMalloc((void **)&d_ov, 8 * 27 * cap));
+    CUDA_TRY(c, cudaMalloc((void **)&d_ol, 4 * cap));
+    int st = MINIFE_OK;
+    for (int64_t b = 0; b < k && st == MINIFE_OK; b += chunk) {
+        const int64_t n = std::min(chunk, k - b);
+        cudaError_t e = cudaMemcpy(d_rows, loc.data() + b, 8 * n, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = launch_extract_rows(matrix_of(c, p), d_rows, n, d_oc, d_ov, d_ol, p.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p.stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(oc.data() + 27 * b, d_oc, 4 * 27 * n, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ov.data() + 27 * b, d_ov, 8 * 27 * n, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(ol.data() + b, d_ol, 4 * n, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            set_err(c, "extract rows: %s", cudaGetErrorString(e));
+            st = MINIFE_ECUDA;
+        }
+    }
+    cudaFree(d_rows);
+    cudaFree(d_oc);
+    cudaFree(d_ov);
+    cudaFree(d_ol);
+    return st;
 }
 
 extern "C" int minife_export_csr(minife_ctx *c, int64_t *row_ptr, int64_t *col, double *val) {
     if (!c || !row_ptr || !col || !val) return MINIFE_EINVAL;
     if (!c->assembled) return MINIFE_ESTATE;
-    if (c->mode == MINIFE_MODE_RANK) {
-        Part &p = c->parts[0];
-        HostPart h;
-        TRY(download_part(c, p, h));
-        row_ptr[0] = 0;
-        for (int64_t r = 0; r < p.rows; ++r) {
-            const int64_t s = r >> 5, lane = r & 31;
-            int64_t o = row_ptr[r];
-            for (int k = 0; k < h.len[r]; ++k) {
-                const int64_t e = h.so[s] + 32 * k + lane;
-                col[o] = gid_of_local(p.plan, h.col[e]);
-                val[o] = h.val[e];
-                ++o;
-            }
-            row_ptr[r + 1] = o;
-        }
-        return MINIFE_OK;
-    }
-    // global row pointer from the closed-form row lengths (rows in global id order)
     const Mesh &m = c->mesh;
-    const int64_t NX = m.NX(), NY = m.NY(), NZ = m.NZ();
+    const bool local = c->mode == MINIFE_MODE_RANK;
+    // row pointer from the closed-form row lengths (global id order, or owned rows)
     row_ptr[0] = 0;
-    int64_t g = 0;
-    for (int64_t iz = 0; iz < NZ; ++iz)
-        for (int64_t iy = 0; iy < NY; ++iy)
-            for (int64_t ix = 0; ix < NX; ++ix, ++g) {
-                const int cx = (ix == 0 || ix == m.nx) ? 2 : 3;
-                const int cy = (iy == 0 || iy == m.ny) ? 2 : 3;
-                const int cz = (iz == 0 || iz == m.nz) ? 2 : 3;
-                row_ptr[g + 1] = row_ptr[g] + cx * cy * cz;
-            }
+    if (local) {
+        const Plan &pl = c->parts[0].plan;
+        for (int64_t r = 0; r < c->parts[0].rows; ++r) {
+            const int64_t g = gid_of_row(pl, r);
+            const int64_t ix = g % m.NX(), iy = (g / m.NX()) % m.NY(), iz = g / (m.NX() * m.NY());
+            const int len = ((ix == 0 || ix == m.nx) ? 2 : 3) * ((iy == 0 || iy == m.ny) ? 2 : 3) *
+                            ((iz == 0 || iz == m.nz) ? 2 : 3);
+            row_ptr[r + 1] = row_ptr[r] + len;
+        }
+    } else {
+        int64_t g = 0;
+        for (int64_t iz = 0; iz < m.NZ(); ++iz)
+            for (int64_t iy = 0; iy < m.NY(); ++iy)
+                for (int64_t ix = 0; ix < m.NX(); ++ix, ++g) {
+                    const int len = ((ix == 0 || ix == m.nx) ? 2 : 3) *
+                                    ((iy == 0 || iy == m.ny) ? 2 : 3) *
+                                    ((iz == 0 || iz == m.nz) ? 2 : 3);
+                    row_ptr[g + 1] = row_ptr[g] + len;
+                }
+    }
     for (auto &p : c->parts) {
-        HostPart h;
-        TRY(download_part(c, p, h));
+        std::vector<int64_t> loc(p.rows);
+        for (int64_t r = 0; r < p.rows; ++r) loc[r] = r;
+        std::vector<int32_t> oc, ol;
+        std::vector<double> ov;
+        TRY(extract_part_rows(c, p, loc, oc, ov, ol));
         for (int64_t r = 0; r < p.rows; ++r) {
-            const int64_t gid = gid_of_local(p.plan, r);
-            const int64_t s = r >> 5, lane = r & 31;
-            int64_t o = row_ptr[gid];
-            if (row_ptr[gid + 1] - o != h.len[r]) {
-                set_err(c, "row %lld: device length %d != closed form", (long long)gid, h.len[r]);
+            const int64_t out_row = local ? r : gid_of_row(p.plan, r);
+            int64_t o = row_ptr[out_row];
+            if (row_ptr[out_row + 1] - o != ol[r]) {
+                set_err(c, "row %lld: device length %d != closed form", (long long)out_row, ol[r]);
                 return MINIFE_ESTATE;
             }
-            for (int k = 0; k < h.len[r]; ++k) {
-                const int64_t e = h.so[s] + 32 * k + lane;
-                col[o] = gid_of_local(p.plan, h.col[e]);
-                val[o] = h.val[e];
+            for (int e = 0; e < ol[r]; ++e) {
+                col[o] = p.plan.col_to_gid(oc[27 * r + e]);
+                val[o] = ov[27 * r + e];
                 ++o;
             }
         }
@@ -1020,7 +1128,6 @@ extern "C" int minife_export_rows(minife_ctx *c, int64_t n, const int64_t *gids,
     const Mesh &m = c->mesh;
     for (int64_t i = 0; i < n; ++i) lens[i] = -1;
     for (auto &p : c->parts) {
-        DevGuard g(p.dev);
         std::vector<int64_t> loc, which;
         for (int64_t i = 0; i < n; ++i) {
             const int64_t gid = gids[i];
@@ -1031,33 +1138,14 @@ extern "C" int minife_export_rows(minife_ctx *c, int64_t n, const int64_t *gids,
             loc.push_back(p.plan.owned_local(ix, iy, iz));
             which.push_back(i);
         }
-        if (loc.empty()) continue;
-        const int64_t k = (int64_t)loc.size();
-        int64_t *d_rows = nullptr;
-        int32_t *d_oc = nullptr, *d_ol = nullptr;
-        double *d_ov = nullptr;
-        CUDA_TRY(c, cudaMalloc((void **)&d_rows, 8 * k));
-        CUDA_TRY(c, cudaMalloc((void **)&d_oc, 4 * 27 * k));
-        CUDA_TRY(c, cudaMalloc((void **)&d_ov, 8 * 27 * k));
-        CUDA_TRY(c, cudaMalloc((void **)&d_ol, 4 * k));
-        CUDA_TRY(c, cudaMemcpy(d_rows, loc.data(), 8 * k, cudaMemcpyHostToDevice));
-        CUDA_TRY(c, launch_extract_rows(p.d_slice_off, p.d_row_len, p.d_col, p.d_val, d_rows, k,
-                                        d_oc, d_ov, d_ol, p.stream));
-        std::vector<int32_t> oc(27 * k), ol(k);
-        std::vector<double> ov(27 * k);
-        CUDA_TRY(c, cudaStreamSynchronize(p.stream));
-        CUDA_TRY(c, cudaMemcpy(oc.data(), d_oc, 4 * 27 * k, cudaMemcpyDeviceToHost));
-        CUDA_TRY(c, cudaMemcpy(ov.data(), d_ov, 8 * 27 * k, cudaMemcpyDeviceToHost));
-        CUDA_TRY(c, cudaMemcpy(ol.data(), d_ol, 4 * k, cudaMemcpyDeviceToHost));
-        cudaFree(d_rows);
-        cudaFree(d_oc);
-        cudaFree(d_ov);
-        cudaFree(d_ol);
-        for (int64_t j = 0; j < k; ++j) {
+        std::vector<int32_t> oc, ol;
+        std::vector<double> ov;
+        TRY(extract_part_rows(c, p, loc, oc, ov, ol));
+        for (size_t j = 0; j < loc.size(); ++j) {
             const int64_t i = which[j];
             lens[i] = ol[j];
             for (int e = 0; e < ol[j]; ++e) {
-                cols[27 * i + e] = gid_of_local(p.plan, oc[27 * j + e]);
+                cols[27 * i + e] = p.plan.col_to_gid(oc[27 * j + e]);
                 vals[27 * i + e] = ov[27 * j + e];
             }
         }
@@ -1069,10 +1157,15 @@ static int get_vec(minife_ctx *c, double *out, double *Part::*member) {
     std::vector<double> tmp;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        tmp.resize(p.rows);
-        CUDA_TRY(c, cudaMemcpy(tmp.data(), p.*member, 8 * p.rows, cudaMemcpyDeviceToHost));
-        if (c->mode == MINIFE_MODE_RANK) memcpy(out, tmp.data(), 8 * p.rows);
-        else scatter_owned(p.plan, tmp.data(), out);
+        CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+        if (c->mode == MINIFE_MODE_RANK || (c->parts.size() == 1 && p.ncols == p.rows)) {
+            // rows already in output order: copy straight into the caller's buffer
+            CUDA_TRY(c, cudaMemcpy(out, p.*member, 8 * p.rows, cudaMemcpyDeviceToHost));
+        } else {
+            tmp.resize(p.rows);
+            CUDA_TRY(c, cudaMemcpy(tmp.data(), p.*member, 8 * p.rows, cudaMemcpyDeviceToHost));
+            scatter_owned(p.plan, tmp.data(), out);
+        }
     }
     return MINIFE_OK;
 }
@@ -1105,7 +1198,7 @@ extern "C" int minife_get_owned_ids(const minife_ctx *c, int64_t *gids) {
     if (!c || !gids) return MINIFE_EINVAL;
     int64_t o = 0;
     for (auto &p : c->parts)
-        for (int64_t l = 0; l < p.rows; ++l) gids[o++] = gid_of_local(p.plan, l);
+        for (int64_t l = 0; l < p.rows; ++l) gids[o++] = gid_of_row(p.plan, l);
     return MINIFE_OK;
 }
 
@@ -1117,8 +1210,8 @@ extern "C" int minife_plan(int nx, int ny, int nz, int world, int rank, minife_p
     if (!out || validate_mesh(nx, ny, nz) != MINIFE_OK) return MINIFE_EINVAL;
     Plan pl;
     if (!build_plan(Mesh{nx, ny, nz}, world, rank, pl)) return MINIFE_EINVAL;
+    // CRS-format SELL entries from the closed-form row lengths (max per 32-row slice)
     int64_t entries = 0;
-    // SELL entries from the closed-form row lengths (max per 32-row slice)
     {
         const Mesh m{nx, ny, nz};
         int64_t r = 0, w = 0;

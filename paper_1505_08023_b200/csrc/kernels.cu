@@ -4,12 +4,15 @@
 // and sum written with __dmul_rn/__dadd_rn/__dsub_rn (never contracted to FMA; the library
 // is also built with -fmad=false), subnormals kept.  Dots are exactly rounded (exact.cuh).
 //
-// Layout: SELL-32, one slice = 32 consecutive local rows; slice s holds
-// width_s = max row length columns, stored k-major: entry k of row 32s+lane lives at
-// slice_off[s] + 32k + lane, so a warp's loads of one k are one contiguous 256 B (val) /
-// 128 B (col) segment.  Entries of a row are in ascending GLOBAL column (C4 order); padding
-// entries (k >= row_len) have val 0 and col = a valid index and are never added.
+// Layout: rows = owned nodes (owned-box order), columns = extended box
+// (owned + one-node halo shell).  Both matrix formats are SELL-32: slice s = rows 32s..32s+31,
+// stored k-major so a warp's load of entry k is one contiguous 256 B (val) / 128 B (index)
+// segment.  Entries of a row are kept in ascending GLOBAL column (C4 order); absent/padding
+// entries are never added (row-length predicate or presence mask).
 #include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
 
 #include "exact.cuh"
 #include "kernels.h"
@@ -30,43 +33,66 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 __device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
     double v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-                 : "=d"(v) : "l"(p), "l"(pol));
+        : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ int ld_stream(const int32_t *p, uint64_t pol) {
     int v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
-                 : "=r"(v) : "l"(p), "l"(pol));
+        : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_stream(const uint32_t *p, uint64_t pol) {
+    unsigned v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 
 // P:36 boundary: every surface node is constrained; value 1 on the plane x = 1 (G4).
-__device__ __forceinline__ bool on_boundary(int64_t ix, int64_t iy, int64_t iz, int nx, int ny,
-                                            int nz) {
+__device__ __forceinline__ bool on_boundary(int ix, int iy, int iz, int nx, int ny, int nz) {
     return ix == 0 || ix == nx || iy == 0 || iy == ny || iz == 0 || iz == nz;
 }
 
+// owned row l -> owned-box coordinates (32-bit arithmetic: a part has < 2^31 rows)
+__device__ __forceinline__ void row_coords(const Geom &g, int64_t l, int &lx, int &ly, int &lz) {
+    const unsigned u = (unsigned)l;
+    const unsigned line = u / (unsigned)g.own_n[0];
+    lx = (int)(u - line * (unsigned)g.own_n[0]);
+    const unsigned plane = line / (unsigned)g.own_n[1];
+    ly = (int)(line - plane * (unsigned)g.own_n[1]);
+    lz = (int)plane;
+}
+
+// owned row l -> extended-box column
+__device__ __forceinline__ int64_t row_to_col(const Geom &g, int64_t l) {
+    int lx, ly, lz;
+    row_coords(g, l, lx, ly, lz);
+    return (int64_t)(lx + g.off[0]) +
+           (int64_t)g.ext_n[0] * ((int64_t)(ly + g.off[1]) + (int64_t)g.ext_n[1] * (lz + g.off[2]));
+}
+
 // ----------------------------------------------------------------------------------------
-// a0.2: row lengths and SELL slice widths
+// a0.2: row lengths and SELL slice widths (CRS format)
 // ----------------------------------------------------------------------------------------
 
 // Row length of node (ix,iy,iz) = c(ix) c(iy) c(iz), c = 2 on a boundary plane else 3
 // (Fig 3.6's in-range count, closed form).
-__global__ void k_rowlen_widths(AsmArgs a, uint8_t *row_len, uint8_t *width, int64_t nslices) {
+__global__ void k_rowlen_widths(Geom g, uint8_t *row_len, uint8_t *width, int64_t nslices) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t slice = row >> 5;
     if (slice >= nslices) return;
     int len = 0;
-    if (row < a.rows) {
-        const int64_t lx = row % a.own_n[0], ly = (row / a.own_n[0]) % a.own_n[1],
-                      lz = row / (a.own_n[0] * a.own_n[1]);
-        const int64_t ix = a.own_lo[0] + lx, iy = a.own_lo[1] + ly, iz = a.own_lo[2] + lz;
-        const int cx = (ix == 0 || ix == a.nx) ? 2 : 3;
-        const int cy = (iy == 0 || iy == a.ny) ? 2 : 3;
-        const int cz = (iz == 0 || iz == a.nz) ? 2 : 3;
+    if (row < g.rows) {
+        int lx, ly, lz;
+        row_coords(g, row, lx, ly, lz);
+        const int ix = g.own_lo[0] + lx, iy = g.own_lo[1] + ly, iz = g.own_lo[2] + lz;
+        const int cx = (ix == 0 || ix == g.nx) ? 2 : 3;
+        const int cy = (iy == 0 || iy == g.ny) ? 2 : 3;
+        const int cz = (iz == 0 || iz == g.nz) ? 2 : 3;
         len = cx * cy * cz;
-        row_len[row] = (uint8_t)len;
     }
+    row_len[row] = (uint8_t)len;        // padding lanes of the last slice: 0
     const int w = __reduce_max_sync(0xffffffffu, (unsigned)len);
     if ((threadIdx.x & 31) == 0) width[slice] = (uint8_t)w;
 }
@@ -94,88 +120,101 @@ __device__ void element_operator(int nx, int ny, int nz, double K[8]) {
     }
 }
 
-// One thread per local row.  Entry (i,j) = fold from +0.0 of K(d(i,j)) over the c(i,j)
-// elements that share nodes i and j (C2; every term is the same K(d), the count is the
-// per-axis product of 1 (coordinates differ) or #elements on that axis containing i).
-// Then C3: constrained row -> identity row, b = v; free row -> for constrained columns in
-// ascending global order b = fl(b - fl(A v)), then A = +0.0.
+// One thread per local row (all 32 lanes of the last slice run: padding lanes write the
+// slice's padding).  Entry (i,j) = fold from +0.0 of K(d(i,j)) over the c(i,j) elements that
+// share nodes i and j (C2: every term is the same K(d); c = per-axis product of 1 where the
+// coordinates differ, else the number of elements on that axis containing i).  Then C3:
+// constrained row -> identity row, b = v; free row -> for constrained columns in ascending
+// global order b = fl(b - fl(A v)), then A = +0.0.  The pattern (incl. zeros) is kept.
 __global__ void k_assemble(AsmArgs a) {
+    const Geom &g = a.g;
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nslices = (a.rows + 31) >> 5;
+    const int64_t nslices = (g.rows + 31) >> 5;
     if ((row >> 5) >= nslices) return;
     const int lane = (int)(row & 31);
     const int64_t s = row >> 5;
-    const int64_t base = a.slice_off[s] + lane;
-    const int w = (int)((a.slice_off[s + 1] - a.slice_off[s]) >> 5);
-    if (row >= a.rows) {                           // padding lanes of the last slice
-        for (int k = 0; k < w; ++k) {
-            a.col[base + 32 * k] = 0;
-            a.val[base + 32 * k] = 0.0;
+    if (row >= g.rows) {                           // padding lanes of the last slice
+        if (a.fmt == FMT_CRS) {
+            const int64_t base = a.slice_off[s] + lane;
+            const int w = (int)((a.slice_off[s + 1] - a.slice_off[s]) >> 5);
+            for (int k = 0; k < w; ++k) {
+                a.col[base + 32 * k] = 0;
+                a.val[base + 32 * k] = 0.0;
+            }
+        } else {
+            for (int t = 0; t < 27; ++t) a.val[(27 * s + t) * 32 + lane] = 0.0;
+            for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
+            a.mask[row] = 0u;                      // mask is padded to 32 * slices
         }
         return;
     }
     double K[8];
-    element_operator(a.nx, a.ny, a.nz, K);
-    const int64_t NX = a.nx + 1, NY = a.ny + 1, NZ = a.nz + 1;
-    const int64_t lx = row % a.own_n[0], ly = (row / a.own_n[0]) % a.own_n[1],
-                  lz = row / (a.own_n[0] * a.own_n[1]);
-    const int64_t ix = a.own_lo[0] + lx, iy = a.own_lo[1] + ly, iz = a.own_lo[2] + lz;
-    const bool row_bc = on_boundary(ix, iy, iz, a.nx, a.ny, a.nz);
-    const int n_el[3] = {(ix > 0) + (ix < a.nx), (iy > 0) + (iy < a.ny), (iz > 0) + (iz < a.nz)};
+    element_operator(g.nx, g.ny, g.nz, K);
+    int lx, ly, lz;
+    row_coords(g, row, lx, ly, lz);
+    const int ix = g.own_lo[0] + lx, iy = g.own_lo[1] + ly, iz = g.own_lo[2] + lz;
+    // extended-box coordinates of the row's node
+    const int ex = lx + g.off[0], ey = ly + g.off[1], ez = lz + g.off[2];
+    const bool row_bc = on_boundary(ix, iy, iz, g.nx, g.ny, g.nz);
+    const int n_el[3] = {(ix > 0) + (ix < g.nx), (iy > 0) + (iy < g.ny), (iz > 0) + (iz < g.nz)};
     double b = 0.0;
-    int k = 0;
+    int k = 0;                                     // CRS entry counter
+    uint32_t mask = 0;
     for (int dz = -1; dz <= 1; ++dz) {
-        const int64_t jz = iz + dz;
-        if (jz < 0 || jz >= NZ) continue;
         for (int dy = -1; dy <= 1; ++dy) {
-            const int64_t jy = iy + dy;
-            if (jy < 0 || jy >= NY) continue;
+            const int jgrp = (dz + 1) * 3 + (dy + 1);
+            const int jy = iy + dy, jz = iz + dz;
+            const bool grp_in = jy >= 0 && jy <= g.ny && jz >= 0 && jz <= g.nz;
+            // run start: extended column of (x-1, y+dy, z+dz); never dereferenced when the
+            // dx = -1 slot is absent
+            const int64_t start = (int64_t)(ex - 1) +
+                                  (int64_t)g.ext_n[0] * ((int64_t)(ey + dy) +
+                                                         (int64_t)g.ext_n[1] * (ez + dz));
+            if (a.fmt == FMT_SEG) a.seg[(9 * s + jgrp) * 32 + lane] = grp_in ? (int32_t)start : 0;
             for (int dx = -1; dx <= 1; ++dx) {
-                const int64_t jx = ix + dx;
-                if (jx < 0 || jx >= NX) continue;
+                const int t = jgrp * 3 + (dx + 1);
+                const int jx = ix + dx;
+                const bool in = grp_in && jx >= 0 && jx <= g.nx;
+                if (!in) {
+                    if (a.fmt == FMT_SEG) a.val[(27 * s + t) * 32 + lane] = 0.0;
+                    continue;
+                }
                 const int c = (dx ? 1 : n_el[0]) * (dy ? 1 : n_el[1]) * (dz ? 1 : n_el[2]);
                 const double Kd = K[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)];
                 double v = 0.0;
-                for (int t = 0; t < c; ++t) v = __dadd_rn(v, Kd);
-                // local column: owned box index, or the external slot (binary search)
-                int32_t lc;
-                const int64_t ox = jx - a.own_lo[0], oy = jy - a.own_lo[1], oz = jz - a.own_lo[2];
-                if (ox >= 0 && ox < a.own_n[0] && oy >= 0 && oy < a.own_n[1] && oz >= 0 &&
-                    oz < a.own_n[2]) {
-                    lc = (int32_t)(ox + a.own_n[0] * (oy + a.own_n[1] * oz));
-                } else {
-                    const int64_t g = jx + NX * (jy + NY * jz);
-                    int64_t lo = 0, hi = a.n_ext - 1;
-                    lc = -1;
-                    while (lo <= hi) {
-                        const int64_t mid = (lo + hi) >> 1;
-                        const int64_t gm = a.ext_sorted_gid[mid];
-                        if (gm == g) {
-                            lc = a.ext_sorted_slot[mid];
-                            break;
-                        }
-                        if (gm < g) lo = mid + 1;
-                        else hi = mid - 1;
-                    }
-                }
+                for (int q = 0; q < c; ++q) v = __dadd_rn(v, Kd);
                 if (row_bc) {
                     v = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
-                } else if (on_boundary(jx, jy, jz, a.nx, a.ny, a.nz)) {
-                    const double bv = (jx == a.nx) ? 1.0 : 0.0;
+                } else if (on_boundary(jx, jy, jz, g.nx, g.ny, g.nz)) {
+                    const double bv = (jx == g.nx) ? 1.0 : 0.0;
                     b = __dsub_rn(b, __dmul_rn(v, bv));
                     v = 0.0;
                 }
-                a.col[base + 32 * k] = lc;
-                a.val[base + 32 * k] = v;
+                if (a.fmt == FMT_CRS) {
+                    const int64_t base = a.slice_off[s] + lane;
+                    a.col[base + 32 * k] = (int32_t)(start + dx + 1);
+                    a.val[base + 32 * k] = v;
+                } else {
+                    a.val[(27 * s + t) * 32 + lane] = v;
+                    mask |= 1u << t;
+                }
                 ++k;
             }
         }
     }
-    for (int kk = k; kk < w; ++kk) {                  // padding: own row, value 0
-        a.col[base + 32 * kk] = (int32_t)row;
-        a.val[base + 32 * kk] = 0.0;
+    if (a.fmt == FMT_CRS) {
+        const int64_t base = a.slice_off[s] + lane;
+        const int w = (int)((a.slice_off[s + 1] - a.slice_off[s]) >> 5);
+        const int32_t own = (int32_t)((int64_t)ex + (int64_t)g.ext_n[0] *
+                                      ((int64_t)ey + (int64_t)g.ext_n[1] * ez));
+        for (int kk = k; kk < w; ++kk) {           // padding: own column, value 0
+            a.col[base + 32 * kk] = own;
+            a.val[base + 32 * kk] = 0.0;
+        }
+    } else {
+        a.mask[row] = mask;
     }
-    if (row_bc) b = (ix == a.nx) ? 1.0 : 0.0;
+    if (row_bc) b = (ix == g.nx) ? 1.0 : 0.0;
     a.b[row] = b;
 }
 
@@ -183,12 +222,14 @@ __global__ void k_assemble(AsmArgs a) {
 // a2: SpMV  y = A x  (+ exact pAp epilogue)
 // ----------------------------------------------------------------------------------------
 
-// C4 per row: s = +0.0; for stored entries in order, s = fl(s + fl(a * x_col)); padding is
-// skipped by the row-length predicate (so a -0.0 row sum is never turned into +0.0).
+// C4 per row: s = +0.0; for stored entries in ascending global column, s = fl(s + fl(a x));
+// absent / padding entries are skipped by predicate (a -0.0 row sum stays -0.0).
 // One warp per slice, one lane per row; warps walk the slices grid-stride so each thread's
 // expansion absorbs many rows before the single flush.
-template <bool DOT>
-__global__ void __launch_bounds__(SPMV_THREADS) k_spmv(SpmvArgs a) {
+
+// CRS format (Fig 3.1 on SELL-32): 12 B per stored entry.
+template <bool DOT, bool IDENT>
+__global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
     if (DOT) {
         if (a.st && a.st->done) return;
@@ -203,14 +244,15 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv(SpmvArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warps_per_block = blockDim.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * warps_per_block;
-    for (int64_t s = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5); s < a.nslices;
+    const Matrix &m = a.m;
+    for (int64_t s = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5); s < m.nslices;
          s += nw) {
-        const int64_t off = a.slice_off[s];
-        const int w = (int)((a.slice_off[s + 1] - off) >> 5);
+        const int64_t off = m.slice_off[s];
+        const int w = (int)((m.slice_off[s + 1] - off) >> 5);
         const int64_t row = s * 32 + lane;
-        const int len = (row < a.rows) ? (int)a.row_len[row] : 0;
-        const double *v = a.val + off + lane;
-        const int32_t *c = a.col + off + lane;
+        const int len = (row < m.rows) ? (int)m.row_len[row] : 0;
+        const double *v = m.val + off + lane;
+        const int32_t *c = m.col + off + lane;
         double sum = 0.0;
         if (w == 27) {
             double vv[27];
@@ -234,9 +276,65 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv(SpmvArgs a) {
                 if (k < len) sum = __dadd_rn(sum, __dmul_rn(vk, __ldg(a.x + ck)));
             }
         }
-        if (row < a.rows) {
+        if (row < m.rows) {
             a.y[row] = sum;
-            if (DOT) ex.add(__dmul_rn(__ldg(a.x + row), sum), sacc);
+            if (DOT) {
+                const double pr = __ldg(a.x + (IDENT ? row : row_to_col(a.g, row)));
+                ex.add(__dmul_rn(pr, sum), sacc);
+            }
+        }
+    }
+    if (DOT) {
+        ex.flush(sacc);
+        __syncthreads();
+        acc_merge_to_global(sacc, a.acc);
+    }
+}
+
+// Segment format (the paper's BCRS, Fig 3.2, on SELL-32): per row 27 value slots in stencil
+// order (dz, dy, dx), one int32 start column per x-run (dz, dy) and a 27-bit presence mask:
+// entry t = 3j + e has column seg[j] + e.  8 B per stored value + 4 B per segment.
+template <bool DOT>
+__global__ void __launch_bounds__(SPMV_THREADS) k_spmv_seg(SpmvArgs a) {
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    if (DOT) {
+        if (a.st && a.st->done) return;
+        acc_zero_shared(sacc);
+        if (blockIdx.x == 0 && a.acc_zero)
+            for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+        __syncthreads();
+    }
+    Expansion ex;
+    ex.init();
+    const uint64_t pol = evict_first_policy();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_per_block = blockDim.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * warps_per_block;
+    const Matrix &m = a.m;
+    for (int64_t s = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5); s < m.nslices;
+         s += nw) {
+        const int64_t row = s * 32 + lane;
+        const bool live = row < m.rows;
+        const unsigned msk = live ? ld_stream(m.mask + row, pol) : 0u;
+        const int32_t *sp = m.seg + 9 * s * 32 + lane;
+        const double *vp = m.val + 27 * s * 32 + lane;
+        int st[9];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) st[j] = ld_stream(sp + 32 * j, pol);
+        double vv[27];
+#pragma unroll
+        for (int t = 0; t < 27; ++t) vv[t] = ld_stream(vp + 32 * t, pol);
+        double xv[27];
+#pragma unroll
+        for (int t = 0; t < 27; ++t)
+            xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + st[t / 3] + (t % 3)) : 0.0;
+        double sum = 0.0;
+#pragma unroll
+        for (int t = 0; t < 27; ++t)
+            if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vv[t], xv[t]));
+        if (live) {
+            a.y[row] = sum;
+            if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);   // slot 13 = the diagonal
         }
     }
     if (DOT) {
@@ -247,9 +345,190 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv(SpmvArgs a) {
 }
 
 // ----------------------------------------------------------------------------------------
+// a2, TMA-pipelined: the matrix stream is moved by the bulk-copy engine into shared memory
+// (cp.async.bulk + mbarrier transaction counts), decoupled from the registers of the warps
+// that compute.  Persistent grid, one CTA per SM: warp TMA_WARPS is the producer, warps
+// 0..TMA_WARPS-1 consume one slice each per tile.  A tile = TILE consecutive slices, whose
+// val / index / mask bytes are contiguous in HBM, so it is 3 bulk copies.
+// ----------------------------------------------------------------------------------------
+
+constexpr int TILE = 8;                    // slices per tile (= consumer warps)
+constexpr int TMA_WARPS = TILE;
+constexpr int TMA_THREADS = 32 * (TMA_WARPS + 1);
+constexpr int SEG_STAGES = 3;
+constexpr int CRS_STAGES = 2;
+// per-stage bytes: SEG = 27 val + 9 seg + 1 mask words per row; CRS = <=27 (val + col) + len
+constexpr int SEG_VAL_B = TILE * 27 * 32 * 8, SEG_SEG_B = TILE * 9 * 32 * 4,
+              SEG_MSK_B = TILE * 32 * 4;
+constexpr int SEG_STAGE_B = SEG_VAL_B + SEG_SEG_B + SEG_MSK_B;          // 65536
+constexpr int CRS_VAL_B = TILE * 27 * 32 * 8, CRS_COL_B = TILE * 27 * 32 * 4,
+              CRS_LEN_B = TILE * 32;
+constexpr int CRS_STAGE_B = CRS_VAL_B + CRS_COL_B + CRS_LEN_B;          // 83200
+constexpr int SEG_SMEM = SEG_STAGES * SEG_STAGE_B;
+constexpr int CRS_SMEM = CRS_STAGES * CRS_STAGE_B;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar`, evict-first in L2
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <bool DOT, int FMT, bool IDENT>
+__global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
+    constexpr int STAGES = FMT == FMT_SEG ? SEG_STAGES : CRS_STAGES;
+    constexpr int STAGE_B = FMT == FMT_SEG ? SEG_STAGE_B : CRS_STAGE_B;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    if (DOT && a.st && a.st->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], TMA_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (DOT) {
+        acc_zero_shared(sacc);
+        if (blockIdx.x == 0 && a.acc_zero)
+            for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    }
+    __syncthreads();
+    const Matrix &m = a.m;
+    const int64_t ntiles = (m.nslices + TILE - 1) / TILE;
+
+    if (warp == TMA_WARPS) {
+        // ---------------- producer: one elected lane issues the bulk copies -------------
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int64_t i = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int st = (int)(i % STAGES);
+                if (i >= STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / STAGES) & 1) ^ 1));
+                const int64_t s0 = tile * TILE;
+                const int64_t rem = m.nslices - s0;
+                const int nsl = rem < TILE ? (int)rem : TILE;
+                unsigned char *buf = smem + (size_t)st * STAGE_B;
+                if (FMT == FMT_SEG) {
+                    const uint32_t bv = nsl * 27 * 32 * 8, bs = nsl * 9 * 32 * 4,
+                                   bm = nsl * 32 * 4;
+                    mbar_expect_tx(&full_bar[st], bv + bs + bm);
+                    bulk_g2s(buf, m.val + s0 * 27 * 32, bv, &full_bar[st], pol);
+                    bulk_g2s(buf + SEG_VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
+                    bulk_g2s(buf + SEG_VAL_B + SEG_SEG_B, m.mask + s0 * 32, bm, &full_bar[st],
+                             pol);
+                } else {
+                    const int64_t e0 = m.slice_off[s0], e1 = m.slice_off[s0 + nsl];
+                    const uint32_t ne = (uint32_t)(e1 - e0);
+                    const uint32_t bv = ne * 8, bc = ne * 4, bl = nsl * 32;
+                    mbar_expect_tx(&full_bar[st], bv + bc + bl);
+                    bulk_g2s(buf, m.val + e0, bv, &full_bar[st], pol);
+                    bulk_g2s(buf + CRS_VAL_B, m.col + e0, bc, &full_bar[st], pol);
+                    bulk_g2s(buf + CRS_VAL_B + CRS_COL_B, m.row_len + s0 * 32, bl, &full_bar[st],
+                             pol);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers: one slice per warp per tile, operands from smem -----
+        Expansion ex;
+        ex.init();
+        int64_t i = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int st = (int)(i % STAGES);
+            mbar_wait(&full_bar[st], (uint32_t)((i / STAGES) & 1));
+            const int64_t s = tile * TILE + warp;
+            if (s < m.nslices) {
+                const unsigned char *buf = smem + (size_t)st * STAGE_B;
+                const int64_t row = s * 32 + lane;
+                double sum = 0.0, pdiag = 0.0;
+                if (FMT == FMT_SEG) {
+                    const double *vs = reinterpret_cast<const double *>(buf) + warp * 27 * 32 + lane;
+                    const int32_t *ss =
+                        reinterpret_cast<const int32_t *>(buf + SEG_VAL_B) + warp * 9 * 32 + lane;
+                    const unsigned msk = reinterpret_cast<const uint32_t *>(
+                        buf + SEG_VAL_B + SEG_SEG_B)[warp * 32 + lane];
+                    int sg[9];
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
+                    double xv[27];
+#pragma unroll
+                    for (int t = 0; t < 27; ++t)
+                        xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
+#pragma unroll
+                    for (int t = 0; t < 27; ++t)
+                        if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * t], xv[t]));
+                    pdiag = xv[13];
+                } else {
+                    const int64_t e0 = m.slice_off[tile * TILE];
+                    const int64_t so = m.slice_off[s] - e0;
+                    const int w = (int)((m.slice_off[s + 1] - m.slice_off[s]) >> 5);
+                    const double *vs = reinterpret_cast<const double *>(buf) + so + lane;
+                    const int32_t *cs = reinterpret_cast<const int32_t *>(buf + CRS_VAL_B) + so + lane;
+                    const int len = (buf + CRS_VAL_B + CRS_COL_B)[warp * 32 + lane];
+                    if (w == 27) {
+                        double xv[27];
+#pragma unroll
+                        for (int k = 0; k < 27; ++k) xv[k] = k < len ? __ldg(a.x + cs[32 * k]) : 0.0;
+#pragma unroll
+                        for (int k = 0; k < 27; ++k)
+                            if (k < len) sum = __dadd_rn(sum, __dmul_rn(vs[32 * k], xv[k]));
+                    } else {
+                        for (int k = 0; k < len; ++k)
+                            sum = __dadd_rn(sum, __dmul_rn(vs[32 * k], __ldg(a.x + cs[32 * k])));
+                    }
+                    if (DOT && row < m.rows)
+                        pdiag = __ldg(a.x + (IDENT ? row : row_to_col(a.g, row)));
+                }
+                if (row < m.rows) {
+                    a.y[row] = sum;
+                    if (DOT) ex.add(__dmul_rn(pdiag, sum), sacc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+        if (DOT) ex.flush(sacc);
+    }
+    if (DOT) {
+        __syncthreads();
+        acc_merge_to_global(sacc, a.acc);
+    }
+}
+
+// ----------------------------------------------------------------------------------------
 // CG init (C6 step 1): x = 0, r = b, p = b, rr = dot(r, r)
 // ----------------------------------------------------------------------------------------
 
+template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
     acc_zero_shared(sacc);
@@ -257,11 +536,11 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     Expansion ex;
     ex.init();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.rows; i += stride) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride) {
         const double bi = a.b[i];
         a.x[i] = 0.0;
         a.r[i] = bi;
-        a.p[i] = bi;
+        a.p[IDENT ? i : row_to_col(a.g, i)] = bi;
         ex.add(__dmul_rn(bi, bi), sacc);
     }
     ex.flush(sacc);
@@ -294,6 +573,14 @@ __global__ void k_init_finalize(UpdArgs a, double tol) {
 // a3 + a4: finalise pAp -> alpha; x += alpha p; r -= alpha Ap; rr' = dot(r, r)
 // ----------------------------------------------------------------------------------------
 
+__device__ __forceinline__ void xr_step(double &x, double &r, double p, double ap, double alpha,
+                                        Expansion &ex, unsigned long long *sacc) {
+    x = __dadd_rn(x, __dmul_rn(alpha, p));
+    r = __dsub_rn(r, __dmul_rn(alpha, ap));
+    ex.add(__dmul_rn(r, r), sacc);
+}
+
+template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_xr(UpdArgs a, int k) {
     __shared__ unsigned long long sacc[ACC_WORDS];
     __shared__ double s_alpha;
@@ -331,13 +618,51 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_xr(UpdArgs a, int k) {
     const double alpha = s_alpha;
     Expansion ex;
     ex.init();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.rows; i += stride) {
-        const double pi = a.p[i], api = a.Ap[i];
-        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pi));
-        const double ri = __dsub_rn(a.r[i], __dmul_rn(alpha, api));
-        a.r[i] = ri;
-        ex.add(__dmul_rn(ri, ri), sacc);
+    const int64_t rows = a.g.rows;
+    if (IDENT) {
+        // 16-byte vector accesses, two pairs in flight per thread
+        const int64_t n2 = rows >> 1;
+        double2 *x2 = reinterpret_cast<double2 *>(a.x);
+        double2 *r2 = reinterpret_cast<double2 *>(a.r);
+        const double2 *p2 = reinterpret_cast<const double2 *>(a.p);
+        const double2 *q2 = reinterpret_cast<const double2 *>(a.Ap);
+        int64_t i = tid;
+        for (; i + stride < n2; i += 2 * stride) {
+            double2 xa = x2[i], ra = r2[i], pa = p2[i], qa = q2[i];
+            double2 xb = x2[i + stride], rb = r2[i + stride], pb = p2[i + stride],
+                    qb = q2[i + stride];
+            xr_step(xa.x, ra.x, pa.x, qa.x, alpha, ex, sacc);
+            xr_step(xa.y, ra.y, pa.y, qa.y, alpha, ex, sacc);
+            xr_step(xb.x, rb.x, pb.x, qb.x, alpha, ex, sacc);
+            xr_step(xb.y, rb.y, pb.y, qb.y, alpha, ex, sacc);
+            x2[i] = xa;
+            r2[i] = ra;
+            x2[i + stride] = xb;
+            r2[i + stride] = rb;
+        }
+        for (; i < n2; i += stride) {
+            double2 xa = x2[i], ra = r2[i], pa = p2[i], qa = q2[i];
+            xr_step(xa.x, ra.x, pa.x, qa.x, alpha, ex, sacc);
+            xr_step(xa.y, ra.y, pa.y, qa.y, alpha, ex, sacc);
+            x2[i] = xa;
+            r2[i] = ra;
+        }
+        if ((rows & 1) && tid == 0) {
+            const int64_t j = rows - 1;
+            double xj = a.x[j], rj = a.r[j];
+            xr_step(xj, rj, a.p[j], a.Ap[j], alpha, ex, sacc);
+            a.x[j] = xj;
+            a.r[j] = rj;
+        }
+    } else {
+        for (int64_t i = tid; i < rows; i += stride) {
+            double xi = a.x[i], ri = a.r[i];
+            xr_step(xi, ri, a.p[row_to_col(a.g, i)], a.Ap[i], alpha, ex, sacc);
+            a.x[i] = xi;
+            a.r[i] = ri;
+        }
     }
     ex.flush(sacc);
     __syncthreads();
@@ -348,6 +673,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_xr(UpdArgs a, int k) {
 // a5 + a6: finalise rr' -> hist[k], stop tests, beta; p = r + beta p
 // ----------------------------------------------------------------------------------------
 
+template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     __shared__ double s_beta;
     __shared__ int s_stop;
@@ -384,20 +710,50 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     if (blockIdx.x == 0 && a.acc_zero)
         for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     const double beta = s_beta;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.rows; i += stride)
-        a.p[i] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[i]));
+    const int64_t rows = a.g.rows;
+    if (IDENT) {
+        const int64_t n2 = rows >> 1;
+        double2 *p2 = reinterpret_cast<double2 *>(a.p);
+        const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
+        int64_t i = tid;
+        for (; i + stride < n2; i += 2 * stride) {
+            double2 pa = p2[i], ra = r2[i], pb = p2[i + stride], rb = r2[i + stride];
+            pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
+            pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
+            pb.x = __dadd_rn(rb.x, __dmul_rn(beta, pb.x));
+            pb.y = __dadd_rn(rb.y, __dmul_rn(beta, pb.y));
+            p2[i] = pa;
+            p2[i + stride] = pb;
+        }
+        for (; i < n2; i += stride) {
+            double2 pa = p2[i], ra = r2[i];
+            pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
+            pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
+            p2[i] = pa;
+        }
+        if ((rows & 1) && tid == 0) {
+            const int64_t j = rows - 1;
+            a.p[j] = __dadd_rn(a.r[j], __dmul_rn(beta, a.p[j]));
+        }
+    } else {
+        for (int64_t i = tid; i < rows; i += stride) {
+            const int64_t c = row_to_col(a.g, i);
+            a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[c]));
+        }
+    }
 }
 
 // ----------------------------------------------------------------------------------------
-// a1: halo pack / virtual-rank transport
+// a1: halo pack / unpack / virtual-rank transport
 // ----------------------------------------------------------------------------------------
 
-__global__ void k_pack(const double *__restrict__ src, const int32_t *__restrict__ idx,
-                       int64_t n, double *__restrict__ dst) {
+__global__ void k_move(const double *__restrict__ src, const int32_t *__restrict__ sidx,
+                       double *__restrict__ dst, const int32_t *__restrict__ didx, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        dst[i] = src[idx[i]];
+        dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i];
 }
 
 struct AccPtrs {
@@ -413,19 +769,29 @@ __global__ void k_vsum(AccPtrs ptrs, int nparts) {
     }
 }
 
-__global__ void k_extract_rows(const int64_t *slice_off, const uint8_t *row_len,
-                               const int32_t *col, const double *val, const int64_t *rows,
-                               int64_t n, int32_t *out_col, double *out_val, int32_t *out_len) {
+__global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t *out_col,
+                               double *out_val, int32_t *out_len) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t row = rows[i];
     const int64_t s = row >> 5, lane = row & 31;
-    const int len = row_len[row];
-    out_len[i] = len;
-    for (int k = 0; k < len; ++k) {
-        out_col[27 * i + k] = col[slice_off[s] + 32 * k + lane];
-        out_val[27 * i + k] = val[slice_off[s] + 32 * k + lane];
+    int len = 0;
+    if (m.fmt == FMT_CRS) {
+        len = m.row_len[row];
+        for (int k = 0; k < len; ++k) {
+            out_col[27 * i + k] = m.col[m.slice_off[s] + 32 * k + lane];
+            out_val[27 * i + k] = m.val[m.slice_off[s] + 32 * k + lane];
+        }
+    } else {
+        const unsigned msk = m.mask[row];
+        for (int t = 0; t < 27; ++t) {
+            if (!((msk >> t) & 1u)) continue;
+            out_col[27 * i + len] = m.seg[(9 * s + t / 3) * 32 + lane] + t % 3;
+            out_val[27 * i + len] = m.val[(27 * s + t) * 32 + lane];
+            ++len;
+        }
     }
+    out_len[i] = len;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -433,58 +799,111 @@ __global__ void k_extract_rows(const int64_t *slice_off, const uint8_t *row_len,
 // ----------------------------------------------------------------------------------------
 
 static int g_sms = 0;
-static int g_spmv_blocks_per_sm = 0;
-static int g_upd_blocks_per_sm = 0;
+static int g_spmv_bps[2] = {0, 0};
+static int g_upd_bps = 0;
 
 static void query_occupancy() {
     if (g_sms) return;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_spmv_blocks_per_sm, k_spmv<true>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_spmv_bps[0], k_spmv_crs<true, true>,
                                                   SPMV_THREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_blocks_per_sm, k_update_xr,
-                                                  UPD_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_spmv_bps[1], k_spmv_seg<true>,
+                                                  SPMV_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_bps, k_update_xr<true>, UPD_THREADS, 0);
     if (g_sms <= 0) g_sms = 148;
-    if (g_spmv_blocks_per_sm <= 0) g_spmv_blocks_per_sm = 1;
-    if (g_upd_blocks_per_sm <= 0) g_upd_blocks_per_sm = 1;
+    for (int f = 0; f < 2; ++f)
+        if (g_spmv_bps[f] <= 0) g_spmv_bps[f] = 1;
+    if (g_upd_bps <= 0) g_upd_bps = 1;
 }
 
-int spmv_grid(int64_t nslices) {
+int spmv_grid(int64_t nslices, int fmt) {
     query_occupancy();
     const int64_t need = (nslices + (SPMV_THREADS / 32) - 1) / (SPMV_THREADS / 32);
-    const int64_t full = (int64_t)g_sms * g_spmv_blocks_per_sm;
+    const int64_t full = (int64_t)g_sms * g_spmv_bps[fmt == FMT_SEG];
     return (int)(need < full ? (need > 0 ? need : 1) : full);
 }
 
 int stream_grid(int64_t rows) {
     query_occupancy();
     const int64_t need = (rows + UPD_THREADS - 1) / UPD_THREADS;
-    const int64_t full = (int64_t)g_sms * g_upd_blocks_per_sm;
+    const int64_t full = (int64_t)g_sms * g_upd_bps;
     return (int)(need < full ? (need > 0 ? need : 1) : full);
 }
 
-cudaError_t launch_rowlen_widths(const AsmArgs &a, uint8_t *row_len, uint8_t *width,
+cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width,
                                  int64_t nslices, cudaStream_t s) {
     const int64_t threads = nslices * 32;
-    k_rowlen_widths<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a, row_len, width, nslices);
+    k_rowlen_widths<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, row_len, width, nslices);
     return cudaGetLastError();
 }
 
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
-    const int64_t threads = ((a.rows + 31) >> 5) * 32;
+    const int64_t threads = ((a.g.rows + 31) >> 5) * 32;
     k_assemble<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 
+template <bool DOT, int FMT, bool IDENT>
+static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
+    constexpr int SMEM = FMT == FMT_SEG ? SEG_SMEM : CRS_SMEM;
+    static unsigned long long attr_set = 0;   // per instantiation, one bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!((attr_set >> (dev & 63)) & 1ull)) {
+        cudaError_t e = cudaFuncSetAttribute(k_spmv_tma<DOT, FMT, IDENT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << (dev & 63);
+    }
+    query_occupancy();
+    const int64_t ntiles = (a.m.nslices + TILE - 1) / TILE;
+    const int grid = (int)std::min<int64_t>(ntiles, g_sms);
+    k_spmv_tma<DOT, FMT, IDENT><<<grid > 0 ? grid : 1, TMA_THREADS, SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Kernel choice per format (measured on B200, 300^3, profiles/r01): SEG -> TMA pipeline
+// (1.105 ms vs 1.442 ms register-streaming); CRS -> register streaming (1.48 ms vs 1.77 ms
+// for its 2-stage TMA variant).  MINIFE_SPMV_IMPL=tma|reg overrides for experiments.
+static int spmv_impl(int fmt) {
+    static int forced = -2;
+    if (forced == -2) {
+        const char *e = getenv("MINIFE_SPMV_IMPL");
+        forced = !e ? -1 : (e[0] == 't' ? 1 : (e[0] == 'r' ? 0 : -1));
+    }
+    if (forced >= 0) return forced;
+    return fmt == FMT_SEG ? 1 : 0;
+}
+
 cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t s) {
-    if (with_dot) k_spmv<true><<<grid, SPMV_THREADS, 0, s>>>(a);
-    else k_spmv<false><<<grid, SPMV_THREADS, 0, s>>>(a);
+    if (spmv_impl(a.m.fmt) == 1) {
+        if (a.m.fmt == FMT_SEG)
+            return with_dot ? launch_tma<true, FMT_SEG, true>(a, s)
+                            : launch_tma<false, FMT_SEG, true>(a, s);
+        if (a.g.ident)
+            return with_dot ? launch_tma<true, FMT_CRS, true>(a, s)
+                            : launch_tma<false, FMT_CRS, true>(a, s);
+        return with_dot ? launch_tma<true, FMT_CRS, false>(a, s)
+                        : launch_tma<false, FMT_CRS, false>(a, s);
+    }
+    if (a.m.fmt == FMT_SEG) {
+        if (with_dot) k_spmv_seg<true><<<grid, SPMV_THREADS, 0, s>>>(a);
+        else k_spmv_seg<false><<<grid, SPMV_THREADS, 0, s>>>(a);
+    } else if (a.g.ident) {
+        if (with_dot) k_spmv_crs<true, true><<<grid, SPMV_THREADS, 0, s>>>(a);
+        else k_spmv_crs<false, true><<<grid, SPMV_THREADS, 0, s>>>(a);
+    } else {
+        if (with_dot) k_spmv_crs<true, false><<<grid, SPMV_THREADS, 0, s>>>(a);
+        else k_spmv_crs<false, false><<<grid, SPMV_THREADS, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s) {
-    k_init_vectors<<<grid, UPD_THREADS, 0, s>>>(a);
+    if (a.g.ident) k_init_vectors<true><<<grid, UPD_THREADS, 0, s>>>(a);
+    else k_init_vectors<false><<<grid, UPD_THREADS, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -494,21 +913,23 @@ cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s) {
 }
 
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    k_update_xr<<<grid, UPD_THREADS, 0, s>>>(a, k);
+    if (a.g.ident) k_update_xr<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    else k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
     return cudaGetLastError();
 }
 
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    k_update_p<<<grid, UPD_THREADS, 0, s>>>(a, k);
+    if (a.g.ident) k_update_p<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    else k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
     return cudaGetLastError();
 }
 
-cudaError_t launch_pack(const double *src, const int32_t *idx, int64_t n, double *dst,
-                        cudaStream_t s) {
+cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
+                        const int32_t *didx, int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     int grid = (int)((n + 255) / 256);
     if (grid > 1184) grid = 1184;
-    k_pack<<<grid, 256, 0, s>>>(src, idx, n, dst);
+    k_move<<<grid, 256, 0, s>>>(src, sidx, dst, didx, n);
     return cudaGetLastError();
 }
 
@@ -519,13 +940,11 @@ cudaError_t launch_vsum(unsigned long long *const *accs, int nparts, cudaStream_
     return cudaGetLastError();
 }
 
-cudaError_t launch_extract_rows(const int64_t *slice_off, const uint8_t *row_len,
-                                const int32_t *col, const double *val, const int64_t *rows,
-                                int64_t n, int32_t *out_col, double *out_val,
-                                int32_t *out_len, cudaStream_t s) {
+cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
+                                int32_t *out_col, double *out_val, int32_t *out_len,
+                                cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    k_extract_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(slice_off, row_len, col, val,
-                                                               rows, n, out_col, out_val,
+    k_extract_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(m, rows, n, out_col, out_val,
                                                                out_len);
     return cudaGetLastError();
 }

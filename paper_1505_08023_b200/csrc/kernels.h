@@ -5,6 +5,14 @@
 
 namespace minife {
 
+// Storage formats of the assembled matrix.
+//   FMT_CRS: SELL-32 with one int32 column per stored entry — the GPU form of the paper's CRS
+//            (Fig 3.1).
+//   FMT_SEG: SELL-32 with 27 value slots per row (stencil order), one int32 column per x-run
+//            ("non-zero segment") and a 27-bit presence mask — the GPU form of the paper's
+//            BCRS (Fig 3.2): "jas" = run start, the mask replaces "offsets".
+enum { FMT_CRS = 0, FMT_SEG = 1 };
+
 // Device-resident CG scalars of one part (C6).  Written only by CTA 0 of the kernel that
 // takes the decision; every CTA computes the same decision from the same exact values.
 struct CgState {
@@ -16,28 +24,45 @@ struct CgState {
     double pAp, alpha, beta;
 };
 
-struct AsmArgs {
-    int nx, ny, nz;
+// Row -> column map: rows are the owned box, columns the extended box (plan.h).
+struct Geom {
+    int nx, ny, nz;                     // global elements per axis
     int own_lo[3];
-    int64_t own_n[3];
-    int64_t rows;                       // owned rows
-    int64_t n_ext;
-    const int64_t *ext_sorted_gid;      // externals sorted by gid
-    const int32_t *ext_sorted_slot;     // their local column (n_owned + slot)
-    const int64_t *slice_off;           // [slices+1]
-    const uint8_t *row_len;             // [rows]
-    int32_t *col;                       // SELL, k-major per slice
+    int own_n[3];
+    int ext_lo[3];
+    int ext_n[3];
+    int off[3];                         // own_lo - ext_lo
+    int64_t rows, ncols;
+    int ident;                          // extended box == owned box (one part)
+};
+
+struct Matrix {
+    int fmt;
+    int64_t rows, nslices;
+    const double *val;                  // CRS: [slice_off[s] + 32k + lane]; SEG: [(27s + t)32 + lane]
+    const int64_t *slice_off;           // CRS only [nslices+1]
+    const uint8_t *row_len;             // CRS only [rows]
+    const int32_t *col;                 // CRS only
+    const int32_t *seg;                 // SEG only: [(9s + j)32 + lane], start column of run j
+    const uint32_t *mask;               // SEG only: [rows], bit t = slot t present
+};
+
+struct AsmArgs {
+    Geom g;
+    int fmt;
+    const int64_t *slice_off;           // CRS
+    uint8_t *row_len;                   // CRS
+    int32_t *col;                       // CRS
+    int32_t *seg;                       // SEG
+    uint32_t *mask;                     // SEG
     double *val;
     double *b;                          // [rows]
 };
 
 struct SpmvArgs {
-    int64_t rows, nslices;
-    const int64_t *slice_off;
-    const uint8_t *row_len;
-    const int32_t *col;
-    const double *val;
-    const double *x;                    // [rows + externals]
+    Matrix m;
+    Geom g;
+    const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
     unsigned long long *acc;            // pAp accumulator (DOT only)
     unsigned long long *acc_zero;       // accumulator to clear (CTA 0), may be null
@@ -45,10 +70,11 @@ struct SpmvArgs {
 };
 
 struct UpdArgs {
-    int64_t rows;
-    double *x, *r, *p;
-    const double *Ap;
-    const double *b;
+    Geom g;
+    double *x, *r;                      // [rows]
+    double *p;                          // [ncols], extended-box order
+    const double *Ap;                   // [rows]
+    const double *b;                    // [rows]
     unsigned long long *acc_in;         // finalised at kernel start
     unsigned long long *acc_out;        // accumulated by this kernel
     unsigned long long *acc_zero;       // cleared by CTA 0 (may be null)
@@ -57,7 +83,7 @@ struct UpdArgs {
 };
 
 // Setup (a0.2-a0.5)
-cudaError_t launch_rowlen_widths(const AsmArgs &a, uint8_t *row_len, uint8_t *width,
+cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width,
                                  int64_t nslices, cudaStream_t s);
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s);
 
@@ -68,19 +94,18 @@ cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s);
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s);
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s);
 
-// Halo / virtual transport
-cudaError_t launch_pack(const double *src, const int32_t *idx, int64_t n, double *dst,
-                        cudaStream_t s);
+// Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
+cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
+                        const int32_t *didx, int64_t n, cudaStream_t s);
 cudaError_t launch_vsum(unsigned long long *const *accs, int nparts, cudaStream_t s);
 
-// Parity helpers
-cudaError_t launch_extract_rows(const int64_t *slice_off, const uint8_t *row_len,
-                                const int32_t *col, const double *val, const int64_t *rows,
-                                int64_t n, int32_t *out_col, double *out_val,
-                                int32_t *out_len, cudaStream_t s);
+// Parity helper: rows[] (local) -> up to 27 (extended column, value) pairs each
+cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
+                                int32_t *out_col, double *out_val, int32_t *out_len,
+                                cudaStream_t s);
 
 // occupancy-derived grid sizes
-int spmv_grid(int64_t nslices);
+int spmv_grid(int64_t nslices, int fmt);
 int stream_grid(int64_t rows);
 
 constexpr int SPMV_THREADS = 256;

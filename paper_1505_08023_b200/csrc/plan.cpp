@@ -67,6 +67,19 @@ int64_t Plan::local_nnz() const {
     return n_owned == 0 ? 0 : prod;
 }
 
+// x-runs per row = (#present y-neighbors) * (#present z-neighbors): 9 inside, fewer on y/z
+// boundary planes; summed separably over the owned box.
+int64_t Plan::local_nns() const {
+    const int n[3] = {mesh.nx, mesh.ny, mesh.nz};
+    int64_t prod = own_n[0];
+    for (int k = 1; k < 3; ++k) {
+        int64_t s = 0;
+        for (int i = own_lo[k]; i <= own_hi[k]; ++i) s += (i == 0 || i == n[k]) ? 2 : 3;
+        prod *= s;
+    }
+    return n_owned == 0 ? 0 : prod;
+}
+
 // externals of rank r in slot order (owner rank, global id), with their owners
 static void externals_of(const Mesh &m, const std::vector<Box> &boxes, int r,
                          std::vector<int64_t> &gid, std::vector<int> &own) {
@@ -108,11 +121,25 @@ bool build_plan(const Mesh &m, int world, int rank, Plan &P) {
     P.world = world;
     if (!rcb(m, world, P.boxes)) return false;
     owned_box(m, P.boxes, rank, P.own_lo, P.own_hi);
-    for (int k = 0; k < 3; ++k) P.own_n[k] = (int64_t)P.own_hi[k] - P.own_lo[k] + 1;
+    const int64_t Nn[3] = {m.NX(), m.NY(), m.NZ()};
+    for (int k = 0; k < 3; ++k) {
+        P.own_n[k] = (int64_t)P.own_hi[k] - P.own_lo[k] + 1;
+        P.ext_lo[k] = P.own_lo[k] > 0 ? P.own_lo[k] - 1 : 0;
+        const int64_t ext_hi = std::min<int64_t>(P.own_hi[k] + 1, Nn[k] - 1);
+        P.ext_n[k] = ext_hi - P.ext_lo[k] + 1;
+        P.off[k] = P.own_lo[k] - P.ext_lo[k];
+    }
     P.n_owned = P.own_n[0] * P.own_n[1] * P.own_n[2];
+    P.n_cols = P.ext_n[0] * P.ext_n[1] * P.ext_n[2];
     std::vector<int> owners;
     externals_of(m, P.boxes, rank, P.ext_gid, owners);
     P.n_ext = (int64_t)P.ext_gid.size();
+    P.ext_pos.resize(P.n_ext);
+    for (int64_t i = 0; i < P.n_ext; ++i) {
+        const int64_t g = P.ext_gid[i];
+        P.ext_pos[i] = P.ext_col(g % Nn[0], (g / Nn[0]) % Nn[1], g / (Nn[0] * Nn[1]));
+    }
+    if (P.n_owned + P.n_ext != P.n_cols) return false;   // extended box == owned ∪ externals
     for (size_t i = 0; i < owners.size(); ++i) {
         if (P.nbr.empty() || P.nbr.back() != owners[i]) {
             P.nbr.push_back(owners[i]);

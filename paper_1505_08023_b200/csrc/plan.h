@@ -25,14 +25,27 @@ struct Box {
 // ranks.
 bool rcb(const Mesh &m, int p, std::vector<Box> &boxes);
 
+// Local numbering:
+//   rows    = owned nodes, owned-box order (= ascending global id);
+//   columns = the EXTENDED box = owned box grown by one node per side, clipped to the domain,
+//             in its own x-fastest order.  It holds exactly owned ∪ externals, and every
+//             x-run of the 27-point stencil is a run of consecutive columns, also across rank
+//             boundaries — what lets one int32 index per run (the paper's BCRS segment,
+//             P:116-124) describe every row.
+//   halo slots (externals) keep the S:99 order (owner rank, global id) for the wire; ext_pos
+//             maps slot -> extended column.
 struct Plan {
     Mesh mesh;
     int rank = 0, world = 1;
     std::vector<Box> boxes;               // all ranks' element boxes
     int own_lo[3], own_hi[3];             // owned node box, inclusive
     int64_t own_n[3];
-    int64_t n_owned = 0, n_ext = 0;
+    int ext_lo[3];                        // extended box origin (global node coords)
+    int64_t ext_n[3];
+    int off[3];                           // own_lo - ext_lo (0 or 1 per axis)
+    int64_t n_owned = 0, n_ext = 0, n_cols = 0;
     std::vector<int64_t> ext_gid;         // slot order: (owner rank, global id)
+    std::vector<int64_t> ext_pos;         // slot -> extended column
     std::vector<int> nbr;                 // neighbor ranks, ascending
     std::vector<int64_t> recv_off, recv_cnt;   // slots [recv_off, +cnt) come from nbr[k]
     std::vector<int64_t> send_off, send_cnt;   // send_idx[send_off, +cnt) go to nbr[k]
@@ -41,6 +54,19 @@ struct Plan {
     int64_t owned_local(int64_t ix, int64_t iy, int64_t iz) const {
         return (ix - own_lo[0]) + own_n[0] * ((iy - own_lo[1]) + own_n[1] * (iz - own_lo[2]));
     }
+    int64_t ext_col(int64_t ix, int64_t iy, int64_t iz) const {
+        return (ix - ext_lo[0]) + ext_n[0] * ((iy - ext_lo[1]) + ext_n[1] * (iz - ext_lo[2]));
+    }
+    int64_t row_to_col(int64_t l) const {
+        const int64_t lx = l % own_n[0], ly = (l / own_n[0]) % own_n[1],
+                      lz = l / (own_n[0] * own_n[1]);
+        return (lx + off[0]) + ext_n[0] * ((ly + off[1]) + ext_n[1] * (lz + off[2]));
+    }
+    int64_t col_to_gid(int64_t c) const {
+        const int64_t a = c % ext_n[0], b = (c / ext_n[0]) % ext_n[1], d = c / (ext_n[0] * ext_n[1]);
+        return (ext_lo[0] + a) + mesh.NX() * ((ext_lo[1] + b) + mesh.NY() * (ext_lo[2] + d));
+    }
+    int64_t local_nns() const;            // segments (x-runs) of the local rows
     bool owns(int64_t ix, int64_t iy, int64_t iz) const {
         return ix >= own_lo[0] && ix <= own_hi[0] && iy >= own_lo[1] && iy <= own_hi[1] &&
                iz >= own_lo[2] && iz <= own_hi[2];

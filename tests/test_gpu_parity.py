@@ -73,10 +73,14 @@ def check_cg(g, n, iters, tol):
     assert _same(x, o.x)
 
 
+FORMATS = [M.FMT_SEG, M.FMT_CRS]
+
+
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("n", MESHES)
-def test_single_gpu_matrix_spmv_cg(n):
+def test_single_gpu_matrix_spmv_cg(n, fmt):
     s = oracle_system(n)
-    with M.Minife(*n) as g:
+    with M.Minife(*n, fmt=fmt) as g:
         g.assemble()
         info = g.get_info()
         assert info.rows == s.rows and info.nnz == s.nnz
@@ -88,12 +92,13 @@ def test_single_gpu_matrix_spmv_cg(n):
         check_cg(g, n, 7, 0.0)          # graph re-capture with another iteration count
 
 
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
-                                 ((12, 11, 10), 8), ((33, 32, 31), 5)])
-def test_virtual_ranks_bit_identical(n, p):
+                                 ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4)])
+def test_virtual_ranks_bit_identical(n, p, fmt):
     """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results."""
     s = oracle_system(n)
-    with M.Minife(*n, virtual=p) as g:
+    with M.Minife(*n, virtual=p, fmt=fmt) as g:
         g.assemble()
         assert g.get_info().nparts == p
         check_matrix(g, s)
@@ -110,16 +115,18 @@ def test_plan_on_device_matches_host_plan():
             b = M.plan(*n, p, r)
             assert (a.rows, a.externals, a.nnz, a.n_neighbors, a.send_total) == \
                    (b.rows, b.externals, b.nnz, b.n_neighbors, b.send_total)
+        g.set_format(M.FMT_CRS)          # plan's sell_entries is the CRS-format count
         g.assemble()
         for r in range(p):
             assert g.part_info(r).sell_entries == M.plan(*n, p, r).sell_entries
 
 
-def test_rank_mode_world1_nccl_path():
+@pytest.mark.parametrize("fmt", FORMATS)
+def test_rank_mode_world1_nccl_path(fmt):
     """SPMD entry point with a 1-rank NCCL communicator (exercises NCCL + graph capture)."""
     n = (10, 10, 10)
     uid = M.nccl_unique_id()
-    with M.Minife(*n, rank=(0, 1, 0, uid)) as g:
+    with M.Minife(*n, rank=(0, 1, 0, uid), fmt=fmt) as g:
         g.assemble()
         check_matrix(g, oracle_system(n))
         check_cg(g, n, 200, 0.0)
@@ -180,17 +187,40 @@ def test_profile_mode_matches_graph_mode():
         assert _same(g.history(), h1) and _same(g.solution(), x1)
 
 
+def test_format_switch_keeps_results():
+    n = (14, 13, 12)
+    s = oracle_system(n)
+    with M.Minife(*n) as g:
+        assert g.get_info().format == M.FMT_SEG
+        g.assemble()
+        seg_info = g.get_info()
+        # nns = number of maximal consecutive-column runs of the oracle's CRS rows
+        nns = sum(1 + int(np.sum(np.diff(s.col[s.row_ptr[i]:s.row_ptr[i + 1]]) != 1))
+                  for i in range(s.rows))
+        assert seg_info.local_nns == nns
+        g.set_format(M.FMT_CRS)
+        with pytest.raises(M.MinifeError):
+            g.cg_solve(5, 0.0)                 # unassembled after a format switch
+        g.assemble()
+        check_matrix(g, s)
+        check_cg(g, n, 60, 0.0)
+        g.set_format(M.FMT_SEG)
+        g.assemble()
+        check_matrix(g, s)
+        check_cg(g, n, 60, 0.0)
+
+
 @pytest.mark.slow
-def test_100cubed_full_parity():
+@pytest.mark.parametrize("fmt", FORMATS)
+def test_100cubed_full_parity(fmt):
     """configs[1] at full size: matrix, SpMV and the 200-iteration CG, element by element."""
     n = (100, 100, 100)
     s = oracle_system(n)
-    with M.Minife(*n) as g:
+    with M.Minife(*n, fmt=fmt) as g:
         g.assemble()
         check_matrix(g, s)
         check_spmv(g, s, 12345)
         check_cg(g, n, 200, 0.0)
-    _oracle_cache.clear()
 
 
 @pytest.mark.slow
