@@ -220,6 +220,14 @@ int minife_plan(int nx, int ny, int nz, int world, int rank, minife_part_info *o
 int minife_plan_lists(int nx, int ny, int nz, int world, int rank, int64_t *ext_gids,
                       int32_t *nbr, int64_t *recv_cnt, int64_t *send_cnt, int32_t *send_idx);
 
+/* Roofline denominators measured on CUDA device `device` (SURVEY §8(d) B_read): best of
+ * `reps` timed passes of a pure-read fp64 stream and of a copy (read + write bytes) over
+ * buffers of `bytes` bytes (>= 8 GB recommended: far larger than L2).  Allocates and frees
+ * its own buffers.  Errors: MINIFE_EINVAL (bytes < 1 MB, reps < 1, NULL), MINIFE_ENODEV,
+ * MINIFE_ENOMEM, MINIFE_ECUDA. */
+int minife_bandwidth_probe(int device, int64_t bytes, int reps, double *read_gbs,
+                           double *copy_gbs);
+
 /* Library version string. */
 const char *minife_version(void);
 

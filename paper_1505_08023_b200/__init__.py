@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libminife_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} not built: run `python -m paper_1505_08023_b200.build` "
+        f"{LIB_PATH} not built: run `python paper_1505_08023_b200/build.py` "
         "(or __graft_entry__.build()); there is no CPU fallback")
 
 
@@ -113,6 +113,7 @@ SIGNATURES = {
     "minife_get_owned_ids": (_I, [_P, _P]),
     "minife_plan": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(minife_part_info)]),
     "minife_plan_lists": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "minife_bandwidth_probe": (_I, [_I, _I64, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_version": (ctypes.c_char_p, []),
 }
 
@@ -159,6 +160,15 @@ def plan_lists(nx: int, ny: int, nz: int, world: int, rank: int) -> dict:
         raise MinifeError(st, "minife_plan_lists")
     return {"info": info, "ext_gids": ext, "nbr": nbr, "recv_cnt": rc, "send_cnt": sc,
             "send_idx": si}
+
+
+def bandwidth_probe(device: int = 0, nbytes: int = 8 << 30, reps: int = 5):
+    """(read GB/s, copy GB/s) of the library's pure-read and copy stream kernels."""
+    r, c = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    st = minife_bandwidth_probe(device, nbytes, reps, ctypes.byref(r), ctypes.byref(c))
+    if st != MINIFE_OK:
+        raise MinifeError(st, "minife_bandwidth_probe")
+    return r.value, c.value
 
 
 def nccl_unique_id() -> bytes:

@@ -1,6 +1,6 @@
 """Build the sm_100a shared library libminife_b200.so in-tree (nvcc, no JIT cache).
 
-    python -m paper_1505_08023_b200.build [--force] [--ptxas-verbose]
+    python paper_1505_08023_b200/build.py [--force] [--ptxas-verbose]
 """
 from __future__ import annotations
 

@@ -268,11 +268,12 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     TRY(dalloc(c, p, &p.d_slice_off, p.nslices + 1));
     TRY(dalloc(c, p, &p.d_row_len, p.nslices * 32));
     TRY(dalloc(c, p, &p.d_width, p.nslices));
-    TRY(dalloc(c, p, &p.d_b, p.rows));
-    TRY(dalloc(c, p, &p.d_x, p.rows));
-    TRY(dalloc(c, p, &p.d_r, p.rows));
-    TRY(dalloc(c, p, &p.d_p, p.ncols));
-    TRY(dalloc(c, p, &p.d_Ap, p.rows));
+    // vectors carry 32 doubles of padding: TMA tile copies round their size up to 16 B
+    TRY(dalloc(c, p, &p.d_b, p.rows + 32));
+    TRY(dalloc(c, p, &p.d_x, p.rows + 32));
+    TRY(dalloc(c, p, &p.d_r, p.rows + 32));
+    TRY(dalloc(c, p, &p.d_p, p.ncols + 32));
+    TRY(dalloc(c, p, &p.d_Ap, p.rows + 32));
     TRY(dalloc(c, p, &p.d_acc, 2 * ACC_WORDS));
     TRY(dalloc(c, p, &p.d_st, 1));
     TRY(alloc_hist(c, p, 201));
@@ -478,6 +479,18 @@ extern "C" const char *minife_strerror(int s) {
 }
 
 extern "C" const char *minife_last_error(const minife_ctx *c) { return c ? c->err.c_str() : ""; }
+
+extern "C" int minife_bandwidth_probe(int device, int64_t bytes, int reps, double *read_gbs,
+                                      double *copy_gbs) {
+    if (bytes < (1 << 20) || reps < 1 || !read_gbs || !copy_gbs) return MINIFE_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return MINIFE_ENODEV;
+    DevGuard g(device);
+    cudaError_t e = probe_bandwidth(bytes, reps, read_gbs, copy_gbs);
+    if (e == cudaErrorMemoryAllocation) return MINIFE_ENOMEM;
+    return e == cudaSuccess ? MINIFE_OK : MINIFE_ECUDA;
+}
 extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
 
 // ----------------------------------------------------------------------------------------

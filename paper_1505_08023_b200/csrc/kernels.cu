@@ -19,6 +19,22 @@
 
 namespace minife {
 
+static void query_occupancy();
+static int g_sms = 0;                      // SMs of the current device (occupancy queries)
+static int g_spmv_bps[2] = {0, 0};
+static int g_upd_bps = 0;
+
+// opt a kernel into > 48 KB dynamic shared memory, once per device
+template <class K>
+static cudaError_t ensure_smem_attr(K kernel, int bytes, unsigned long long &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((mask >> (dev & 63)) & 1ull) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) mask |= 1ull << (dev & 63);
+    return e;
+}
+
 // ----------------------------------------------------------------------------------------
 // small helpers
 // ----------------------------------------------------------------------------------------
@@ -746,6 +762,210 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
 }
 
 // ----------------------------------------------------------------------------------------
+// a3-a6, TMA-pipelined (one part: rows == columns): the vector streams are staged in shared
+// memory by bulk copies (producer warp), consumer warps compute from smem and store with
+// streaming stores.  Bytes in flight per SM = STAGES x tile, independent of occupancy.
+// Vectors are allocated with >= 32 doubles of padding, so a tile copy may round its size up
+// to 16 B; rows >= a.g.rows are never written.
+// ----------------------------------------------------------------------------------------
+
+constexpr int UT_ROWS = 1024;                         // rows per tile
+constexpr int UT_STAGES = 6;                          // 6 x 32 KB in flight per SM (K6)
+constexpr int UT_CWARPS = 8;                          // consumer warps
+constexpr int UT_THREADS = 32 * (UT_CWARPS + 1);      // + producer warp
+constexpr int UT_CONS = 32 * UT_CWARPS;
+constexpr int XR_SMEM = UT_STAGES * 4 * UT_ROWS * 8;  // x, r, p, Ap   = 192 KB
+constexpr int P_SMEM = UT_STAGES * 2 * UT_ROWS * 8;   // r, p          =  96 KB
+
+// Decisions of K6 (a3): finalise pAp, stop tests, alpha.  Thread 0 of each CTA; returns stop.
+__device__ __forceinline__ int xr_prologue(const UpdArgs &a, int k, double &alpha) {
+    const double pAp = acc_finalize(a.acc_in);
+    const double rr = a.rr[k - 1];
+    int stop = 0, status = 0, conv = 0;
+    if (!isfinite(pAp)) {
+        stop = 1;
+        status = 7;
+    } else if (pAp <= 0.0) {
+        stop = 1;
+        if (rr == 0.0) conv = 1;
+        else status = 6;
+    }
+    alpha = __ddiv_rn(rr, pAp);
+    if (blockIdx.x == 0) {
+        a.st->pAp = pAp;
+        a.st->alpha = alpha;
+        if (stop) {
+            a.st->status = status;
+            a.st->converged = conv;
+            a.st->iters = k - 1;
+            a.st->done = 1;
+        }
+    }
+    return stop;
+}
+
+// Decisions of K7 (a5): finalise rr', history, stop tests, beta.
+__device__ __forceinline__ int p_prologue(const UpdArgs &a, int k, double &beta) {
+    const double rr_new = acc_finalize(a.acc_in);
+    const double h = __dsqrt_rn(rr_new);
+    const double rr_old = a.rr[k - 1];
+    int stop = 0, status = 0, conv = 0;
+    if (!isfinite(rr_new)) {
+        stop = 1;
+        status = 7;
+    } else if (rr_new == 0.0 || h <= a.st->stop) {
+        stop = 1;
+        conv = 1;
+    }
+    beta = __ddiv_rn(rr_new, rr_old);
+    if (blockIdx.x == 0) {
+        a.hist[k] = h;
+        a.rr[k] = rr_new;
+        a.st->iters = k;
+        a.st->beta = beta;
+        if (stop) {
+            a.st->status = status;
+            a.st->converged = conv;
+            a.st->done = 1;
+        }
+    }
+    return stop;
+}
+
+// XR = true: K6 (x += alpha p, r -= alpha Ap, exact rr);  XR = false: K7 (p = r + beta p)
+template <bool XR>
+__global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) {
+    constexpr int NIN = XR ? 4 : 2;
+    constexpr int STAGE_D = NIN * UT_ROWS;            // doubles per stage
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *sm = reinterpret_cast<double *>(smem_raw);
+    __shared__ __align__(8) uint64_t full_bar[UT_STAGES], empty_bar[UT_STAGES];
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ double s_coef;
+    __shared__ int s_stop;
+    if (a.st->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < UT_STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], UT_CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        double coef;
+        s_stop = XR ? xr_prologue(a, k, coef) : p_prologue(a, k, coef);
+        s_coef = coef;
+    }
+    if (XR) acc_zero_shared(sacc);
+    __syncthreads();
+    if (s_stop) return;
+    if (!XR && blockIdx.x == 0 && a.acc_zero)
+        for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    const double coef = s_coef;
+    const int64_t rows = a.g.rows;
+    const int64_t ntiles = (rows + UT_ROWS - 1) / UT_ROWS;
+
+    if (warp == UT_CWARPS) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int64_t i = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int st = (int)(i % UT_STAGES);
+                if (i >= UT_STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / UT_STAGES) & 1) ^ 1));
+                const int64_t r0 = t * UT_ROWS;
+                const int64_t n = min((int64_t)UT_ROWS, rows - r0);
+                const uint32_t bytes = (uint32_t)(((n + 1) & ~(int64_t)1) * 8);   // 16 B multiple
+                double *buf = sm + (size_t)st * STAGE_D;
+                mbar_expect_tx(&full_bar[st], NIN * bytes);
+                if (XR) {
+                    bulk_g2s(buf, a.x + r0, bytes, &full_bar[st], pol);
+                    bulk_g2s(buf + UT_ROWS, a.r + r0, bytes, &full_bar[st], pol);
+                    bulk_g2s(buf + 2 * UT_ROWS, a.p + r0, bytes, &full_bar[st], pol);
+                    bulk_g2s(buf + 3 * UT_ROWS, a.Ap + r0, bytes, &full_bar[st], pol);
+                } else {
+                    bulk_g2s(buf, a.r + r0, bytes, &full_bar[st], pol);
+                    bulk_g2s(buf + UT_ROWS, a.p + r0, bytes, &full_bar[st], pol);
+                }
+            }
+        }
+    } else {
+        // two independent expansions per thread: two TwoSum dependency chains in flight
+        Expansion ex[2];
+        ex[0].init();
+        ex[1].init();
+        int64_t i = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int st = (int)(i % UT_STAGES);
+            mbar_wait(&full_bar[st], (uint32_t)((i / UT_STAGES) & 1));
+            const double *buf = sm + (size_t)st * STAGE_D;
+            const int64_t r0 = t * UT_ROWS;
+#pragma unroll
+            for (int j = 0; j < UT_ROWS / UT_CONS; ++j) {
+                const int l = threadIdx.x + j * UT_CONS;
+                if (r0 + l < rows) {
+                    if (XR) {
+                        double xi = buf[l], ri = buf[UT_ROWS + l];
+                        xr_step(xi, ri, buf[2 * UT_ROWS + l], buf[3 * UT_ROWS + l], coef,
+                                ex[j & 1], sacc);
+                        __stcs(a.x + r0 + l, xi);
+                        __stcs(a.r + r0 + l, ri);
+                    } else {
+                        __stcs(a.p + r0 + l, __dadd_rn(buf[l], __dmul_rn(coef, buf[UT_ROWS + l])));
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+        if (XR) {
+            ex[0].flush(sacc);
+            ex[1].flush(sacc);
+        }
+    }
+    if (XR) {
+        __syncthreads();
+        acc_merge_to_global(sacc, a.acc_out);
+    }
+}
+
+// Pure-read probe with the same bulk-copy engine (B_read for the TMA kernels).
+__global__ void __launch_bounds__(UT_THREADS, 1) k_read_tma(const double *src, int64_t n) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *sm = reinterpret_cast<double *>(smem_raw);
+    __shared__ __align__(8) uint64_t full_bar[UT_STAGES], empty_bar[UT_STAGES];
+    constexpr int TD = 4 * UT_ROWS;                   // 32 KB tiles
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < UT_STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], UT_CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t ntiles = n / TD;
+    if (warp == UT_CWARPS) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int64_t i = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int st = (int)(i % UT_STAGES);
+                if (i >= UT_STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / UT_STAGES) & 1) ^ 1));
+                mbar_expect_tx(&full_bar[st], TD * 8);
+                bulk_g2s(sm + (size_t)st * TD, src + t * TD, TD * 8, &full_bar[st], pol);
+            }
+        }
+    } else {
+        int64_t i = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int st = (int)(i % UT_STAGES);
+            mbar_wait(&full_bar[st], (uint32_t)((i / UT_STAGES) & 1));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------------
 // a1: halo pack / unpack / virtual-rank transport
 // ----------------------------------------------------------------------------------------
 
@@ -754,6 +974,101 @@ __global__ void k_move(const double *__restrict__ src, const int32_t *__restrict
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i];
+}
+
+// ----------------------------------------------------------------------------------------
+// roofline probes: pure-read fp64 stream and copy, 16-byte accesses
+// ----------------------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_read_stream(const double2 *__restrict__ src, int64_t n2,
+                                                     double *__restrict__ sink) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        const double2 a = __ldcs(src + i), b = __ldcs(src + i + stride),
+                      c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
+        s0 += a.x + a.y;
+        s1 += b.x + b.y;
+        s2 += c.x + c.y;
+        s3 += d.x + d.y;
+    }
+    for (; i < n2; i += stride) {
+        const double2 a = __ldcs(src + i);
+        s0 += a.x + a.y;
+    }
+    const double s = (s0 + s1) + (s2 + s3);
+    if (s == 12345.678) sink[0] = s;       // keeps the loads alive; never true for 0-filled data
+}
+
+__global__ void __launch_bounds__(256) k_copy_stream(const double2 *__restrict__ src,
+                                                     double2 *__restrict__ dst, int64_t n2) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < n2; i += 2 * stride) {
+        const double2 a = __ldcs(src + i), b = __ldcs(src + i + stride);
+        __stcs(dst + i, a);
+        __stcs(dst + i + stride, b);
+    }
+    for (; i < n2; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *copy_gbs) {
+    query_occupancy();
+    const int64_t n2 = bytes / 16;
+    double2 *a = nullptr, *b = nullptr;
+    double *sink = nullptr;
+    cudaEvent_t e0, e1;
+    cudaError_t e = cudaMalloc((void **)&a, n2 * 16);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b, n2 * 16);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&sink, 8);
+    if (e == cudaSuccess) e = cudaMemset(a, 0, n2 * 16);
+    if (e == cudaSuccess) e = cudaMemset(b, 0, n2 * 16);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = g_sms * 8;
+    float best_r = 1e30f, best_c = 1e30f;
+    for (int r = 0; e == cudaSuccess && r < reps + 1; ++r) {
+        float ms = 0.f;
+        cudaEventRecord(e0);
+        k_read_stream<<<grid, 256>>>(a, n2, sink);
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) best_r = std::min(best_r, ms);
+        cudaEventRecord(e0);
+        k_copy_stream<<<grid, 256>>>(a, b, n2);
+        cudaEventRecord(e1);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) best_c = std::min(best_c, ms);
+    }
+    // the bulk-copy engine's read rate (what the TMA-pipelined kernels can draw)
+    static unsigned long long attr = 0;
+    if (e == cudaSuccess) e = ensure_smem_attr(k_read_tma, UT_STAGES * 4 * UT_ROWS * 8, attr);
+    for (int r = 0; e == cudaSuccess && r < reps + 1; ++r) {
+        float ms = 0.f;
+        cudaEventRecord(e0);
+        k_read_tma<<<g_sms, UT_THREADS, UT_STAGES * 4 * UT_ROWS * 8>>>(
+            reinterpret_cast<const double *>(a), (n2 * 2) / (4 * UT_ROWS) * (4 * UT_ROWS));
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        const float scaled = ms * (float)((double)(n2 * 16) /
+                                          (double)((n2 * 2) / (4 * UT_ROWS) * (4 * UT_ROWS) * 8));
+        if (r > 0) best_r = std::min(best_r, scaled);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(sink);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (e == cudaSuccess) {
+        *read_gbs = (double)(n2 * 16) / (best_r * 1e-3) / 1e9;
+        *copy_gbs = 2.0 * (double)(n2 * 16) / (best_c * 1e-3) / 1e9;
+    }
+    return e;
 }
 
 struct AccPtrs {
@@ -797,10 +1112,6 @@ __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t
 // ----------------------------------------------------------------------------------------
 // launch wrappers
 // ----------------------------------------------------------------------------------------
-
-static int g_sms = 0;
-static int g_spmv_bps[2] = {0, 0};
-static int g_upd_bps = 0;
 
 static void query_occupancy() {
     if (g_sms) return;
@@ -912,15 +1223,56 @@ cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static int tma_update_grid(int64_t rows) {
+    query_occupancy();
+    const int64_t nt = (rows + UT_ROWS - 1) / UT_ROWS;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(nt, g_sms));
+}
+
+// Update kernels: register streaming by default (B200, 300^3: 0.375 ms/iteration for K6+K7
+// vs 0.417 ms for the TMA-pipelined variant, profiles/r01); MINIFE_UPD_IMPL=tma selects it.
+static bool upd_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MINIFE_UPD_IMPL");
+        v = (e && e[0] == 't') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// one part (rows == columns): TMA-pipelined streams; otherwise the register kernels that
+// map rows into the extended-box p
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    if (a.g.ident) k_update_xr<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
-    else k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    if (!a.g.ident || !upd_tma()) {
+        if (a.g.ident) k_update_xr<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        return cudaGetLastError();
+    }
+    if (a.g.ident) {
+        static unsigned long long m = 0;
+        cudaError_t e = ensure_smem_attr(k_update_tma<true>, XR_SMEM, m);
+        if (e != cudaSuccess) return e;
+        k_update_tma<true><<<tma_update_grid(a.g.rows), UT_THREADS, XR_SMEM, s>>>(a, k);
+    } else {
+        k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    if (a.g.ident) k_update_p<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
-    else k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    if (!a.g.ident || !upd_tma()) {
+        if (a.g.ident) k_update_p<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        return cudaGetLastError();
+    }
+    if (a.g.ident) {
+        static unsigned long long m = 0;
+        cudaError_t e = ensure_smem_attr(k_update_tma<false>, P_SMEM, m);
+        if (e != cudaSuccess) return e;
+        k_update_tma<false><<<tma_update_grid(a.g.rows), UT_THREADS, P_SMEM, s>>>(a, k);
+    } else {
+        k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+    }
     return cudaGetLastError();
 }
 

@@ -104,6 +104,10 @@ cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,
                                 cudaStream_t s);
 
+// Roofline probes on the current device: best-of-reps pure-read and copy bandwidth (GB/s,
+// copy counts read + write bytes) over `bytes`-sized buffers.
+cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *copy_gbs);
+
 // occupancy-derived grid sizes
 int spmv_grid(int64_t nslices, int fmt);
 int stream_grid(int64_t rows);
