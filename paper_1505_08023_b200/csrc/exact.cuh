@@ -91,44 +91,71 @@ __device__ __forceinline__ void acc_merge_to_global(const unsigned long long *s,
     }
 }
 
-// Normalise carries and round to nearest-even (one thread).  Exact zero -> +0.0.
-static __device__ __noinline__ double acc_finalize(const unsigned long long *gw) {
-    if (gw[ACC_FLAG] != 0ull) return __longlong_as_double(0x7ff8000000000000ll);
-    uint32_t d[ACC_DIGITS];
+// Cooperative copy of a global accumulator into shared memory (all threads of the CTA).
+__device__ __forceinline__ void acc_load_shared(unsigned long long *s,
+                                                const unsigned long long *g) {
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = __ldcg(g + i);
+}
+
+// One window of the digit scan: the top nonzero digit seen so far, the two digits below it,
+// and whether anything below those is nonzero.
+struct DigitWindow {
+    int T = -1;
+    uint32_t dT = 0, d1 = 0, d2 = 0;
+    bool sticky = false;
+    uint32_t prev1 = 0, prev2 = 0;    // digits i-1, i-2 of the scan
+    bool below = false;               // OR of digits <= i-3
+    __device__ __forceinline__ void push(int i, uint32_t d) {
+        if (d != 0) {
+            T = i;
+            dT = d;
+            d1 = prev1;
+            d2 = prev2;
+            sticky = below;
+        }
+        below |= prev2 != 0;
+        prev2 = prev1;
+        prev1 = d;
+    }
+};
+
+// Normalise carries and round to nearest-even (one thread; s = shared copy of the words).
+// Exact zero -> +0.0.  One pass from the least significant digit with constant state:
+// the sign is only known at the end, so the window is tracked for both the value and its
+// two's-complement negation (digit e_i = -d_i while every lower digit is 0, else ~d_i).
+static __device__ __noinline__ double acc_finalize(const unsigned long long *s) {
+    if (s[ACC_FLAG] != 0ull) return __longlong_as_double(0x7ff8000000000000ll);
     long long carry = 0;
+    bool all_zero = true;
+    DigitWindow pos, neg;
 #pragma unroll 4
     for (int i = 0; i < ACC_DIGITS; ++i) {
-        const long long v = (long long)gw[i] + carry;
-        d[i] = (uint32_t)((unsigned long long)v & 0xffffffffull);
-        carry = (v - (long long)d[i]) >> 32;   // exact floor division by 2^32
+        const long long v = (long long)s[i] + carry;
+        const uint32_t d = (uint32_t)((unsigned long long)v & 0xffffffffull);
+        carry = (v - (long long)d) >> 32;      // exact floor division by 2^32
+        pos.push(i, d);
+        neg.push(i, all_zero ? 0u - d : ~d);
+        all_zero = all_zero && d == 0;
     }
-    const bool neg = carry < 0;                // value = sum d_i 2^(32i) - [neg] 2^(32*68)
-    if (neg) {
-        unsigned long long c = 1;
-        for (int i = 0; i < ACC_DIGITS; ++i) {
-            c += (uint32_t)~d[i];
-            d[i] = (uint32_t)c;
-            c >>= 32;
-        }
-    }
-    int T = ACC_DIGITS - 1;
-    while (T >= 0 && d[T] == 0) --T;
+    const bool negative = carry < 0;           // value = sum d_i 2^(32i) - [neg] 2^(32*68)
+    const DigitWindow &w = negative ? neg : pos;
+    const int T = w.T;
     if (T < 0) return 0.0;
-    const int t = 32 * T + 31 - __clz(d[T]);   // top bit, in units of 2^-1074
+    const uint32_t dT = w.dT, d1 = w.d1, d2 = w.d2;
+    const int t = 32 * T + 31 - __clz(dT);     // top bit, in units of 2^-1074
     double mag;
-    if (t <= 52) {
-        const unsigned long long v = (unsigned long long)d[0] | ((unsigned long long)d[1] << 32);
+    if (t <= 52) {                             // T <= 1: the value is digits T..0, exact
+        const unsigned long long v =
+            T == 1 ? ((unsigned long long)dT << 32) | d1 : (unsigned long long)dT;
         mag = scalbn((double)v, -1074);        // < 2^53 ulps of 2^-1074: exact
     } else {
         // 96-bit window of digits T, T-1, T-2 (missing digits read as 0)
-        const uint32_t d1 = T >= 1 ? d[T - 1] : 0u, d2 = T >= 2 ? d[T - 2] : 0u;
-        const unsigned __int128 W = ((unsigned __int128)d[T] << 64) |
+        const unsigned __int128 W = ((unsigned __int128)dT << 64) |
                                     ((unsigned __int128)d1 << 32) | (unsigned __int128)d2;
         const int sh = t - 32 * (T - 2);        // top bit position inside W, in [64, 95]
         unsigned long long M = (unsigned long long)(W >> (sh - 52));   // 53 bits
         const int guard = (int)((W >> (sh - 53)) & 1u);
-        bool sticky = (W & ((((unsigned __int128)1) << (sh - 53)) - 1)) != 0;
-        for (int i = T - 3; i >= 0 && !sticky; --i) sticky = d[i] != 0;
+        bool sticky = w.sticky || (W & ((((unsigned __int128)1) << (sh - 53)) - 1)) != 0;
         int top = t;
         if (guard && (sticky || (M & 1ull))) {
             ++M;
@@ -139,7 +166,7 @@ static __device__ __noinline__ double acc_finalize(const unsigned long long *gw)
         }
         mag = scalbn((double)M, top - 52 - 1074);   // inf iff round-to-nearest overflows
     }
-    return neg ? -mag : mag;
+    return negative ? -mag : mag;
 }
 
 }  // namespace minife

@@ -22,7 +22,7 @@ namespace minife {
 static void query_occupancy();
 static int g_sms = 0;                      // SMs of the current device (occupancy queries)
 static int g_spmv_bps[2] = {0, 0};
-static int g_upd_bps = 0;
+static int g_upd_bps = 0, g_updp_bps = 0;
 
 // opt a kernel into > 48 KB dynamic shared memory, once per device
 template <class K>
@@ -565,8 +565,11 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
 }
 
 __global__ void k_init_finalize(UpdArgs a, double tol) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    acc_load_shared(s_in, a.acc_out);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const double rr0 = acc_finalize(a.acc_out);
+        const double rr0 = acc_finalize(s_in);
         const double h0 = __dsqrt_rn(rr0);
         a.rr[0] = rr0;
         a.hist[0] = h0;
@@ -596,38 +599,78 @@ __device__ __forceinline__ void xr_step(double &x, double &r, double p, double a
     ex.add(__dmul_rn(r, r), sacc);
 }
 
+// Decisions of K6 (a3, C6): finalise pAp, stop tests, alpha.  Thread 0 of each CTA (s_in =
+// shared copy of the all-reduced accumulator); every CTA takes the same decision, CTA 0
+// records it.  Returns stop.
+__device__ __forceinline__ int xr_prologue(const UpdArgs &a, const unsigned long long *s_in,
+                                           int k, double &alpha) {
+    const double pAp = acc_finalize(s_in);
+    const double rr = a.rr[k - 1];
+    int stop = 0, status = 0, conv = 0;
+    if (!isfinite(pAp)) {
+        stop = 1;
+        status = 7;
+    } else if (pAp <= 0.0) {
+        stop = 1;
+        if (rr == 0.0) conv = 1;
+        else status = 6;
+    }
+    alpha = __ddiv_rn(rr, pAp);
+    if (blockIdx.x == 0) {
+        a.st->pAp = pAp;
+        a.st->alpha = alpha;
+        if (stop) {
+            a.st->status = status;
+            a.st->converged = conv;
+            a.st->iters = k - 1;
+            a.st->done = 1;
+        }
+    }
+    return stop;
+}
+
+// Decisions of K7 (a5, C6): finalise rr', history, stop tests, beta.
+__device__ __forceinline__ int p_prologue(const UpdArgs &a, const unsigned long long *s_in,
+                                          int k, double &beta) {
+    const double rr_new = acc_finalize(s_in);
+    const double h = __dsqrt_rn(rr_new);
+    const double rr_old = a.rr[k - 1];
+    int stop = 0, status = 0, conv = 0;
+    if (!isfinite(rr_new)) {
+        stop = 1;
+        status = 7;
+    } else if (rr_new == 0.0 || h <= a.st->stop) {
+        stop = 1;
+        conv = 1;
+    }
+    beta = __ddiv_rn(rr_new, rr_old);
+    if (blockIdx.x == 0) {
+        a.hist[k] = h;
+        a.rr[k] = rr_new;
+        a.st->iters = k;
+        a.st->beta = beta;
+        if (stop) {
+            a.st->status = status;
+            a.st->converged = conv;
+            a.st->done = 1;
+        }
+    }
+    return stop;
+}
+
 template <bool IDENT>
-__global__ void __launch_bounds__(UPD_THREADS) k_update_xr(UpdArgs a, int k) {
-    __shared__ unsigned long long sacc[ACC_WORDS];
+__global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) {
+    __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
     __shared__ double s_alpha;
     __shared__ int s_stop;
     if (a.st->done) return;
     acc_zero_shared(sacc);
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const double pAp = acc_finalize(a.acc_in);
-        const double rr = a.rr[k - 1];
-        int stop = 0, status = 0, conv = 0;
-        if (!isfinite(pAp)) {
-            stop = 1;
-            status = 7;
-        } else if (pAp <= 0.0) {
-            stop = 1;
-            if (rr == 0.0) conv = 1;
-            else status = 6;
-        }
-        const double alpha = __ddiv_rn(rr, pAp);
+        double alpha;
+        s_stop = xr_prologue(a, s_in, k, alpha);
         s_alpha = alpha;
-        s_stop = stop;
-        if (blockIdx.x == 0) {
-            a.st->pAp = pAp;
-            a.st->alpha = alpha;
-            if (stop) {
-                a.st->status = status;
-                a.st->converged = conv;
-                a.st->iters = k - 1;
-                a.st->done = 1;
-            }
-        }
     }
     __syncthreads();
     if (s_stop) return;
@@ -691,35 +734,16 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_xr(UpdArgs a, int k) {
 
 template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta;
     __shared__ int s_stop;
     if (a.st->done) return;
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const double rr_new = acc_finalize(a.acc_in);
-        const double h = __dsqrt_rn(rr_new);
-        const double rr_old = a.rr[k - 1];
-        int stop = 0, status = 0, conv = 0;
-        if (!isfinite(rr_new)) {
-            stop = 1;
-            status = 7;
-        } else if (rr_new == 0.0 || h <= a.st->stop) {
-            stop = 1;
-            conv = 1;
-        }
-        const double beta = __ddiv_rn(rr_new, rr_old);
+        double beta;
+        s_stop = p_prologue(a, s_in, k, beta);
         s_beta = beta;
-        s_stop = stop;
-        if (blockIdx.x == 0) {
-            a.hist[k] = h;
-            a.rr[k] = rr_new;
-            a.st->iters = k;
-            a.st->beta = beta;
-            if (stop) {
-                a.st->status = status;
-                a.st->converged = conv;
-                a.st->done = 1;
-            }
-        }
     }
     __syncthreads();
     if (s_stop) return;
@@ -777,61 +801,6 @@ constexpr int UT_CONS = 32 * UT_CWARPS;
 constexpr int XR_SMEM = UT_STAGES * 4 * UT_ROWS * 8;  // x, r, p, Ap   = 192 KB
 constexpr int P_SMEM = UT_STAGES * 2 * UT_ROWS * 8;   // r, p          =  96 KB
 
-// Decisions of K6 (a3): finalise pAp, stop tests, alpha.  Thread 0 of each CTA; returns stop.
-__device__ __forceinline__ int xr_prologue(const UpdArgs &a, int k, double &alpha) {
-    const double pAp = acc_finalize(a.acc_in);
-    const double rr = a.rr[k - 1];
-    int stop = 0, status = 0, conv = 0;
-    if (!isfinite(pAp)) {
-        stop = 1;
-        status = 7;
-    } else if (pAp <= 0.0) {
-        stop = 1;
-        if (rr == 0.0) conv = 1;
-        else status = 6;
-    }
-    alpha = __ddiv_rn(rr, pAp);
-    if (blockIdx.x == 0) {
-        a.st->pAp = pAp;
-        a.st->alpha = alpha;
-        if (stop) {
-            a.st->status = status;
-            a.st->converged = conv;
-            a.st->iters = k - 1;
-            a.st->done = 1;
-        }
-    }
-    return stop;
-}
-
-// Decisions of K7 (a5): finalise rr', history, stop tests, beta.
-__device__ __forceinline__ int p_prologue(const UpdArgs &a, int k, double &beta) {
-    const double rr_new = acc_finalize(a.acc_in);
-    const double h = __dsqrt_rn(rr_new);
-    const double rr_old = a.rr[k - 1];
-    int stop = 0, status = 0, conv = 0;
-    if (!isfinite(rr_new)) {
-        stop = 1;
-        status = 7;
-    } else if (rr_new == 0.0 || h <= a.st->stop) {
-        stop = 1;
-        conv = 1;
-    }
-    beta = __ddiv_rn(rr_new, rr_old);
-    if (blockIdx.x == 0) {
-        a.hist[k] = h;
-        a.rr[k] = rr_new;
-        a.st->iters = k;
-        a.st->beta = beta;
-        if (stop) {
-            a.st->status = status;
-            a.st->converged = conv;
-            a.st->done = 1;
-        }
-    }
-    return stop;
-}
-
 // XR = true: K6 (x += alpha p, r -= alpha Ap, exact rr);  XR = false: K7 (p = r + beta p)
 template <bool XR>
 __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) {
@@ -840,11 +809,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sm = reinterpret_cast<double *>(smem_raw);
     __shared__ __align__(8) uint64_t full_bar[UT_STAGES], empty_bar[UT_STAGES];
-    __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
     __shared__ double s_coef;
     __shared__ int s_stop;
     if (a.st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
     if (threadIdx.x == 0) {
         for (int s = 0; s < UT_STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -852,7 +823,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         double coef;
-        s_stop = XR ? xr_prologue(a, k, coef) : p_prologue(a, k, coef);
+        s_stop = XR ? xr_prologue(a, s_in, k, coef) : p_prologue(a, s_in, k, coef);
         s_coef = coef;
     }
     if (XR) acc_zero_shared(sacc);
@@ -1123,6 +1094,8 @@ static void query_occupancy() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_spmv_bps[1], k_spmv_seg<true>,
                                                   SPMV_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_bps, k_update_xr<true>, UPD_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updp_bps, k_update_p<true>, UPD_THREADS, 0);
+    if (g_updp_bps <= 0) g_updp_bps = 1;
     if (g_sms <= 0) g_sms = 148;
     for (int f = 0; f < 2; ++f)
         if (g_spmv_bps[f] <= 0) g_spmv_bps[f] = 1;
@@ -1261,7 +1234,12 @@ cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) 
 
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s) {
     if (!a.g.ident || !upd_tma()) {
-        if (a.g.ident) k_update_p<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        if (a.g.ident) {
+            // K7 has its own (higher) occupancy than K6, whose grid is passed in
+            const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
+            const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
+            k_update_p<true><<<g7, UPD_THREADS, 0, s>>>(a, k);
+        }
         else k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
         return cudaGetLastError();
     }
