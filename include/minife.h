@@ -52,6 +52,14 @@ extern "C" {
                                   paper's BCRS (Fig 3.2) on the GPU; 8 B per entry
                                   + 4 B per segment.  Default.                                */
 
+/* ---- CG iteration schemes ------------------------------------------------- */
+#define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | x/r update + rr | p update.      */
+                               /* Default.  12 nnz-class bytes + 88 B per row.               */
+#define MINIFE_SCHEME_FUSED 1  /* SURVEY §8(f) NEXT #2, one part + MINIFE_FMT_SEG only (other */
+                               /* ctxs run 3K): the p update is formed at gather time inside  */
+                               /* the SpMV and x is updated one iteration late there; a second */
+                               /* kernel does r and rr.  72 B per row, 2 launches.            */
+
 typedef struct minife_ctx minife_ctx;
 
 /* Per-part (per-rank) plan, host-computed from the RCB partition (G15). */
@@ -148,6 +156,11 @@ const char *minife_last_error(const minife_ctx *ctx);
  * ctx becomes unassembled.  Results are bit-identical in both formats (same values, same
  * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
 int minife_set_format(minife_ctx *ctx, int format);
+
+/* Select the CG iteration scheme of later solves (MINIFE_SCHEME_*).  Both schemes perform
+ * C6's operations on the same values in the same order: results are bit-identical.
+ * Errors: MINIFE_EINVAL (ctx NULL or unknown scheme). */
+int minife_set_scheme(minife_ctx *ctx, int scheme);
 
 /* Structure -> SELL-32 (a0.2), element operator (a0.3, C1), gather-assembly (a0.4, C2) and
  * Dirichlet elimination (a0.5, C3) on the device, for every part.  Idempotent.

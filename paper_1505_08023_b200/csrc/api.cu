@@ -88,8 +88,10 @@ struct Part {
     double *d_val = nullptr;
     // vectors: b, x, r, Ap in row (owned) order; p in column (extended-box) order
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
+    double *d_p2 = nullptr;                       // fused scheme: second p buffer (lazy)
     double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
-    unsigned long long *d_acc = nullptr;          // [0, ACC_WORDS) pAp, [ACC_WORDS, 2*) rr
+    // exact accumulators, parity double-buffered: [pAp_0, rr_0, pAp_1, rr_1] x ACC_WORDS
+    unsigned long long *d_acc = nullptr;
     CgState *d_st = nullptr;
     double *d_hist = nullptr, *d_rr = nullptr;
     int hist_cap = 0;
@@ -101,8 +103,11 @@ struct Part {
     cudaStream_t stream = nullptr;
     int grid_spmv = 1, grid_upd = 1;
     size_t bytes = 0, matrix_bytes = 0;
-    unsigned long long *acc_pAp() const { return d_acc; }
-    unsigned long long *acc_rr() const { return d_acc + ACC_WORDS; }
+    unsigned long long *acc_pAp(int par = 0) const { return d_acc + (2 * (par & 1)) * ACC_WORDS; }
+    unsigned long long *acc_rr(int par = 0) const {
+        return d_acc + (2 * (par & 1) + 1) * ACC_WORDS;
+    }
+    double *p_buf(int k) const { return (k & 1) ? d_p2 : d_p; }   // fused: p_k lives in k % 2
 };
 
 struct DevGuard {
@@ -122,6 +127,7 @@ struct minife_ctx {
     Mesh mesh{};
     int mode = MINIFE_MODE_SINGLE;
     int fmt = MINIFE_FMT_SEG;
+    int scheme = MINIFE_SCHEME_3K;
     int world = 1, rank = 0;
     std::vector<Part> parts;
     cudaStream_t user_stream = nullptr;
@@ -214,7 +220,7 @@ static void free_part(Part &p) {
     DevGuard g(p.dev);
     free_matrix(p);
     void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width,   p.d_b,        p.d_x,
-                    p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,
+                    p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf};
     for (void *b : bufs)
@@ -274,10 +280,10 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     TRY(dalloc(c, p, &p.d_r, p.rows + 32));
     TRY(dalloc(c, p, &p.d_p, p.ncols + 32));
     TRY(dalloc(c, p, &p.d_Ap, p.rows + 32));
-    TRY(dalloc(c, p, &p.d_acc, 2 * ACC_WORDS));
+    TRY(dalloc(c, p, &p.d_acc, 4 * ACC_WORDS));
     TRY(dalloc(c, p, &p.d_st, 1));
     TRY(alloc_hist(c, p, 201));
-    CUDA_TRY(c, cudaMemset(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long)));
+    CUDA_TRY(c, cudaMemset(p.d_acc, 0, 4 * ACC_WORDS * sizeof(unsigned long long)));
     CUDA_TRY(c, cudaMemset(p.d_st, 0, sizeof(CgState)));
     CUDA_TRY(c, cudaMemset(p.d_p, 0, p.ncols * sizeof(double)));
     // halo index lists, as extended columns
@@ -448,6 +454,15 @@ extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
     if (!c) return MINIFE_EINVAL;
     if (c->mode != MINIFE_MODE_SINGLE && c->mode != MINIFE_MODE_RANK) return MINIFE_ESTATE;
     c->user_stream = (cudaStream_t)stream;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_set_scheme(minife_ctx *c, int scheme) {
+    if (!c || (scheme != MINIFE_SCHEME_3K && scheme != MINIFE_SCHEME_FUSED)) return MINIFE_EINVAL;
+    if (scheme != c->scheme) {
+        c->scheme = scheme;
+        drop_graph(c);
+    }
     return MINIFE_OK;
 }
 
@@ -698,7 +713,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         cudaStream_t s = launch_stream(c, p);
-        CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 2 * ACC_WORDS * sizeof(unsigned long long), s));
+        CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 4 * ACC_WORDS * sizeof(unsigned long long), s));
         UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
         CUDA_TRY(c, launch_init_vectors(a, p.grid_upd, s));
@@ -747,6 +762,71 @@ static int ensure_hist(minife_ctx *c, int max_iters) {
     return MINIFE_OK;
 }
 
+// Fused two-kernel iteration: one part, SEG format,
+// selected with minife_set_scheme (default: the three-kernel sequence, faster on B200 today,
+// profiles/r01).  Both schemes give the same results, bit for bit.
+static bool fused_mode(const minife_ctx *c) {
+    return c->scheme == MINIFE_SCHEME_FUSED && c->parts.size() == 1 &&
+           c->fmt == MINIFE_FMT_SEG && c->parts[0].ncols == c->parts[0].rows;
+}
+
+static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    cudaStream_t s = launch_stream(c, p);
+    // F1(k): p_k = r + beta_{k-1} p_{k-1} at gather time, Ap_k, exact pAp_k, deferred x
+    SpmvArgs a = spmv_args(c, p, p.p_buf(k - 1), p.d_Ap, true);
+    a.acc = p.acc_pAp(k);
+    a.acc_zero = p.acc_rr(k);            // read by F1(k-1): free for K6'(k)
+    a.fused_k = k;
+    a.r = p.d_r;
+    a.p_old = p.p_buf(k - 1);
+    a.p_new = p.p_buf(k);
+    a.xsol = p.d_x;
+    a.acc_rr_in = p.acc_rr(k - 1);
+    a.hist = p.d_hist;
+    a.rr = p.d_rr;
+    a.stw = p.d_st;
+    CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, s));
+    if (t) t->mark(0);
+    // K6'(k): alpha_k, r -= alpha_k Ap_k, exact rr_k
+    UpdArgs u = upd_args(c, p, 0);
+    u.acc_in = p.acc_pAp(k);
+    u.acc_out = p.acc_rr(k);
+    CUDA_TRY(c, launch_update_r(u, k, p.acc_pAp(k + 1), p.grid_upd, s));
+    if (t) t->mark(1);
+    return MINIFE_OK;
+}
+
+// init + max_iters iterations (+ the fused scheme's finish kernel), enqueued on the streams
+static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
+    if (fused_mode(c) && !c->parts[0].d_p2) {
+        Part &p = c->parts[0];
+        DevGuard g(p.dev);
+        TRY(dalloc(c, p, &p.d_p2, p.ncols + 32));
+        CUDA_TRY(c, cudaMemset(p.d_p2, 0, (p.ncols + 32) * sizeof(double)));
+    }
+    return MINIFE_OK;
+}
+
+static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
+    const bool fused = fused_mode(c);
+    TRY(enqueue_init(c, tol));
+    if (t) t->mark(-1);
+    for (int k = 1; k <= max_iters; ++k)
+        TRY(fused ? enqueue_iteration_fused(c, k, t) : enqueue_iteration(c, k, t));
+    if (fused) {
+        Part &p = c->parts[0];
+        DevGuard g(p.dev);
+        UpdArgs u = upd_args(c, p, 0);
+        u.acc_in = p.acc_rr(max_iters);
+        CUDA_TRY(c, launch_cg_finish(u, max_iters, p.p_buf(0), p.p_buf(1), p.grid_upd,
+                                     launch_stream(c, p)));
+        if (t) t->mark(2);
+    }
+    return MINIFE_OK;
+}
+
 static double spmv_alg_bytes(const minife_ctx *c, const Part &q) {
     // CRS 12 nnz (+16 rows of x/y); segment format 8 nnz + 4 nns (+16 rows)
     return c->fmt == MINIFE_FMT_CRS ? 12.0 * (double)q.nnz
@@ -778,8 +858,10 @@ static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, doub
         res->seconds = seconds;
         const double rows = (double)c->mesh.rows(), nnz = (double)c->mesh.nnz();
         res->flops = (double)st.iters * (2.0 * nnz + 10.0 * rows);
+        // vector bytes per row: 88 (three-kernel scheme) or 72 (fused scheme)
+        const double vec = fused_mode(c) ? 72.0 : 88.0;
         double bytes = 0.0;
-        for (auto &q : c->parts) bytes += spmv_alg_bytes(c, q) + 88.0 * (double)q.rows;
+        for (auto &q : c->parts) bytes += spmv_alg_bytes(c, q) + vec * (double)q.rows;
         res->bytes = (double)st.iters * bytes;
     }
     return status;
@@ -792,7 +874,7 @@ static int check_solve_args(minife_ctx *c, int max_iters, double tol) {
         return MINIFE_ESTATE;
     }
     if (max_iters < 1 || !(tol >= 0.0)) return MINIFE_EINVAL;
-    return MINIFE_OK;
+    return ensure_fused_buffers(c);
 }
 
 extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_cg_result *res) {
@@ -803,8 +885,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     if (c->mode == MINIFE_MODE_MULTI) {
         // one host thread drives every device: launch the sequence directly
         CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
-        TRY(enqueue_init(c, tol));
-        for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration(c, k, nullptr));
+        TRY(enqueue_solve(c, max_iters, tol, nullptr));
         CUDA_TRY(c, cudaEventRecord(c->ev1, p0.stream));
         for (auto &p : c->parts) {
             DevGuard gg(p.dev);
@@ -818,9 +899,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
             cudaStream_t saved = c->user_stream;
             c->user_stream = nullptr;
             CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-            int st = enqueue_init(c, tol);
-            for (int k = 1; st == MINIFE_OK && k <= max_iters; ++k)
-                st = enqueue_iteration(c, k, nullptr);
+            int st = enqueue_solve(c, max_iters, tol, nullptr);
             cudaGraph_t graph = nullptr;
             cudaError_t e = cudaStreamEndCapture(cap, &graph);
             c->user_stream = saved;
@@ -853,9 +932,7 @@ extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_tim
     DevGuard g(p0.dev);
     PhaseTimer t;
     t.s = launch_stream(c, p0);
-    TRY(enqueue_init(c, 0.0));
-    t.mark(-1);
-    for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration(c, k, &t));
+    TRY(enqueue_solve(c, max_iters, 0.0, &t));
     for (auto &p : c->parts) {
         DevGuard gg(p.dev);
         CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
@@ -872,7 +949,8 @@ extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_tim
         out->update_xr_ms = ms[1];
         out->update_p_ms = ms[2];
         out->comm_ms = ms[3];
-        out->spmv_launches = out->update_xr_launches = out->update_p_launches = max_iters;
+        out->spmv_launches = out->update_xr_launches = max_iters;
+        out->update_p_launches = fused_mode(c) ? 1 : max_iters;   // fused: the finish kernel
         out->iterations = max_iters;
     }
     return read_result(c, max_iters, nullptr, 0.0);

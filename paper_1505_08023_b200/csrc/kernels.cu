@@ -22,7 +22,7 @@ namespace minife {
 static void query_occupancy();
 static int g_sms = 0;                      // SMs of the current device (occupancy queries)
 static int g_spmv_bps[2] = {0, 0};
-static int g_upd_bps = 0, g_updp_bps = 0;
+static int g_upd_bps = 0, g_updp_bps = 0, g_updr_bps = 0;
 
 // opt a kernel into > 48 KB dynamic shared memory, once per device
 template <class K>
@@ -416,21 +416,48 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-template <bool DOT, int FMT, bool IDENT>
+__device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k, double *hist,
+                                           double *rr, CgState *st, double &beta);
+
+// FUSED (SEG, DOT, one part only): fused CG iteration k = a.fused_k, DESIGN.md §5.  The
+// prologue takes K7's decisions for iteration k-1 (finalise rr_{k-1}, hist, stop tests,
+// beta_{k-1}); the operand gathered for column c is p_k[c] = fl(r[c] + fl(beta p_{k-1}[c]))
+// (p_1 = r); p_k and x += fl(alpha_{k-1} p_{k-1}) are written for the own rows.  Values and
+// operation order are those of the three-kernel C6 sequence, so results are bit-identical.
+template <bool DOT, int FMT, bool IDENT, bool FUSED>
 __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
     constexpr int STAGES = FMT == FMT_SEG ? SEG_STAGES : CRS_STAGES;
     constexpr int STAGE_B = FMT == FMT_SEG ? SEG_STAGE_B : CRS_STAGE_B;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ unsigned long long s_in[FUSED ? ACC_WORDS : 1];
+    __shared__ double s_beta, s_alpha_prev;
+    __shared__ int s_stop;
     if (DOT && a.st && a.st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fk = FUSED ? a.fused_k : 0;
+    if (FUSED && fk >= 2) {
+        acc_load_shared(s_in, a.acc_rr_in);
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], TMA_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_stop = 0;
+        if (FUSED) {
+            double beta = 0.0, alpha_prev = 0.0;
+            if (fk >= 2) {
+                s_stop = rr_decision(s_in, fk - 1, a.hist, a.rr, a.stw, beta);
+                alpha_prev = a.stw->alpha;                    // alpha_{k-1} (K6 of k-1)
+                if (!s_stop && blockIdx.x == 0) a.stw->x_done = fk - 1;
+            }
+            s_beta = beta;
+            s_alpha_prev = alpha_prev;
+        }
     }
     if (DOT) {
         acc_zero_shared(sacc);
@@ -438,6 +465,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     }
     __syncthreads();
+    if (FUSED && s_stop) return;
     const Matrix &m = a.m;
     const int64_t ntiles = (m.nslices + TILE - 1) / TILE;
 
@@ -496,13 +524,36 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
 #pragma unroll
                     for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
                     double xv[27];
+                    if (!FUSED) {
 #pragma unroll
-                    for (int t = 0; t < 27; ++t)
-                        xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
+                        for (int t = 0; t < 27; ++t)
+                            xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
+                    } else if (fk == 1) {
+#pragma unroll
+                        for (int t = 0; t < 27; ++t)             // p_1 = r_0 (= b), exactly
+                            xv[t] = ((msk >> t) & 1u) ? __ldg(a.r + sg[t / 3] + (t % 3)) : 0.0;
+                    } else {
+                        const double beta = s_beta;
+                        double rv[27], pv[27];
+#pragma unroll
+                        for (int t = 0; t < 27; ++t) {
+                            const bool on = (msk >> t) & 1u;
+                            const int c = sg[t / 3] + (t % 3);
+                            rv[t] = on ? __ldg(a.r + c) : 0.0;
+                            pv[t] = on ? __ldg(a.p_old + c) : 0.0;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 27; ++t)             // K7: p = r + fl(beta p)
+                            xv[t] = __dadd_rn(rv[t], __dmul_rn(beta, pv[t]));
+                        if (row < m.rows)                        // deferred x update (K6, k-1)
+                            a.xsol[row] =
+                                __dadd_rn(a.xsol[row], __dmul_rn(s_alpha_prev, pv[13]));
+                    }
 #pragma unroll
                     for (int t = 0; t < 27; ++t)
                         if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * t], xv[t]));
                     pdiag = xv[13];
+                    if (FUSED && row < m.rows) a.p_new[row] = pdiag;
                 } else {
                     const int64_t e0 = m.slice_off[tile * TILE];
                     const int64_t so = m.slice_off[s] - e0;
@@ -582,6 +633,8 @@ __global__ void k_init_finalize(UpdArgs a, double tol) {
         st.pAp = 0.0;
         st.alpha = 0.0;
         st.beta = 0.0;
+        st.alpha_iter = 0;
+        st.x_done = 0;
         *a.st = st;
     }
     if (a.acc_zero)
@@ -624,38 +677,46 @@ __device__ __forceinline__ int xr_prologue(const UpdArgs &a, const unsigned long
             a.st->converged = conv;
             a.st->iters = k - 1;
             a.st->done = 1;
+        } else {
+            a.st->alpha_iter = k;
         }
     }
     return stop;
 }
 
-// Decisions of K7 (a5, C6): finalise rr', history, stop tests, beta.
-__device__ __forceinline__ int p_prologue(const UpdArgs &a, const unsigned long long *s_in,
-                                          int k, double &beta) {
+// Decisions after rr_k (a5, C6): finalise rr_k, hist[k], stop tests, beta_k.
+__device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k, double *hist,
+                                           double *rr, CgState *st, double &beta) {
     const double rr_new = acc_finalize(s_in);
     const double h = __dsqrt_rn(rr_new);
-    const double rr_old = a.rr[k - 1];
+    const double rr_old = rr[k - 1];
     int stop = 0, status = 0, conv = 0;
     if (!isfinite(rr_new)) {
         stop = 1;
         status = 7;
-    } else if (rr_new == 0.0 || h <= a.st->stop) {
+    } else if (rr_new == 0.0 || h <= st->stop) {
         stop = 1;
         conv = 1;
     }
     beta = __ddiv_rn(rr_new, rr_old);
     if (blockIdx.x == 0) {
-        a.hist[k] = h;
-        a.rr[k] = rr_new;
-        a.st->iters = k;
-        a.st->beta = beta;
+        hist[k] = h;
+        rr[k] = rr_new;
+        st->iters = k;
+        st->beta = beta;
         if (stop) {
-            a.st->status = status;
-            a.st->converged = conv;
-            a.st->done = 1;
+            st->status = status;
+            st->converged = conv;
+            st->done = 1;
         }
     }
     return stop;
+}
+
+// Decisions of K7 (a5, C6).
+__device__ __forceinline__ int p_prologue(const UpdArgs &a, const unsigned long long *s_in,
+                                          int k, double &beta) {
+    return rr_decision(s_in, k, a.hist, a.rr, a.st, beta);
 }
 
 template <bool IDENT>
@@ -783,6 +844,104 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[c]));
         }
     }
+}
+
+// ----------------------------------------------------------------------------------------
+// fused scheme, second kernel of iteration k (K6'): alpha_k, r -= alpha Ap, exact rr_k.
+// x is not touched here (its update for iteration k is applied by the next fused SpMV or by
+// k_cg_finish).  One part only (rows == columns).
+// ----------------------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
+                                                          unsigned long long *acc_pAp_next) {
+    __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
+    __shared__ double s_alpha;
+    __shared__ int s_stop;
+    if (a.st->done) return;
+    acc_zero_shared(sacc);
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double alpha;
+        s_stop = xr_prologue(a, s_in, k, alpha);
+        s_alpha = alpha;
+    }
+    __syncthreads();
+    if (s_stop) return;
+    if (blockIdx.x == 0)                          // consumed by K6' of k-1: free for k+1
+        for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) acc_pAp_next[i] = 0ull;
+    const double alpha = s_alpha;
+    Expansion ex[2];
+    ex[0].init();
+    ex[1].init();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t rows = a.g.rows, n2 = rows >> 1;
+    double2 *r2 = reinterpret_cast<double2 *>(a.r);
+    const double2 *q2 = reinterpret_cast<const double2 *>(a.Ap);
+    int64_t i = tid;
+    for (; i + stride < n2; i += 2 * stride) {
+        double2 ra = r2[i], qa = q2[i], rb = r2[i + stride], qb = q2[i + stride];
+        ra.x = __dsub_rn(ra.x, __dmul_rn(alpha, qa.x));
+        ra.y = __dsub_rn(ra.y, __dmul_rn(alpha, qa.y));
+        rb.x = __dsub_rn(rb.x, __dmul_rn(alpha, qb.x));
+        rb.y = __dsub_rn(rb.y, __dmul_rn(alpha, qb.y));
+        r2[i] = ra;
+        r2[i + stride] = rb;
+        ex[0].add(__dmul_rn(ra.x, ra.x), sacc);
+        ex[1].add(__dmul_rn(ra.y, ra.y), sacc);
+        ex[0].add(__dmul_rn(rb.x, rb.x), sacc);
+        ex[1].add(__dmul_rn(rb.y, rb.y), sacc);
+    }
+    for (; i < n2; i += stride) {
+        double2 ra = r2[i], qa = q2[i];
+        ra.x = __dsub_rn(ra.x, __dmul_rn(alpha, qa.x));
+        ra.y = __dsub_rn(ra.y, __dmul_rn(alpha, qa.y));
+        r2[i] = ra;
+        ex[0].add(__dmul_rn(ra.x, ra.x), sacc);
+        ex[1].add(__dmul_rn(ra.y, ra.y), sacc);
+    }
+    if ((rows & 1) && tid == 0) {
+        const int64_t j = rows - 1;
+        const double rj = __dsub_rn(a.r[j], __dmul_rn(alpha, a.Ap[j]));
+        a.r[j] = rj;
+        ex[0].add(__dmul_rn(rj, rj), sacc);
+    }
+    ex[0].flush(sacc);
+    ex[1].flush(sacc);
+    __syncthreads();
+    acc_merge_to_global(sacc, a.acc_out);
+}
+
+// After the last iteration K: finalise rr_K (hist[K], stop flags) unless a stop test already
+// fired, then apply the pending x update x += fl(alpha_j p_j) if iteration j = alpha_iter has
+// not been applied yet (p_j lives in buffer j % 2).
+__global__ void __launch_bounds__(UPD_THREADS) k_cg_finish(UpdArgs a, int K, const double *p_even,
+                                                           const double *p_odd) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    __shared__ int s_apply, s_iter;
+    __shared__ double s_alpha;
+    const int done = a.st->done;
+    if (!done && blockIdx.x == 0) {
+        acc_load_shared(s_in, a.acc_in);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double beta;
+            rr_decision(s_in, K, a.hist, a.rr, a.st, beta);
+        }
+    }
+    if (threadIdx.x == 0) {
+        s_iter = a.st->alpha_iter;
+        s_apply = s_iter > a.st->x_done;
+        s_alpha = a.st->alpha;
+    }
+    __syncthreads();
+    if (!s_apply) return;
+    const double *p = (s_iter & 1) ? p_odd : p_even;
+    const double alpha = s_alpha;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride)
+        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, p[i]));
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1096,6 +1255,8 @@ static void query_occupancy() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_bps, k_update_xr<true>, UPD_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updp_bps, k_update_p<true>, UPD_THREADS, 0);
     if (g_updp_bps <= 0) g_updp_bps = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updr_bps, k_update_r, UPD_THREADS, 0);
+    if (g_updr_bps <= 0) g_updr_bps = 1;
     if (g_sms <= 0) g_sms = 148;
     for (int f = 0; f < 2; ++f)
         if (g_spmv_bps[f] <= 0) g_spmv_bps[f] = 1;
@@ -1129,22 +1290,32 @@ cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <bool DOT, int FMT, bool IDENT>
+template <bool DOT, int FMT, bool IDENT, bool FUSED = false>
 static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
     constexpr int SMEM = FMT == FMT_SEG ? SEG_SMEM : CRS_SMEM;
     static unsigned long long attr_set = 0;   // per instantiation, one bit per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!((attr_set >> (dev & 63)) & 1ull)) {
-        cudaError_t e = cudaFuncSetAttribute(k_spmv_tma<DOT, FMT, IDENT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set |= 1ull << (dev & 63);
-    }
+    cudaError_t e = ensure_smem_attr(k_spmv_tma<DOT, FMT, IDENT, FUSED>, SMEM, attr_set);
+    if (e != cudaSuccess) return e;
     query_occupancy();
     const int64_t ntiles = (a.m.nslices + TILE - 1) / TILE;
     const int grid = (int)std::min<int64_t>(ntiles, g_sms);
-    k_spmv_tma<DOT, FMT, IDENT><<<grid > 0 ? grid : 1, TMA_THREADS, SMEM, s>>>(a);
+    k_spmv_tma<DOT, FMT, IDENT, FUSED><<<grid > 0 ? grid : 1, TMA_THREADS, SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp_next_zero,
+                            int grid, cudaStream_t s) {
+    query_occupancy();
+    const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
+    const int g6 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updr_bps));
+    (void)grid;
+    k_update_r<<<g6, UPD_THREADS, 0, s>>>(a, k, acc_pAp_next_zero);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_finish(const UpdArgs &a, int K, const double *p_even, const double *p_odd,
+                             int grid, cudaStream_t s) {
+    k_cg_finish<<<grid, UPD_THREADS, 0, s>>>(a, K, p_even, p_odd);
     return cudaGetLastError();
 }
 
@@ -1162,6 +1333,10 @@ static int spmv_impl(int fmt) {
 }
 
 cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t s) {
+    if (a.fused_k > 0) {
+        if (a.m.fmt != FMT_SEG || !a.g.ident || !with_dot) return cudaErrorInvalidValue;
+        return launch_tma<true, FMT_SEG, true, true>(a, s);
+    }
     if (spmv_impl(a.m.fmt) == 1) {
         if (a.m.fmt == FMT_SEG)
             return with_dot ? launch_tma<true, FMT_SEG, true>(a, s)

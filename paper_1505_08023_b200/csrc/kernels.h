@@ -22,6 +22,8 @@ struct CgState {
     int converged;
     double stop;       // fl(tol * hist[0])
     double pAp, alpha, beta;
+    int alpha_iter;    // fused scheme: iteration whose alpha is in `alpha`
+    int x_done;        // fused scheme: last iteration whose x update has been applied
 };
 
 // Row -> column map: rows are the owned box, columns the extended box (plan.h).
@@ -67,6 +69,15 @@ struct SpmvArgs {
     unsigned long long *acc;            // pAp accumulator (DOT only)
     unsigned long long *acc_zero;       // accumulator to clear (CTA 0), may be null
     const CgState *st;                  // early exit when st->done (may be null)
+    // fused CG iteration (one part, SEG format): the SpMV operand is
+    // p_k = r + beta_{k-1} p_{k-1} formed at gather time (p_1 = r), written to p_new for the
+    // own rows, and x += alpha_{k-1} p_{k-1} is applied for the own rows.
+    int fused_k;                        // 0: plain SpMV; k >= 1: fused iteration k
+    const double *r, *p_old;
+    double *p_new, *xsol;
+    unsigned long long *acc_rr_in;      // rr_{k-1} accumulator (k >= 2)
+    double *hist, *rr;
+    CgState *stw;                       // writable state (decisions)
 };
 
 struct UpdArgs {
@@ -93,6 +104,11 @@ cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s);
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s);
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s);
+// fused scheme: K6' (alpha_k; r -= alpha Ap; exact rr) and the finish kernel (rr_K, pending x)
+cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp_next_zero,
+                            int grid, cudaStream_t s);
+cudaError_t launch_cg_finish(const UpdArgs &a, int K, const double *p_even, const double *p_odd,
+                             int grid, cudaStream_t s);
 
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,

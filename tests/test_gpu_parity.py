@@ -187,6 +187,25 @@ def test_profile_mode_matches_graph_mode():
         assert _same(g.history(), h1) and _same(g.solution(), x1)
 
 
+@pytest.mark.parametrize("n", [(1, 1, 1), (10, 10, 10), (23, 17, 9), (33, 32, 31)])
+def test_fused_scheme_bit_identical(n):
+    """SURVEY §8(f) NEXT #2: the fused two-kernel iteration performs C6 exactly."""
+    s = oracle_system(n)
+    with M.Minife(*n) as g:
+        g.set_scheme(M.SCHEME_FUSED)
+        g.assemble()
+        check_cg(g, n, 200, 0.0)
+        check_cg(g, n, 200, 1e-8)       # stop inside the fused prologue -> pending x update
+        check_cg(g, n, 7, 0.0)          # odd count: p_K in the second buffer
+        check_cg(g, n, 8, 0.0)
+        t = g.cg_profile(50)
+        assert t.update_p_launches == 1 and t.spmv_ms > 0
+        check_cg(g, n, 50, 0.0)
+        g.set_scheme(M.SCHEME_3K)
+        check_cg(g, n, 200, 0.0)
+        check_spmv(g, s, 12345)
+
+
 def test_format_switch_keeps_results():
     n = (14, 13, 12)
     s = oracle_system(n)
