@@ -77,6 +77,59 @@ struct Expansion {
         for (int j = 0; j < NEXP; ++j)
             if (c[j] != 0.0) acc_add(acc, c[j]);
     }
+    // Warp-aggregated flush (all 32 lanes must call it, converged).  For each component
+    // index j the lanes' values are cut into signed 16-bit chunks on a common grid anchored
+    // at the warp's largest value (digit D weighs 2^(16 D - 1074)); 13 integer warp sums
+    // (REDUX) cover the window D in [Dmax-8, Dmax+4], and lane 0 adds each nonzero sum
+    // (|sum| < 2^21) to the accumulator word D/2.  A value more than 128 bits below the
+    // warp's largest one, or non-finite, takes acc_add.  Exact: integer sums of exact chunks.
+    __device__ __forceinline__ void warp_flush(unsigned long long *acc) const {
+        const unsigned FULL = 0xffffffffu;
+        const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+        for (int j = 0; j < NEXP; ++j) {
+            const double v = c[j];
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+            const int e = (int)((bits >> 52) & 0x7ff);
+            const unsigned long long frac = bits & 0xfffffffffffffull;
+            const bool nz = (e != 0 || frac != 0) && e != 0x7ff;
+            const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
+            const int pos = e ? e - 1 : 0;
+            const int d16 = pos >> 4, s16 = pos & 15;
+            const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
+            if (e == 0x7ff) acc_add(acc, v);                      // flag word
+            if (dmax1 == 0u) continue;                            // warp-uniform
+            const int lo = (int)dmax1 - 1 - 8;
+            const bool inwin = nz && d16 >= lo;
+            if (nz && !inwin) acc_add(acc, v);                    // far below: slow path
+            // m << s16 as five 16-bit chunks (m < 2^53, s16 < 16: < 2^69)
+            const unsigned long long mlo = m << s16;
+            const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
+            int ch[5];
+            ch[0] = (int)(mlo & 0xffff);
+            ch[1] = (int)((mlo >> 16) & 0xffff);
+            ch[2] = (int)((mlo >> 32) & 0xffff);
+            ch[3] = (int)(mlo >> 48);
+            ch[4] = (int)mhi;
+            if (bits >> 63) {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
+            }
+#pragma unroll
+            for (int t = 0; t < 13; ++t) {
+                const int D = lo + t;
+                const int q = D - d16;
+                int contrib = 0;
+#pragma unroll
+                for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
+                const int sum = __reduce_add_sync(FULL, contrib);
+                if (lane == 0 && sum != 0 && D >= 0) {
+                    const long long val = (long long)sum * ((D & 1) ? 65536ll : 1ll);
+                    atomicAdd(&acc[D >> 1], (unsigned long long)val);
+                }
+            }
+        }
+    }
 };
 
 // CTA helpers: zero the shared words (all threads), merge them into a global accumulator.

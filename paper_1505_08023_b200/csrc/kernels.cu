@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
         }
     }
     if (DOT) {
-        ex.flush(sacc);
+        ex.warp_flush(sacc);
         __syncthreads();
         acc_merge_to_global(sacc, a.acc);
     }
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_seg(SpmvArgs a) {
         }
     }
     if (DOT) {
-        ex.flush(sacc);
+        ex.warp_flush(sacc);
         __syncthreads();
         acc_merge_to_global(sacc, a.acc);
     }
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
-        if (DOT) ex.flush(sacc);
+        if (DOT) ex.warp_flush(sacc);
     }
     if (DOT) {
         __syncthreads();
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
         a.p[IDENT ? i : row_to_col(a.g, i)] = bi;
         ex.add(__dmul_rn(bi, bi), sacc);
     }
-    ex.flush(sacc);
+    ex.warp_flush(sacc);
     __syncthreads();
     acc_merge_to_global(sacc, a.acc_out);
 }
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
             a.r[i] = ri;
         }
     }
-    ex.flush(sacc);
+    ex.warp_flush(sacc);
     __syncthreads();
     acc_merge_to_global(sacc, a.acc_out);
 }
@@ -907,8 +907,8 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
         a.r[j] = rj;
         ex[0].add(__dmul_rn(rj, rj), sacc);
     }
-    ex[0].flush(sacc);
-    ex[1].flush(sacc);
+    ex[0].warp_flush(sacc);
+    ex[1].warp_flush(sacc);
     __syncthreads();
     acc_merge_to_global(sacc, a.acc_out);
 }
@@ -1047,8 +1047,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
             if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
         if (XR) {
-            ex[0].flush(sacc);
-            ex[1].flush(sacc);
+            ex[0].warp_flush(sacc);
+            ex[1].warp_flush(sacc);
         }
     }
     if (XR) {
