@@ -51,6 +51,11 @@ extern "C" {
                                   x-run ("non-zero segment") + a 27-bit presence mask: the
                                   paper's BCRS (Fig 3.2) on the GPU; 8 B per entry
                                   + 4 B per segment.  Default.                                */
+#define MINIFE_FMT_SYM 2       /* MINIFE_FMT_SEG storing only the upper-triangle value slots
+                                  (14 per row incl. the diagonal); a lower entry a_ij is read
+                                  from row j's mirror slot (a_ij == a_ji bitwise: the assembled
+                                  system is exactly symmetric, C2/C3).  Single-part ctxs only;
+                                  results identical to the other formats.                     */
 
 /* ---- CG iteration schemes ------------------------------------------------- */
 #define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | x/r update + rr | p update.      */
@@ -240,6 +245,10 @@ int minife_plan_lists(int nx, int ny, int nz, int world, int rank, int64_t *ext_
  * MINIFE_ENOMEM, MINIFE_ECUDA. */
 int minife_bandwidth_probe(int device, int64_t bytes, int reps, double *read_gbs,
                            double *copy_gbs);
+
+/* L2-resident read rate (GB/s) of the bulk-copy engine measured by the last
+ * minife_bandwidth_probe call on this process (48 MB buffer re-read); 0 before any probe. */
+double minife_probe_l2_read_gbs(void);
 
 /* Library version string. */
 const char *minife_version(void);

@@ -40,7 +40,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 MINIFE_OK, MINIFE_EINVAL, MINIFE_ESTATE, MINIFE_ECUDA, MINIFE_ENCCL = 0, 1, 2, 3, 4
 MINIFE_ENOMEM, MINIFE_ENOTSPD, MINIFE_EDIVERGED, MINIFE_ENODEV = 5, 6, 7, 8
 MODE_SINGLE, MODE_VIRTUAL, MODE_MULTI, MODE_RANK = 0, 1, 2, 3
-FMT_CRS, FMT_SEG = 0, 1
+FMT_CRS, FMT_SEG, FMT_SYM = 0, 1, 2
 SCHEME_3K, SCHEME_FUSED = 0, 1
 
 
@@ -116,6 +116,7 @@ SIGNATURES = {
     "minife_plan": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(minife_part_info)]),
     "minife_plan_lists": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "minife_bandwidth_probe": (_I, [_I, _I64, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
+    "minife_probe_l2_read_gbs": (_D, []),
     "minife_version": (ctypes.c_char_p, []),
 }
 

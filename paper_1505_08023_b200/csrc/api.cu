@@ -205,6 +205,14 @@ static void dfree(Part &p, T *&ptr, size_t n) {
     p.bytes -= (n ? n : 1) * sizeof(T);
 }
 
+// column vector (+32 doubles of padding: TMA tile copies round their size up to 16 B), zeroed
+static int alloc_colvec(minife_ctx *c, Part &p, double **ptr) {
+    const size_t n = (size_t)(p.ncols + 32);
+    TRY(dalloc(c, p, ptr, n));
+    CUDA_TRY(c, cudaMemset(*ptr, 0, n * sizeof(double)));
+    return MINIFE_OK;
+}
+
 static void free_matrix(Part &p) {
     DevGuard g(p.dev);
     for (void **b : {(void **)&p.d_col, (void **)&p.d_seg, (void **)&p.d_mask, (void **)&p.d_val}) {
@@ -278,14 +286,13 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     TRY(dalloc(c, p, &p.d_b, p.rows + 32));
     TRY(dalloc(c, p, &p.d_x, p.rows + 32));
     TRY(dalloc(c, p, &p.d_r, p.rows + 32));
-    TRY(dalloc(c, p, &p.d_p, p.ncols + 32));
+    TRY(alloc_colvec(c, p, &p.d_p));
     TRY(dalloc(c, p, &p.d_Ap, p.rows + 32));
     TRY(dalloc(c, p, &p.d_acc, 4 * ACC_WORDS));
     TRY(dalloc(c, p, &p.d_st, 1));
     TRY(alloc_hist(c, p, 201));
     CUDA_TRY(c, cudaMemset(p.d_acc, 0, 4 * ACC_WORDS * sizeof(unsigned long long)));
     CUDA_TRY(c, cudaMemset(p.d_st, 0, sizeof(CgState)));
-    CUDA_TRY(c, cudaMemset(p.d_p, 0, p.ncols * sizeof(double)));
     // halo index lists, as extended columns
     std::vector<int32_t> send_col(plan.send_idx.size()), recv_pos(plan.n_ext);
     for (size_t i = 0; i < plan.send_idx.size(); ++i)
@@ -467,7 +474,12 @@ extern "C" int minife_set_scheme(minife_ctx *c, int scheme) {
 }
 
 extern "C" int minife_set_format(minife_ctx *c, int format) {
-    if (!c || (format != MINIFE_FMT_CRS && format != MINIFE_FMT_SEG)) return MINIFE_EINVAL;
+    if (!c || (format != MINIFE_FMT_CRS && format != MINIFE_FMT_SEG && format != MINIFE_FMT_SYM))
+        return MINIFE_EINVAL;
+    if (format == MINIFE_FMT_SYM && !(c->parts.size() == 1 && c->parts[0].ncols == c->parts[0].rows)) {
+        set_err(c, "MINIFE_FMT_SYM needs a single part (mirror rows must be local)");
+        return MINIFE_EINVAL;
+    }
     if (format != c->fmt) {
         c->fmt = format;
         c->assembled = false;
@@ -506,6 +518,11 @@ extern "C" int minife_bandwidth_probe(int device, int64_t bytes, int reps, doubl
     if (e == cudaErrorMemoryAllocation) return MINIFE_ENOMEM;
     return e == cudaSuccess ? MINIFE_OK : MINIFE_ECUDA;
 }
+
+namespace minife {
+extern double g_l2_read_gbs;
+}
+extern "C" double minife_probe_l2_read_gbs(void) { return minife::g_l2_read_gbs; }
 extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
 
 // ----------------------------------------------------------------------------------------
@@ -556,13 +573,15 @@ extern "C" int minife_assemble(minife_ctx *c) {
                                         cudaMemcpyHostToDevice, s));
             CUDA_TRY(c, cudaStreamSynchronize(s));
         } else {
-            const int64_t entries = 27 * 32 * p.nslices;
-            if (!p.d_seg) {
+            // SEG: 27 value slots per row; SYM: the 14 upper slots
+            const int64_t entries = (c->fmt == MINIFE_FMT_SYM ? 14 : 27) * 32 * p.nslices;
+            if (!p.d_seg || entries != p.entries) {
                 free_matrix(p);
                 TRY(dalloc(c, p, &p.d_val, entries));
+                const size_t vbytes = 8 * (size_t)entries;
                 TRY(dalloc(c, p, &p.d_seg, 9 * 32 * p.nslices));
                 TRY(dalloc(c, p, &p.d_mask, 32 * p.nslices));   // padded: whole-slice copies
-                p.matrix_bytes = 8 * (size_t)entries + 4 * (size_t)(9 * 32 * p.nslices) +
+                p.matrix_bytes = vbytes + 4 * (size_t)(9 * 32 * p.nslices) +
                                  4 * (size_t)(32 * p.nslices);
                 p.entries = entries;
             }
@@ -803,8 +822,7 @@ static int ensure_fused_buffers(minife_ctx *c) {   // never called while a strea
     if (fused_mode(c) && !c->parts[0].d_p2) {
         Part &p = c->parts[0];
         DevGuard g(p.dev);
-        TRY(dalloc(c, p, &p.d_p2, p.ncols + 32));
-        CUDA_TRY(c, cudaMemset(p.d_p2, 0, (p.ncols + 32) * sizeof(double)));
+        TRY(alloc_colvec(c, p, &p.d_p2));
     }
     return MINIFE_OK;
 }
@@ -829,6 +847,9 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
 
 static double spmv_alg_bytes(const minife_ctx *c, const Part &q) {
     // CRS 12 nnz (+16 rows of x/y); segment format 8 nnz + 4 nns (+16 rows)
+    // SYM: values of the upper triangle incl. the diagonal, (nnz + rows) / 2
+    if (c->fmt == MINIFE_FMT_SYM)
+        return 8.0 * 0.5 * (double)(q.nnz + q.rows) + 4.0 * (double)q.nns;
     return c->fmt == MINIFE_FMT_CRS ? 12.0 * (double)q.nnz
                                     : 8.0 * (double)q.nnz + 4.0 * (double)q.nns;
 }
@@ -1012,7 +1033,7 @@ extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         if (!p.d_xin) {
-            TRY(dalloc(c, p, &p.d_xin, p.ncols));
+            TRY(alloc_colvec(c, p, &p.d_xin));
             TRY(dalloc(c, p, &p.d_yout, p.rows));
         }
         const double *src = x;

@@ -23,6 +23,7 @@ static void query_occupancy();
 static int g_sms = 0;                      // SMs of the current device (occupancy queries)
 static int g_spmv_bps[2] = {0, 0};
 static int g_upd_bps = 0, g_updp_bps = 0, g_updr_bps = 0;
+double g_l2_read_gbs = 0.0;                // last probe_bandwidth: L2-resident TMA read rate
 
 // opt a kernel into > 48 KB dynamic shared memory, once per device
 template <class K>
@@ -158,12 +159,19 @@ __global__ void k_assemble(AsmArgs a) {
                 a.val[base + 32 * k] = 0.0;
             }
         } else {
-            for (int t = 0; t < 27; ++t) a.val[(27 * s + t) * 32 + lane] = 0.0;
+            const int nslot = a.fmt == FMT_SYM ? 14 : 27;
+            for (int t = 0; t < nslot; ++t) a.val[(nslot * s + t) * 32 + lane] = 0.0;
             for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
             a.mask[row] = 0u;                      // mask is padded to 32 * slices
         }
         return;
     }
+    // value slot t of this row: SEG stores all 27 stencil slots, SYM the upper slots t >= 13
+    // (both SELL-32, k-major)
+    const bool sym = a.fmt == FMT_SYM;
+    auto vptr = [&](int t) -> double * {
+        return sym ? a.val + (14 * s + (t - 13)) * 32 + lane : a.val + (27 * s + t) * 32 + lane;
+    };
     double K[8];
     element_operator(g.nx, g.ny, g.nz, K);
     int lx, ly, lz;
@@ -186,13 +194,13 @@ __global__ void k_assemble(AsmArgs a) {
             const int64_t start = (int64_t)(ex - 1) +
                                   (int64_t)g.ext_n[0] * ((int64_t)(ey + dy) +
                                                          (int64_t)g.ext_n[1] * (ez + dz));
-            if (a.fmt == FMT_SEG) a.seg[(9 * s + jgrp) * 32 + lane] = grp_in ? (int32_t)start : 0;
+            if (a.fmt != FMT_CRS) a.seg[(9 * s + jgrp) * 32 + lane] = grp_in ? (int32_t)start : 0;
             for (int dx = -1; dx <= 1; ++dx) {
                 const int t = jgrp * 3 + (dx + 1);
                 const int jx = ix + dx;
                 const bool in = grp_in && jx >= 0 && jx <= g.nx;
                 if (!in) {
-                    if (a.fmt == FMT_SEG) a.val[(27 * s + t) * 32 + lane] = 0.0;
+                    if (a.fmt == FMT_SEG || (sym && t >= 13)) *vptr(t) = 0.0;
                     continue;
                 }
                 const int c = (dx ? 1 : n_el[0]) * (dy ? 1 : n_el[1]) * (dz ? 1 : n_el[2]);
@@ -211,7 +219,7 @@ __global__ void k_assemble(AsmArgs a) {
                     a.col[base + 32 * k] = (int32_t)(start + dx + 1);
                     a.val[base + 32 * k] = v;
                 } else {
-                    a.val[(27 * s + t) * 32 + lane] = v;
+                    if (!sym || t >= 13) *vptr(t) = v;   // SYM: lower half is mirrored
                     mask |= 1u << t;
                 }
                 ++k;
@@ -382,6 +390,13 @@ constexpr int CRS_VAL_B = TILE * 27 * 32 * 8, CRS_COL_B = TILE * 27 * 32 * 4,
 constexpr int CRS_STAGE_B = CRS_VAL_B + CRS_COL_B + CRS_LEN_B;          // 83200
 constexpr int SEG_SMEM = SEG_STAGES * SEG_STAGE_B;
 constexpr int CRS_SMEM = CRS_STAGES * CRS_STAGE_B;
+template <int FMT> struct TmaCfg;
+template <> struct TmaCfg<FMT_SEG> {
+    static constexpr int NV = 27, STAGES = SEG_STAGES, STAGE_B = SEG_STAGE_B, SMEM = SEG_SMEM;
+};
+template <> struct TmaCfg<FMT_CRS> {
+    static constexpr int NV = 27, STAGES = CRS_STAGES, STAGE_B = CRS_STAGE_B, SMEM = CRS_SMEM;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -426,8 +441,10 @@ __device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k
 // operation order are those of the three-kernel C6 sequence, so results are bit-identical.
 template <bool DOT, int FMT, bool IDENT, bool FUSED>
 __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
-    constexpr int STAGES = FMT == FMT_SEG ? SEG_STAGES : CRS_STAGES;
-    constexpr int STAGE_B = FMT == FMT_SEG ? SEG_STAGE_B : CRS_STAGE_B;
+    constexpr int STAGES = TmaCfg<FMT>::STAGES;
+    constexpr int STAGE_B = TmaCfg<FMT>::STAGE_B;
+    constexpr int NV = TmaCfg<FMT>::NV;                 // value slots per row in the tile
+    constexpr int VAL_B = TILE * NV * 32 * 8;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
     __shared__ unsigned long long sacc[ACC_WORDS];
@@ -481,14 +498,13 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
                 const int64_t rem = m.nslices - s0;
                 const int nsl = rem < TILE ? (int)rem : TILE;
                 unsigned char *buf = smem + (size_t)st * STAGE_B;
-                if (FMT == FMT_SEG) {
-                    const uint32_t bv = nsl * 27 * 32 * 8, bs = nsl * 9 * 32 * 4,
+                if (FMT != FMT_CRS) {
+                    const uint32_t bv = nsl * NV * 32 * 8, bs = nsl * 9 * 32 * 4,
                                    bm = nsl * 32 * 4;
                     mbar_expect_tx(&full_bar[st], bv + bs + bm);
-                    bulk_g2s(buf, m.val + s0 * 27 * 32, bv, &full_bar[st], pol);
-                    bulk_g2s(buf + SEG_VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
-                    bulk_g2s(buf + SEG_VAL_B + SEG_SEG_B, m.mask + s0 * 32, bm, &full_bar[st],
-                             pol);
+                    bulk_g2s(buf, m.val + s0 * NV * 32, bv, &full_bar[st], pol);
+                    bulk_g2s(buf + VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
+                    bulk_g2s(buf + VAL_B + SEG_SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
                 } else {
                     const int64_t e0 = m.slice_off[s0], e1 = m.slice_off[s0 + nsl];
                     const uint32_t ne = (uint32_t)(e1 - e0);
@@ -514,12 +530,12 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
                 const unsigned char *buf = smem + (size_t)st * STAGE_B;
                 const int64_t row = s * 32 + lane;
                 double sum = 0.0, pdiag = 0.0;
-                if (FMT == FMT_SEG) {
-                    const double *vs = reinterpret_cast<const double *>(buf) + warp * 27 * 32 + lane;
+                if (FMT != FMT_CRS) {
+                    const double *vs = reinterpret_cast<const double *>(buf) + warp * NV * 32 + lane;
                     const int32_t *ss =
-                        reinterpret_cast<const int32_t *>(buf + SEG_VAL_B) + warp * 9 * 32 + lane;
+                        reinterpret_cast<const int32_t *>(buf + VAL_B) + warp * 9 * 32 + lane;
                     const unsigned msk = reinterpret_cast<const uint32_t *>(
-                        buf + SEG_VAL_B + SEG_SEG_B)[warp * 32 + lane];
+                        buf + VAL_B + SEG_SEG_B)[warp * 32 + lane];
                     int sg[9];
 #pragma unroll
                     for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
@@ -578,6 +594,122 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
                 if (row < m.rows) {
                     a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(pdiag, sum), sacc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+        if (DOT) ex.warp_flush(sacc);
+    }
+    if (DOT) {
+        __syncthreads();
+        acc_merge_to_global(sacc, a.acc);
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// a2 in FMT_SYM (one part).  The upper value slots are stored SELL-14 (val[(14 s + u) 32 +
+// lane], u = t - 13), so a 16-slice tile is one contiguous bulk copy (plus the run starts and
+// masks).  Lower slot t < 13 of row i needs a_ij = a_ji: row j = the slot's column c, mirror
+// slot 26 - t, i.e. val[((c >> 5) 14 + 13 - t) 32 + (c & 31)] -- consecutive lanes have
+// consecutive c, so each mirrored read is a coalesced 256 B access, served by L2 (row j's
+// tile was streamed about one plane earlier).  HBM sees each stored value once.  16 consumer
+// warps per SM keep the mirrored and x reads in flight.
+// ----------------------------------------------------------------------------------------
+
+constexpr int SY_TILE = 16;                                    // slices per tile = consumers
+constexpr int SY_THREADS = 32 * (SY_TILE + 1);
+constexpr int SY_VAL_B = SY_TILE * 14 * 32 * 8;                // 57344
+constexpr int SY_SEG_B = SY_TILE * 9 * 32 * 4;                 // 18432
+constexpr int SY_MSK_B = SY_TILE * 32 * 4;                     // 2048
+constexpr int SY_STAGE_B = SY_VAL_B + SY_SEG_B + SY_MSK_B;     // 77824
+constexpr int SY_STAGES = 2;
+constexpr int SY_SMEM = SY_STAGES * SY_STAGE_B;
+
+template <bool DOT>
+__global__ void __launch_bounds__(SY_THREADS, 1) k_spmv_sym(SpmvArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full_bar[SY_STAGES], empty_bar[SY_STAGES];
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    if (DOT && a.st && a.st->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SY_STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], SY_TILE);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (DOT) {
+        acc_zero_shared(sacc);
+        if (blockIdx.x == 0 && a.acc_zero)
+            for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    }
+    __syncthreads();
+    const Matrix &m = a.m;
+    const int64_t ntiles = (m.nslices + SY_TILE - 1) / SY_TILE;
+
+    if (warp == SY_TILE) {
+        if (lane == 0) {
+            // values are read a second time (mirrored): normal L2 priority; indices: first
+            const uint64_t pol = evict_first_policy();
+            uint64_t pol_keep;
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+            int64_t i = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int st = (int)(i % SY_STAGES);
+                if (i >= SY_STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / SY_STAGES) & 1) ^ 1));
+                const int64_t s0 = tile * SY_TILE;
+                const int64_t rem = m.nslices - s0;
+                const int nsl = rem < SY_TILE ? (int)rem : SY_TILE;
+                unsigned char *buf = smem + (size_t)st * SY_STAGE_B;
+                const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
+                mbar_expect_tx(&full_bar[st], bv + bs + bm);
+                bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &full_bar[st], pol_keep);
+                bulk_g2s(buf + SY_VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
+                bulk_g2s(buf + SY_VAL_B + SY_SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
+            }
+        }
+    } else {
+        Expansion ex;
+        ex.init();
+        int64_t i = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int st = (int)(i % SY_STAGES);
+            mbar_wait(&full_bar[st], (uint32_t)((i / SY_STAGES) & 1));
+            const int64_t s = tile * SY_TILE + warp;
+            if (s < m.nslices) {
+                const unsigned char *buf = smem + (size_t)st * SY_STAGE_B;
+                const double *vs = reinterpret_cast<const double *>(buf) + warp * 14 * 32 + lane;
+                const int32_t *ss =
+                    reinterpret_cast<const int32_t *>(buf + SY_VAL_B) + warp * 9 * 32 + lane;
+                const unsigned msk =
+                    reinterpret_cast<const uint32_t *>(buf + SY_VAL_B + SY_SEG_B)[warp * 32 + lane];
+                const int64_t row = s * 32 + lane;
+                int sg[9];
+#pragma unroll
+                for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
+                double lv[13], xv[27];
+#pragma unroll
+                for (int t = 0; t < 27; ++t) {
+                    const bool on = (msk >> t) & 1u;
+                    const int c = sg[t / 3] + (t % 3);
+                    xv[t] = on ? __ldg(a.x + c) : 0.0;
+                    if (t < 13)
+                        lv[t] = on ? __ldg(m.val + ((int64_t)(c >> 5) * 14 + (13 - t)) * 32 +
+                                           (c & 31))
+                                   : 0.0;
+                }
+                double sum = 0.0;
+#pragma unroll
+                for (int t = 0; t < 13; ++t)
+                    if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(lv[t], xv[t]));
+#pragma unroll
+                for (int t = 13; t < 27; ++t)
+                    if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
+                if (row < m.rows) {
+                    a.y[row] = sum;
+                    if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);
                 }
             }
             __syncwarp();
@@ -1058,7 +1190,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
 }
 
 // Pure-read probe with the same bulk-copy engine (B_read for the TMA kernels).
-__global__ void __launch_bounds__(UT_THREADS, 1) k_read_tma(const double *src, int64_t n) {
+__global__ void __launch_bounds__(UT_THREADS, 1) k_read_tma(const double *src, int64_t n,
+                                                            int passes) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sm = reinterpret_cast<double *>(smem_raw);
     __shared__ __align__(8) uint64_t full_bar[UT_STAGES], empty_bar[UT_STAGES];
@@ -1073,20 +1206,23 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_read_tma(const double *src, i
     }
     __syncthreads();
     const int64_t ntiles = n / TD;
+    const int64_t total = ntiles * passes;          // passes > 1: L2-resident re-reads
     if (warp == UT_CWARPS) {
         if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
+            uint64_t pol = evict_first_policy();
+            if (passes > 1)
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
             int64_t i = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++i) {
                 const int st = (int)(i % UT_STAGES);
                 if (i >= UT_STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / UT_STAGES) & 1) ^ 1));
                 mbar_expect_tx(&full_bar[st], TD * 8);
-                bulk_g2s(sm + (size_t)st * TD, src + t * TD, TD * 8, &full_bar[st], pol);
+                bulk_g2s(sm + (size_t)st * TD, src + (t % ntiles) * TD, TD * 8, &full_bar[st], pol);
             }
         }
     } else {
         int64_t i = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++i) {
             const int st = (int)(i % UT_STAGES);
             mbar_wait(&full_bar[st], (uint32_t)((i / UT_STAGES) & 1));
             __syncwarp();
@@ -1180,13 +1316,31 @@ cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *c
         float ms = 0.f;
         cudaEventRecord(e0);
         k_read_tma<<<g_sms, UT_THREADS, UT_STAGES * 4 * UT_ROWS * 8>>>(
-            reinterpret_cast<const double *>(a), (n2 * 2) / (4 * UT_ROWS) * (4 * UT_ROWS));
+            reinterpret_cast<const double *>(a), (n2 * 2) / (4 * UT_ROWS) * (4 * UT_ROWS), 1);
         cudaEventRecord(e1);
         e = cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         const float scaled = ms * (float)((double)(n2 * 16) /
                                           (double)((n2 * 2) / (4 * UT_ROWS) * (4 * UT_ROWS) * 8));
         if (r > 0) best_r = std::min(best_r, scaled);
+    }
+    // L2-resident read through the same engine: a 48 MB buffer (fits the 126 MB L2) read 40
+    // times within one launch
+    {
+        const int64_t nl = (int64_t)6 << 20;                     // doubles = 48 MB
+        const int passes = 40;
+        float best_l2 = 1e30f;
+        for (int r = 0; e == cudaSuccess && r < reps + 2; ++r) {
+            float ms = 0.f;
+            cudaEventRecord(e0);
+            k_read_tma<<<g_sms, UT_THREADS, UT_STAGES * 4 * UT_ROWS * 8>>>(
+                reinterpret_cast<const double *>(a), nl, passes);
+            cudaEventRecord(e1);
+            e = cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r > 1) best_l2 = std::min(best_l2, ms);
+        }
+        g_l2_read_gbs = (double)(nl * 8) * passes / (best_l2 * 1e-3) / 1e9;
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaFree(a);
@@ -1231,8 +1385,14 @@ __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t
         const unsigned msk = m.mask[row];
         for (int t = 0; t < 27; ++t) {
             if (!((msk >> t) & 1u)) continue;
-            out_col[27 * i + len] = m.seg[(9 * s + t / 3) * 32 + lane] + t % 3;
-            out_val[27 * i + len] = m.val[(27 * s + t) * 32 + lane];
+            const int c = m.seg[(9 * s + t / 3) * 32 + lane] + t % 3;
+            out_col[27 * i + len] = c;
+            if (m.fmt == FMT_SEG)
+                out_val[27 * i + len] = m.val[(27 * s + t) * 32 + lane];
+            else if (t >= 13)                  // SYM: own upper slot
+                out_val[27 * i + len] = m.val[(14 * s + (t - 13)) * 32 + lane];
+            else                               // SYM: mirror slot of row c (one part)
+                out_val[27 * i + len] = m.val[((int64_t)(c >> 5) * 14 + (13 - t)) * 32 + (c & 31)];
             ++len;
         }
     }
@@ -1292,7 +1452,7 @@ cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
 
 template <bool DOT, int FMT, bool IDENT, bool FUSED = false>
 static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
-    constexpr int SMEM = FMT == FMT_SEG ? SEG_SMEM : CRS_SMEM;
+    constexpr int SMEM = TmaCfg<FMT>::SMEM;
     static unsigned long long attr_set = 0;   // per instantiation, one bit per device
     cudaError_t e = ensure_smem_attr(k_spmv_tma<DOT, FMT, IDENT, FUSED>, SMEM, attr_set);
     if (e != cudaSuccess) return e;
@@ -1328,6 +1488,7 @@ static int spmv_impl(int fmt) {
         const char *e = getenv("MINIFE_SPMV_IMPL");
         forced = !e ? -1 : (e[0] == 't' ? 1 : (e[0] == 'r' ? 0 : -1));
     }
+    if (fmt == FMT_SYM) return 1;                       // TMA kernel only
     if (forced >= 0) return forced;
     return fmt == FMT_SEG ? 1 : 0;
 }
@@ -1336,6 +1497,19 @@ cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t
     if (a.fused_k > 0) {
         if (a.m.fmt != FMT_SEG || !a.g.ident || !with_dot) return cudaErrorInvalidValue;
         return launch_tma<true, FMT_SEG, true, true>(a, s);
+    }
+    if (a.m.fmt == FMT_SYM) {
+        if (!a.g.ident) return cudaErrorInvalidValue;        // one part only
+        static unsigned long long m0 = 0, m1 = 0;
+        cudaError_t e = with_dot ? ensure_smem_attr(k_spmv_sym<true>, SY_SMEM, m1)
+                                 : ensure_smem_attr(k_spmv_sym<false>, SY_SMEM, m0);
+        if (e != cudaSuccess) return e;
+        query_occupancy();
+        const int64_t ntiles = (a.m.nslices + SY_TILE - 1) / SY_TILE;
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
+        if (with_dot) k_spmv_sym<true><<<g, SY_THREADS, SY_SMEM, s>>>(a);
+        else k_spmv_sym<false><<<g, SY_THREADS, SY_SMEM, s>>>(a);
+        return cudaGetLastError();
     }
     if (spmv_impl(a.m.fmt) == 1) {
         if (a.m.fmt == FMT_SEG)

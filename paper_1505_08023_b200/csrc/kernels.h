@@ -11,7 +11,11 @@ namespace minife {
 //   FMT_SEG: SELL-32 with 27 value slots per row (stencil order), one int32 column per x-run
 //            ("non-zero segment") and a 27-bit presence mask — the GPU form of the paper's
 //            BCRS (Fig 3.2): "jas" = run start, the mask replaces "offsets".
-enum { FMT_CRS = 0, FMT_SEG = 1 };
+//   FMT_SYM: FMT_SEG with only the upper-triangle value slots stored (14 per row, stencil
+//            slots 13..26 incl. the diagonal); a lower entry a_ij (j < i) is read from row j's
+//            mirror slot, a_ij == a_ji exactly (the assembled system is bitwise symmetric,
+//            pinned by the oracle tests).  One part only (rows == columns).
+enum { FMT_CRS = 0, FMT_SEG = 1, FMT_SYM = 2 };
 
 // Device-resident CG scalars of one part (C6).  Written only by CTA 0 of the kernel that
 // takes the decision; every CTA computes the same decision from the same exact values.
@@ -42,11 +46,12 @@ struct Matrix {
     int fmt;
     int64_t rows, nslices;
     const double *val;                  // CRS: [slice_off[s] + 32k + lane]; SEG: [(27s + t)32 + lane]
+                                        // SYM: [(14s + t - 13)32 + lane], t >= 13
     const int64_t *slice_off;           // CRS only [nslices+1]
     const uint8_t *row_len;             // CRS only [rows]
     const int32_t *col;                 // CRS only
-    const int32_t *seg;                 // SEG only: [(9s + j)32 + lane], start column of run j
-    const uint32_t *mask;               // SEG only: [rows], bit t = slot t present
+    const int32_t *seg;                 // SEG/SYM: [(9s + j)32 + lane], start column of run j
+    const uint32_t *mask;               // SEG/SYM: [32 slices], bit t = slot t present
 };
 
 struct AsmArgs {
@@ -55,8 +60,8 @@ struct AsmArgs {
     const int64_t *slice_off;           // CRS
     uint8_t *row_len;                   // CRS
     int32_t *col;                       // CRS
-    int32_t *seg;                       // SEG
-    uint32_t *mask;                     // SEG
+    int32_t *seg;                       // SEG / SYM
+    uint32_t *mask;                     // SEG / SYM
     double *val;
     double *b;                          // [rows]
 };

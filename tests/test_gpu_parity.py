@@ -73,10 +73,11 @@ def check_cg(g, n, iters, tol):
     assert _same(x, o.x)
 
 
-FORMATS = [M.FMT_SEG, M.FMT_CRS]
+FORMATS = [M.FMT_SEG, M.FMT_CRS]           # every process model
+ALL_FORMATS = FORMATS + [M.FMT_SYM]         # single-part ctxs
 
 
-@pytest.mark.parametrize("fmt", FORMATS)
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
 @pytest.mark.parametrize("n", MESHES)
 def test_single_gpu_matrix_spmv_cg(n, fmt):
     s = oracle_system(n)
@@ -121,7 +122,7 @@ def test_plan_on_device_matches_host_plan():
             assert g.part_info(r).sell_entries == M.plan(*n, p, r).sell_entries
 
 
-@pytest.mark.parametrize("fmt", FORMATS)
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
 def test_rank_mode_world1_nccl_path(fmt):
     """SPMD entry point with a 1-rank NCCL communicator (exercises NCCL + graph capture)."""
     n = (10, 10, 10)
@@ -230,7 +231,7 @@ def test_format_switch_keeps_results():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("fmt", FORMATS)
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
 def test_100cubed_full_parity(fmt):
     """configs[1] at full size: matrix, SpMV and the 200-iteration CG, element by element."""
     n = (100, 100, 100)
@@ -251,24 +252,27 @@ def test_300cubed_sampled_parity():
     rng = np.random.default_rng(0)
     gids = np.unique(np.concatenate([rng.integers(0, rows, 400),
                                      [0, 1, 300, 301, rows // 2, rows - 1, rows - 302]]))
-    with M.Minife(*n) as g:
-        g.assemble()
-        cols, vals, lens = g.export_rows(gids)
-        x = minife_inputs.uniform_pm1(rows, 12345)
-        y = g.spmv(x)
-        for i, gid in enumerate(gids):
-            oc, ov, ob = O.row(*n, int(gid))
-            assert lens[i] == oc.size
-            assert np.array_equal(cols[i, :lens[i]], oc)
-            assert _same(vals[i, :lens[i]], ov)
-            yo = O.spmv(np.array([0, oc.size]), oc, ov, x)[0]
-            assert y[gid] == yo
-        r1 = g.cg_solve(200, 0.0)
-        h1 = g.history()
-        x1 = g.solution()
+    x = minife_inputs.uniform_pm1(rows, 12345)
+    results = []
+    for fmt in (M.FMT_SYM, M.FMT_SEG):
+        with M.Minife(*n, fmt=fmt) as g:
+            g.assemble()
+            cols, vals, lens = g.export_rows(gids)
+            y = g.spmv(x)
+            for i, gid in enumerate(gids):
+                oc, ov, ob = O.row(*n, int(gid))
+                assert lens[i] == oc.size
+                assert np.array_equal(cols[i, :lens[i]], oc)
+                assert _same(vals[i, :lens[i]], ov)
+                yo = O.spmv(np.array([0, oc.size]), oc, ov, x)[0]
+                assert y[gid] == yo
+            r1 = g.cg_solve(200, 0.0)
+            assert r1.iterations == 200
+            results.append((g.history(), g.solution()))
     with M.Minife(*n, virtual=2) as g2:
         g2.assemble()
         r2 = g2.cg_solve(200, 0.0)
-        assert r2.iterations == r1.iterations == 200
-        assert _same(g2.history(), h1)
-        assert _same(g2.solution(), x1)
+        assert r2.iterations == 200
+        for h1, x1 in results:
+            assert _same(g2.history(), h1)
+            assert _same(g2.solution(), x1)
