@@ -65,6 +65,14 @@ extern "C" {
                                /* the SpMV and x is updated one iteration late there; a second */
                                /* kernel does r and rr.  72 B per row, 2 launches.            */
 
+/* ---- halo transports of VIRTUAL ctxs ------------------------------------------------------ */
+#define MINIFE_TRANSPORT_DIRECT 0  /* gather the owner's columns straight into the receiver's
+                                      halo columns (one kernel per neighbor pair). Default.   */
+#define MINIFE_TRANSPORT_WIRE 1    /* the RANK/MULTI wire protocol: pack the send lists, move
+                                      each neighbor block into the receiver's contiguous
+                                      receive buffer (device copies standing in for
+                                      ncclSend/ncclRecv), unpack into the halo columns.       */
+
 typedef struct minife_ctx minife_ctx;
 
 /* Per-part (per-rank) plan, host-computed from the RCB partition (G15). */
@@ -161,6 +169,11 @@ const char *minife_last_error(const minife_ctx *ctx);
  * ctx becomes unassembled.  Results are bit-identical in both formats (same values, same
  * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
 int minife_set_format(minife_ctx *ctx, int format);
+
+/* VIRTUAL ctxs: select the halo transport (MINIFE_TRANSPORT_*), so the wire protocol of the
+ * multi-GPU modes runs, bit-exactly checkable, on one GPU.  Errors: MINIFE_EINVAL (NULL,
+ * unknown transport), MINIFE_ESTATE (not a VIRTUAL ctx). */
+int minife_set_transport(minife_ctx *ctx, int transport);
 
 /* Select the CG iteration scheme of later solves (MINIFE_SCHEME_*).  Both schemes perform
  * C6's operations on the same values in the same order: results are bit-identical.

@@ -42,6 +42,7 @@ MINIFE_ENOMEM, MINIFE_ENOTSPD, MINIFE_EDIVERGED, MINIFE_ENODEV = 5, 6, 7, 8
 MODE_SINGLE, MODE_VIRTUAL, MODE_MULTI, MODE_RANK = 0, 1, 2, 3
 FMT_CRS, FMT_SEG, FMT_SYM = 0, 1, 2
 SCHEME_3K, SCHEME_FUSED = 0, 1
+TRANSPORT_DIRECT, TRANSPORT_WIRE = 0, 1
 
 
 class minife_part_info(ctypes.Structure):
@@ -100,6 +101,7 @@ SIGNATURES = {
     "minife_last_error": (ctypes.c_char_p, [_P]),
     "minife_set_format": (_I, [_P, _I]),
     "minife_set_scheme": (_I, [_P, _I]),
+    "minife_set_transport": (_I, [_P, _I]),
     "minife_assemble": (_I, [_P]),
     "minife_cg_solve": (_I, [_P, _I, _D, ctypes.POINTER(minife_cg_result)]),
     "minife_cg_profile": (_I, [_P, _I, ctypes.POINTER(minife_kernel_times)]),
@@ -249,6 +251,10 @@ class Minife:
         """FMT_SEG (default, the paper's BCRS on SELL-32) or FMT_CRS (one index per entry)."""
         self._check(minife_set_format(self.h, fmt), "minife_set_format")
         self.info = self.get_info()
+
+    def set_transport(self, transport: int):
+        """VIRTUAL ctxs: TRANSPORT_DIRECT (default) or TRANSPORT_WIRE (the NCCL-mode protocol)."""
+        self._check(minife_set_transport(self.h, transport), "minife_set_transport")
 
     def set_scheme(self, scheme: int):
         """SCHEME_3K (default) or SCHEME_FUSED (one part + FMT_SEG); bit-identical results."""

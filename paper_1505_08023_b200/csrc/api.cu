@@ -128,6 +128,7 @@ struct minife_ctx {
     int mode = MINIFE_MODE_SINGLE;
     int fmt = MINIFE_FMT_SEG;
     int scheme = MINIFE_SCHEME_3K;
+    int transport = MINIFE_TRANSPORT_DIRECT;   // VIRTUAL ctxs only
     int world = 1, rank = 0;
     std::vector<Part> parts;
     cudaStream_t user_stream = nullptr;
@@ -464,6 +465,17 @@ extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
     return MINIFE_OK;
 }
 
+extern "C" int minife_set_transport(minife_ctx *c, int transport) {
+    if (!c || (transport != MINIFE_TRANSPORT_DIRECT && transport != MINIFE_TRANSPORT_WIRE))
+        return MINIFE_EINVAL;
+    if (c->mode != MINIFE_MODE_VIRTUAL) return MINIFE_ESTATE;
+    if (transport != c->transport) {
+        c->transport = transport;
+        drop_graph(c);
+    }
+    return MINIFE_OK;
+}
+
 extern "C" int minife_set_scheme(minife_ctx *c, int scheme) {
     if (!c || (scheme != MINIFE_SCHEME_3K && scheme != MINIFE_SCHEME_FUSED)) return MINIFE_EINVAL;
     if (scheme != c->scheme) {
@@ -613,7 +625,7 @@ extern "C" int minife_assemble(minife_ctx *c) {
 template <class VecOf>
 static int enqueue_halo(minife_ctx *c, VecOf vec) {
     if (c->world == 1) return MINIFE_OK;
-    if (c->mode == MINIFE_MODE_VIRTUAL) {
+    if (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_DIRECT) {
         // device-local transport: read the owner's columns through its send list, write the
         // receiver's halo columns
         cudaStream_t s = c->parts[0].stream;
@@ -630,11 +642,36 @@ static int enqueue_halo(minife_ctx *c, VecOf vec) {
         }
         return MINIFE_OK;
     }
-    // NCCL: pack each part's send lists, grouped send/recv per neighbor, unpack the slots
+    // wire protocol: pack each part's send lists, exchange per neighbor, unpack the slots
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         CUDA_TRY(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
-                                (int64_t)p.plan.send_idx.size(), stream_of(c, p)));
+                                (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
+    }
+    if (c->mode == MINIFE_MODE_VIRTUAL) {
+        // loopback stand-in for ncclSend/ncclRecv: the bytes q sends to p land in p's receive
+        // block for q, exactly where ncclRecv would put them
+        cudaStream_t s = c->parts[0].stream;
+        for (auto &p : c->parts) {
+            for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
+                Part &q = c->parts[p.plan.nbr[k]];
+                auto it = std::lower_bound(q.plan.nbr.begin(), q.plan.nbr.end(), p.plan.rank);
+                const size_t j = (size_t)(it - q.plan.nbr.begin());
+                if (j >= q.plan.nbr.size() || q.plan.nbr[j] != p.plan.rank ||
+                    q.plan.send_cnt[j] != p.plan.recv_cnt[k]) {
+                    set_err(c, "halo plan mismatch between parts %d and %d", p.plan.rank,
+                            q.plan.rank);
+                    return MINIFE_ESTATE;
+                }
+                CUDA_TRY(c, cudaMemcpyAsync(p.d_recvbuf + p.plan.recv_off[k],
+                                            q.d_sendbuf + q.plan.send_off[j],
+                                            sizeof(double) * p.plan.recv_cnt[k],
+                                            cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        for (auto &p : c->parts)
+            CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, s));
+        return MINIFE_OK;
     }
     NCCL_TRY(c, nccl()->GroupStart());
     for (auto &p : c->parts) {

@@ -96,10 +96,13 @@ def test_single_gpu_matrix_spmv_cg(n, fmt):
 @pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
                                  ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4)])
-def test_virtual_ranks_bit_identical(n, p, fmt):
-    """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results."""
+@pytest.mark.parametrize("transport", [0, 1])
+def test_virtual_ranks_bit_identical(n, p, fmt, transport):
+    """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results.  transport 1
+    runs the multi-GPU wire protocol (pack -> per-neighbor receive blocks -> unpack)."""
     s = oracle_system(n)
     with M.Minife(*n, virtual=p, fmt=fmt) as g:
+        g.set_transport(transport)
         g.assemble()
         assert g.get_info().nparts == p
         check_matrix(g, s)
