@@ -50,12 +50,12 @@ extern "C" {
 #define MINIFE_FMT_SEG 1       /* SELL-32, 27 value slots per row + one int32 start column per
                                   x-run ("non-zero segment") + a 27-bit presence mask: the
                                   paper's BCRS (Fig 3.2) on the GPU; 8 B per entry
-                                  + 4 B per segment.  Default.                                */
+                                  + 4 B per segment.  Default of multi-part ctxs.             */
 #define MINIFE_FMT_SYM 2       /* MINIFE_FMT_SEG storing only the upper-triangle value slots
                                   (14 per row incl. the diagonal); a lower entry a_ij is read
                                   from row j's mirror slot (a_ij == a_ji bitwise: the assembled
-                                  system is exactly symmetric, C2/C3).  Single-part ctxs only;
-                                  results identical to the other formats.                     */
+                                  system is exactly symmetric, C2/C3).  Single-part ctxs only
+                                  (their default); results identical to the other formats.    */
 
 /* ---- CG iteration schemes ------------------------------------------------- */
 #define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | x/r update + rr | p update.      */
@@ -165,7 +165,8 @@ const char *minife_last_error(const minife_ctx *ctx);
 
 /* ---- the hot path ---------------------------------------------------------------------- */
 
-/* Select the storage format used by the next minife_assemble (default MINIFE_FMT_SEG).  The
+/* Select the storage format used by the next minife_assemble (default: MINIFE_FMT_SYM for a
+ * single-part ctx, MINIFE_FMT_SEG otherwise; SYM is refused for multi-part ctxs).  The
  * ctx becomes unassembled.  Results are bit-identical in both formats (same values, same
  * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
 int minife_set_format(minife_ctx *ctx, int format);
@@ -262,6 +263,31 @@ int minife_bandwidth_probe(int device, int64_t bytes, int reps, double *read_gbs
 /* L2-resident read rate (GB/s) of the bulk-copy engine measured by the last
  * minife_bandwidth_probe call on this process (48 MB buffer re-read); 0 before any probe. */
 double minife_probe_l2_read_gbs(void);
+
+/* ---- exact dot products (reading C5) --------------------------------------- */
+
+#define MINIFE_ACC_WORDS 72    /* device superaccumulator: words 0..67 = signed int64 digits,
+                                  word i weighs 2^(32 i - 1074); word 68 counts non-finite
+                                  terms; 69..71 padding (576 B, the all-reduced payload)     */
+
+/* Exactly rounded dot product of host vectors u, v (n doubles each) on CUDA device `device`:
+ * RN(sum^exact fl(u_i v_i)), ties to even, exact zero -> +0.0, any non-finite product -> NaN.
+ * This is the operation behind every CG dot of the hot path (Fig 2.2 "dot"), computed
+ * by the same device code: per-thread TwoSum expansions, a CTA fixed-point superaccumulator,
+ * global int64 words, warp-parallel carry normalisation and rounding.  The result does not
+ * depend on the order of the terms.  Exact while every per-thread partial sum stays below
+ * 2^1023 in magnitude (the expansions use binary64 TwoSum; the CG dots are orders of
+ * magnitude below).  Allocates and frees its own device buffers; synchronous.
+ * Errors: MINIFE_EINVAL (n < 0, n >= 2^29, out NULL, u/v NULL with n > 0), MINIFE_ENODEV,
+ * MINIFE_ENOMEM, MINIFE_ECUDA. */
+int minife_dot(int device, int64_t n, const double *u, const double *v, double *out);
+
+/* The rounding step of minife_dot alone, on device `device`: *out = RN(sum_{i<68} words[i]
+ * 2^(32 i - 1074)) for any MINIFE_ACC_WORDS signed int64 words (host array; word 68 != 0 ->
+ * NaN; words 69..71 ignored); overflow rounds to +-inf.  Exposed so that tests can pin the
+ * device's carry normalisation and round-to-nearest-even against exact integer arithmetic.
+ * Errors: MINIFE_EINVAL (NULL), MINIFE_ENODEV, MINIFE_ENOMEM, MINIFE_ECUDA. */
+int minife_exact_round(int device, const int64_t *words, double *out);
 
 /* Library version string. */
 const char *minife_version(void);

@@ -119,6 +119,8 @@ SIGNATURES = {
     "minife_plan_lists": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "minife_bandwidth_probe": (_I, [_I, _I64, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_probe_l2_read_gbs": (_D, []),
+    "minife_dot": (_I, [_I, _I64, _P, _P, ctypes.POINTER(_D)]),
+    "minife_exact_round": (_I, [_I, _P, ctypes.POINTER(_D)]),
     "minife_version": (ctypes.c_char_p, []),
 }
 
@@ -176,6 +178,34 @@ def bandwidth_probe(device: int = 0, nbytes: int = 8 << 30, reps: int = 5):
     return r.value, c.value
 
 
+ACC_WORDS = 72
+
+
+def dot(u: np.ndarray, v: np.ndarray, device: int = 0) -> float:
+    """Exactly rounded dot product on the device (C5; the CG dots' own code path)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if u.shape != v.shape or u.ndim != 1:
+        raise ValueError("u and v must be 1-D of equal length")
+    out = ctypes.c_double(0.0)
+    st = minife_dot(device, u.size, _ptr(u), _ptr(v), ctypes.byref(out))
+    if st != MINIFE_OK:
+        raise MinifeError(st, "minife_dot")
+    return out.value
+
+
+def exact_round(words, device: int = 0) -> float:
+    """RN(sum_i words[i] 2^(32 i - 1074)) by the device's accumulator rounding step."""
+    w = np.zeros(ACC_WORDS, dtype=np.int64)
+    src = np.asarray(words, dtype=np.int64)
+    w[:src.size] = src
+    out = ctypes.c_double(0.0)
+    st = minife_exact_round(device, _ptr(w), ctypes.byref(out))
+    if st != MINIFE_OK:
+        raise MinifeError(st, "minife_exact_round")
+    return out.value
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     st = minife_nccl_unique_id(buf)
@@ -212,7 +242,10 @@ class Minife:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:       # interpreter shutdown: module globals already cleared
+            pass
 
     def __enter__(self):
         return self

@@ -12,7 +12,7 @@
 //      words, word i weighting 2^(32 i - 1074); a double adds < 2^33 to each of <= 3 words;
 //   3. per rank / globally: the CTA words are added to a global copy with int64 atomicAdd;
 //      across ranks an int64-SUM all-reduce (associative, so deterministic).
-// A consumer kernel normalises the carries and rounds once (acc_finalize).
+// A consumer kernel normalises the carries and rounds once (acc_finalize_warp).
 // Capacity: < 2^29 additions per accumulator word (any n < 5e8 terms) keeps every word and
 // carry inside int64.  Word ACC_FLAG counts non-finite inputs (then the result is NaN).
 #pragma once
@@ -150,75 +150,122 @@ __device__ __forceinline__ void acc_load_shared(unsigned long long *s,
     for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = __ldcg(g + i);
 }
 
-// One window of the digit scan: the top nonzero digit seen so far, the two digits below it,
-// and whether anything below those is nonzero.
-struct DigitWindow {
-    int T = -1;
-    uint32_t dT = 0, d1 = 0, d2 = 0;
-    bool sticky = false;
-    uint32_t prev1 = 0, prev2 = 0;    // digits i-1, i-2 of the scan
-    bool below = false;               // OR of digits <= i-3
-    __device__ __forceinline__ void push(int i, uint32_t d) {
-        if (d != 0) {
-            T = i;
-            dT = d;
-            d1 = prev1;
-            d2 = prev2;
-            sticky = below;
-        }
-        below |= prev2 != 0;
-        prev2 = prev1;
-        prev1 = d;
-    }
-};
-
-// Normalise carries and round to nearest-even (one thread; s = shared copy of the words).
-// Exact zero -> +0.0.  One pass from the least significant digit with constant state:
-// the sign is only known at the end, so the window is tracked for both the value and its
-// two's-complement negation (digit e_i = -d_i while every lower digit is 0, else ~d_i).
-static __device__ __noinline__ double acc_finalize(const unsigned long long *s) {
-    if (s[ACC_FLAG] != 0ull) return __longlong_as_double(0x7ff8000000000000ll);
-    long long carry = 0;
-    bool all_zero = true;
-    DigitWindow pos, neg;
-#pragma unroll 4
-    for (int i = 0; i < ACC_DIGITS; ++i) {
-        const long long v = (long long)s[i] + carry;
-        const uint32_t d = (uint32_t)((unsigned long long)v & 0xffffffffull);
-        carry = (v - (long long)d) >> 32;      // exact floor division by 2^32
-        pos.push(i, d);
-        neg.push(i, all_zero ? 0u - d : ~d);
-        all_zero = all_zero && d == 0;
-    }
-    const bool negative = carry < 0;           // value = sum d_i 2^(32i) - [neg] 2^(32*68)
-    const DigitWindow &w = negative ? neg : pos;
-    const int T = w.T;
-    if (T < 0) return 0.0;
-    const uint32_t dT = w.dT, d1 = w.d1, d2 = w.d2;
+// Round a 96-bit window (digits T, T-1, T-2 of the magnitude, 32 bits each) plus a sticky
+// bit to nearest-even; T = index of the top nonzero digit (units of 2^(32 T - 1074)).
+__device__ __forceinline__ double round_window(int T, uint32_t dT, uint32_t d1, uint32_t d2,
+                                               bool below) {
     const int t = 32 * T + 31 - __clz(dT);     // top bit, in units of 2^-1074
-    double mag;
     if (t <= 52) {                             // T <= 1: the value is digits T..0, exact
         const unsigned long long v =
             T == 1 ? ((unsigned long long)dT << 32) | d1 : (unsigned long long)dT;
-        mag = scalbn((double)v, -1074);        // < 2^53 ulps of 2^-1074: exact
-    } else {
-        // 96-bit window of digits T, T-1, T-2 (missing digits read as 0)
-        const unsigned __int128 W = ((unsigned __int128)dT << 64) |
-                                    ((unsigned __int128)d1 << 32) | (unsigned __int128)d2;
-        const int sh = t - 32 * (T - 2);        // top bit position inside W, in [64, 95]
-        unsigned long long M = (unsigned long long)(W >> (sh - 52));   // 53 bits
-        const int guard = (int)((W >> (sh - 53)) & 1u);
-        bool sticky = w.sticky || (W & ((((unsigned __int128)1) << (sh - 53)) - 1)) != 0;
-        int top = t;
-        if (guard && (sticky || (M & 1ull))) {
-            ++M;
-            if (M == (1ull << 53)) {
-                M >>= 1;
-                ++top;
-            }
-        }
-        mag = scalbn((double)M, top - 52 - 1074);   // inf iff round-to-nearest overflows
+        return scalbn((double)v, -1074);       // < 2^53 ulps of 2^-1074: exact
     }
+    const unsigned __int128 W = ((unsigned __int128)dT << 64) |
+                                ((unsigned __int128)d1 << 32) | (unsigned __int128)d2;
+    const int sh = t - 32 * (T - 2);           // top bit position inside W, in [64, 95]
+    unsigned long long M = (unsigned long long)(W >> (sh - 52));   // 53 bits
+    const int guard = (int)((W >> (sh - 53)) & 1u);
+    const bool sticky = below || (W & ((((unsigned __int128)1) << (sh - 53)) - 1)) != 0;
+    int top = t;
+    if (guard && (sticky || (M & 1ull))) {
+        ++M;
+        if (M == (1ull << 53)) {
+            M >>= 1;
+            ++top;
+        }
+    }
+    return scalbn((double)M, top - 52 - 1074);   // inf iff round-to-nearest overflows
+}
+
+// Carry maps of the warp-parallel normalisation: a digit with pre-carry value u (in
+// [-2^31, 2^32 + 2^31)) maps an incoming carry c in {-1, 0, 1} to floor((u + c) / 2^32),
+// again in {-1, 0, 1}.  Encoded as three 2-bit fields (field c+1 holds result+1).
+__device__ __forceinline__ unsigned carry_map(long long u) {
+    unsigned m = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m |= (unsigned)(((u + (c - 1)) >> 32) + 1) << (2 * c);
+    return m;
+}
+__device__ __forceinline__ unsigned map_at(unsigned m, unsigned c) { return (m >> (2 * c)) & 3u; }
+__device__ __forceinline__ unsigned map_after(unsigned g, unsigned f) {   // g o f
+    return map_at(g, map_at(f, 0)) | (map_at(g, map_at(f, 1)) << 2) |
+           (map_at(g, map_at(f, 2)) << 4);
+}
+
+// Normalise carries and round to nearest-even, cooperatively: the 32 lanes of one warp call
+// it converged with the same s (the accumulator words); every lane returns RN(value).  Exact
+// zero -> +0.0, a nonzero ACC_FLAG -> NaN.
+//   value = sum_i s_i 2^(32 i - 1074), s_i signed int64, i < ACC_DIGITS.
+// Lane l owns digits 3l..3l+2 (96 digits; those >= ACC_DIGITS are 0).  Splitting every word
+// into lo (32 bits, unsigned) + hi (signed) leaves u_i = lo_i + hi_(i-1), after which each
+// carry is -1, 0 or +1; the carries are resolved by a warp scan of carry maps (composition is
+// associative), giving the 96-digit two's-complement value.  Sign = the carry out of the top
+// digit; the magnitude's top digit, its two lower neighbours and the sticky OR of the rest
+// are found with warp votes and rounded once (round_window).  O(log 32) dependent steps in
+// place of a 68-step carry chain on one thread.
+__device__ __forceinline__ double acc_finalize_warp(const unsigned long long *s) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = (int)(threadIdx.x & 31u);
+    if (s[ACC_FLAG] != 0ull) return __longlong_as_double(0x7ff8000000000000ll);
+    long long lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int i = 3 * lane + k;
+        const long long w = i < ACC_DIGITS ? (long long)s[i] : 0ll;
+        lo[k] = w & 0xffffffffll;
+        hi[k] = w >> 32;                                   // arithmetic: floor(w / 2^32)
+    }
+    const long long hprev = __shfl_up_sync(FULL, hi[2], 1);
+    const long long u[3] = {lo[0] + (lane ? hprev : 0ll), lo[1] + hi[0], lo[2] + hi[1]};
+    unsigned G = map_after(carry_map(u[2]), map_after(carry_map(u[1]), carry_map(u[0])));
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {               // inclusive scan: G_l o ... o G_0
+        const unsigned prev = __shfl_up_sync(FULL, G, off);
+        if (lane >= off) G = map_after(G, prev);
+    }
+    const unsigned Gex = __shfl_up_sync(FULL, G, 1);
+    long long c = lane ? (long long)map_at(Gex, 1) - 1 : 0ll;   // carry into digit 3l
+    const bool negative = (int)map_at(__shfl_sync(FULL, G, 31), 1) - 1 < 0;
+    uint32_t d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const long long v = u[k] + c;
+        d[k] = (uint32_t)(v & 0xffffffffll);
+        c = v >> 32;
+    }
+    if (negative) {                                        // magnitude = two's complement
+        int low = 96;
+#pragma unroll
+        for (int k = 2; k >= 0; --k)
+            if (d[k]) low = 3 * lane + k;
+        low = (int)__reduce_min_sync(FULL, (unsigned)low);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int i = 3 * lane + k;
+            d[k] = i < low ? 0u : (i == low ? 0u - d[k] : ~d[k]);
+        }
+    }
+    int top = -1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (d[k]) top = 3 * lane + k;
+    const int T = (int)__reduce_max_sync(FULL, (unsigned)(top + 1)) - 1;
+    if (T < 0) return 0.0;
+    uint32_t dw[3];                                        // digits T, T-1, T-2 (0 if < 0)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int idx = T - q;
+        const int src = idx >= 0 ? idx / 3 : 0;
+        const int k = idx - 3 * lane;
+        const uint32_t mine = (idx >= 0 && lane == src) ? (k == 0 ? d[0] : (k == 1 ? d[1] : d[2]))
+                                                        : 0u;
+        dw[q] = __shfl_sync(FULL, mine, src);
+    }
+    bool below = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) below |= (3 * lane + k < T - 2) && d[k] != 0u;
+    below = __any_sync(FULL, below);
+    const double mag = round_window(T, dw[0], dw[1], dw[2], below);
     return negative ? -mag : mag;
 }
 

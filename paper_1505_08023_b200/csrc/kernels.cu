@@ -431,8 +431,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-__device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k, double *hist,
-                                           double *rr, CgState *st, double &beta);
+__device__ __forceinline__ int rr_decision(double rr_new, int k, double *hist, double *rr,
+                                           CgState *st, double &beta);
 
 // FUSED (SEG, DOT, one part only): fused CG iteration k = a.fused_k, DESIGN.md §5.  The
 // prologue takes K7's decisions for iteration k-1 (finalise rr_{k-1}, hist, stop tests,
@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
         acc_load_shared(s_in, a.acc_rr_in);
         __syncthreads();
     }
+    const double fin = (FUSED && fk >= 2 && threadIdx.x < 32) ? acc_finalize_warp(s_in) : 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
         if (FUSED) {
             double beta = 0.0, alpha_prev = 0.0;
             if (fk >= 2) {
-                s_stop = rr_decision(s_in, fk - 1, a.hist, a.rr, a.stw, beta);
+                s_stop = rr_decision(fin, fk - 1, a.hist, a.rr, a.stw, beta);
                 alpha_prev = a.stw->alpha;                    // alpha_{k-1} (K6 of k-1)
                 if (!s_stop && blockIdx.x == 0) a.stw->x_done = fk - 1;
             }
@@ -617,17 +618,17 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
 // warps per SM keep the mirrored and x reads in flight.
 // ----------------------------------------------------------------------------------------
 
-constexpr int SY_TILE = 16;                                    // slices per tile = consumers
-constexpr int SY_THREADS = 32 * (SY_TILE + 1);
-constexpr int SY_VAL_B = SY_TILE * 14 * 32 * 8;                // 57344
-constexpr int SY_SEG_B = SY_TILE * 9 * 32 * 4;                 // 18432
-constexpr int SY_MSK_B = SY_TILE * 32 * 4;                     // 2048
-constexpr int SY_STAGE_B = SY_VAL_B + SY_SEG_B + SY_MSK_B;     // 77824
-constexpr int SY_STAGES = 2;
-constexpr int SY_SMEM = SY_STAGES * SY_STAGE_B;
+template <int NW, int NST> struct SyCfg {                     // NW slices per tile = consumers
+    static constexpr int TILE = NW, THREADS = 32 * (NW + 1), STAGES = NST;
+    static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
+    static constexpr int STAGE_B = VAL_B + SEG_B + MSK_B, SMEM = NST * STAGE_B;
+};
 
-template <bool DOT>
-__global__ void __launch_bounds__(SY_THREADS, 1) k_spmv_sym(SpmvArgs a) {
+template <bool DOT, int NW, int NST>
+__global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArgs a) {
+    constexpr int SY_TILE = NW, SY_STAGES = NST;
+    constexpr int SY_VAL_B = SyCfg<NW, NST>::VAL_B, SY_SEG_B = SyCfg<NW, NST>::SEG_B;
+    constexpr int SY_STAGE_B = SyCfg<NW, NST>::STAGE_B;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[SY_STAGES], empty_bar[SY_STAGES];
     __shared__ unsigned long long sacc[ACC_WORDS];
@@ -691,15 +692,15 @@ __global__ void __launch_bounds__(SY_THREADS, 1) k_spmv_sym(SpmvArgs a) {
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
                 double lv[13], xv[27];
 #pragma unroll
-                for (int t = 0; t < 27; ++t) {
+                for (int t = 0; t < 13; ++t) {                 // mirrored lower values
                     const bool on = (msk >> t) & 1u;
                     const int c = sg[t / 3] + (t % 3);
-                    xv[t] = on ? __ldg(a.x + c) : 0.0;
-                    if (t < 13)
-                        lv[t] = on ? __ldg(m.val + ((int64_t)(c >> 5) * 14 + (13 - t)) * 32 +
-                                           (c & 31))
-                                   : 0.0;
+                    lv[t] = on ? __ldg(m.val + ((int64_t)(c >> 5) * 14 + (13 - t)) * 32 + (c & 31))
+                               : 0.0;
                 }
+#pragma unroll
+                for (int t = 0; t < 27; ++t)
+                    xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
                 double sum = 0.0;
 #pragma unroll
                 for (int t = 0; t < 13; ++t)
@@ -751,8 +752,9 @@ __global__ void k_init_finalize(UpdArgs a, double tol) {
     __shared__ unsigned long long s_in[ACC_WORDS];
     acc_load_shared(s_in, a.acc_out);
     __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
-        const double rr0 = acc_finalize(s_in);
+        const double rr0 = fin;
         const double h0 = __dsqrt_rn(rr0);
         a.rr[0] = rr0;
         a.hist[0] = h0;
@@ -787,9 +789,7 @@ __device__ __forceinline__ void xr_step(double &x, double &r, double p, double a
 // Decisions of K6 (a3, C6): finalise pAp, stop tests, alpha.  Thread 0 of each CTA (s_in =
 // shared copy of the all-reduced accumulator); every CTA takes the same decision, CTA 0
 // records it.  Returns stop.
-__device__ __forceinline__ int xr_prologue(const UpdArgs &a, const unsigned long long *s_in,
-                                           int k, double &alpha) {
-    const double pAp = acc_finalize(s_in);
+__device__ __forceinline__ int xr_prologue(const UpdArgs &a, double pAp, int k, double &alpha) {
     const double rr = a.rr[k - 1];
     int stop = 0, status = 0, conv = 0;
     if (!isfinite(pAp)) {
@@ -817,9 +817,8 @@ __device__ __forceinline__ int xr_prologue(const UpdArgs &a, const unsigned long
 }
 
 // Decisions after rr_k (a5, C6): finalise rr_k, hist[k], stop tests, beta_k.
-__device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k, double *hist,
-                                           double *rr, CgState *st, double &beta) {
-    const double rr_new = acc_finalize(s_in);
+__device__ __forceinline__ int rr_decision(double rr_new, int k, double *hist, double *rr,
+                                           CgState *st, double &beta) {
     const double h = __dsqrt_rn(rr_new);
     const double rr_old = rr[k - 1];
     int stop = 0, status = 0, conv = 0;
@@ -846,9 +845,8 @@ __device__ __forceinline__ int rr_decision(const unsigned long long *s_in, int k
 }
 
 // Decisions of K7 (a5, C6).
-__device__ __forceinline__ int p_prologue(const UpdArgs &a, const unsigned long long *s_in,
-                                          int k, double &beta) {
-    return rr_decision(s_in, k, a.hist, a.rr, a.st, beta);
+__device__ __forceinline__ int p_prologue(const UpdArgs &a, double rr_new, int k, double &beta) {
+    return rr_decision(rr_new, k, a.hist, a.rr, a.st, beta);
 }
 
 template <bool IDENT>
@@ -860,9 +858,10 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     acc_zero_shared(sacc);
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
         double alpha;
-        s_stop = xr_prologue(a, s_in, k, alpha);
+        s_stop = xr_prologue(a, fin, k, alpha);
         s_alpha = alpha;
     }
     __syncthreads();
@@ -933,9 +932,10 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     if (a.st->done) return;
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
         double beta;
-        s_stop = p_prologue(a, s_in, k, beta);
+        s_stop = p_prologue(a, fin, k, beta);
         s_beta = beta;
     }
     __syncthreads();
@@ -993,9 +993,10 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
     acc_zero_shared(sacc);
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
         double alpha;
-        s_stop = xr_prologue(a, s_in, k, alpha);
+        s_stop = xr_prologue(a, fin, k, alpha);
         s_alpha = alpha;
     }
     __syncthreads();
@@ -1057,9 +1058,10 @@ __global__ void __launch_bounds__(UPD_THREADS) k_cg_finish(UpdArgs a, int K, con
     if (!done && blockIdx.x == 0) {
         acc_load_shared(s_in, a.acc_in);
         __syncthreads();
+        const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
         if (threadIdx.x == 0) {
             double beta;
-            rr_decision(s_in, K, a.hist, a.rr, a.st, beta);
+            rr_decision(fin, K, a.hist, a.rr, a.st, beta);
         }
     }
     if (threadIdx.x == 0) {
@@ -1107,6 +1109,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
         for (int s = 0; s < UT_STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -1114,7 +1117,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         double coef;
-        s_stop = XR ? xr_prologue(a, s_in, k, coef) : p_prologue(a, s_in, k, coef);
+        s_stop = XR ? xr_prologue(a, fin, k, coef) : p_prologue(a, fin, k, coef);
         s_coef = coef;
     }
     if (XR) acc_zero_shared(sacc);
@@ -1368,6 +1371,33 @@ __global__ void k_vsum(AccPtrs ptrs, int nparts) {
     }
 }
 
+// C5 as a standalone operation: acc += sum^exact fl(u_i v_i) (the same three levels as the
+// CG kernels' epilogues), then k_acc_round.
+__global__ void __launch_bounds__(UPD_THREADS) k_dot(const double *__restrict__ u,
+                                                     const double *__restrict__ v, int64_t n,
+                                                     unsigned long long *acc) {
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    acc_zero_shared(sacc);
+    __syncthreads();
+    Expansion ex;
+    ex.init();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        ex.add(__dmul_rn(u[i], v[i]), sacc);
+    ex.warp_flush(sacc);
+    __syncthreads();
+    acc_merge_to_global(sacc, acc);
+}
+
+// *out = RN(value of the accumulator), one warp.
+__global__ void k_acc_round(const unsigned long long *acc, double *out) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    acc_load_shared(s_in, acc);
+    __syncwarp();
+    const double v = acc_finalize_warp(s_in);
+    if (threadIdx.x == 0) *out = v;
+}
+
 __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t *out_col,
                                double *out_val, int32_t *out_len) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1463,6 +1493,21 @@ static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// SYM tile shape (B200, 300^3: 16 consumer warps x 2 stages 0.90 ms/launch, 12 x 3 0.95 ms,
+// 8 x 4 1.31 ms -- the kernel is bound by the latency of its L2 gathers, so warps beat stages)
+template <bool DOT>
+static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
+    using C = SyCfg<16, 2>;
+    static unsigned long long attr_set = 0;
+    cudaError_t e = ensure_smem_attr(k_spmv_sym<DOT, 16, 2>, C::SMEM, attr_set);
+    if (e != cudaSuccess) return e;
+    query_occupancy();
+    const int64_t ntiles = (a.m.nslices + C::TILE - 1) / C::TILE;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
+    k_spmv_sym<DOT, 16, 2><<<g, C::THREADS, C::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp_next_zero,
                             int grid, cudaStream_t s) {
     query_occupancy();
@@ -1500,16 +1545,7 @@ cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t
     }
     if (a.m.fmt == FMT_SYM) {
         if (!a.g.ident) return cudaErrorInvalidValue;        // one part only
-        static unsigned long long m0 = 0, m1 = 0;
-        cudaError_t e = with_dot ? ensure_smem_attr(k_spmv_sym<true>, SY_SMEM, m1)
-                                 : ensure_smem_attr(k_spmv_sym<false>, SY_SMEM, m0);
-        if (e != cudaSuccess) return e;
-        query_occupancy();
-        const int64_t ntiles = (a.m.nslices + SY_TILE - 1) / SY_TILE;
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
-        if (with_dot) k_spmv_sym<true><<<g, SY_THREADS, SY_SMEM, s>>>(a);
-        else k_spmv_sym<false><<<g, SY_THREADS, SY_SMEM, s>>>(a);
-        return cudaGetLastError();
+        return with_dot ? launch_sym<true>(a, s) : launch_sym<false>(a, s);
     }
     if (spmv_impl(a.m.fmt) == 1) {
         if (a.m.fmt == FMT_SEG)
@@ -1616,6 +1652,19 @@ cudaError_t launch_vsum(unsigned long long *const *accs, int nparts, cudaStream_
     AccPtrs p{};
     for (int q = 0; q < nparts && q < 64; ++q) p.p[q] = accs[q];
     k_vsum<<<1, 128, 0, s>>>(p, nparts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dot(const double *u, const double *v, int64_t n, unsigned long long *acc,
+                       cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int g = stream_grid(n);
+    k_dot<<<g, UPD_THREADS, 0, s>>>(u, v, n, acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStream_t s) {
+    k_acc_round<<<1, 32, 0, s>>>(acc, out);
     return cudaGetLastError();
 }
 

@@ -120,6 +120,12 @@ cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
                         const int32_t *didx, int64_t n, cudaStream_t s);
 cudaError_t launch_vsum(unsigned long long *const *accs, int nparts, cudaStream_t s);
 
+// C5 standalone: acc (ACC_WORDS words, zeroed by the caller) += exact sum of fl(u_i v_i);
+// *out = RN(acc) (warp-parallel carry normalisation + rounding, exact.cuh).
+cudaError_t launch_dot(const double *u, const double *v, int64_t n, unsigned long long *acc,
+                       cudaStream_t s);
+cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStream_t s);
+
 // Parity helper: rows[] (local) -> up to 27 (extended column, value) pairs each
 cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,

@@ -195,7 +195,7 @@ def test_profile_mode_matches_graph_mode():
 def test_fused_scheme_bit_identical(n):
     """SURVEY §8(f) NEXT #2: the fused two-kernel iteration performs C6 exactly."""
     s = oracle_system(n)
-    with M.Minife(*n) as g:
+    with M.Minife(*n, fmt=M.FMT_SEG) as g:      # the fused scheme runs on FMT_SEG
         g.set_scheme(M.SCHEME_FUSED)
         g.assemble()
         check_cg(g, n, 200, 0.0)
@@ -214,7 +214,8 @@ def test_format_switch_keeps_results():
     n = (14, 13, 12)
     s = oracle_system(n)
     with M.Minife(*n) as g:
-        assert g.get_info().format == M.FMT_SEG
+        assert g.get_info().format == M.FMT_SYM     # single-part default
+        g.set_format(M.FMT_SEG)
         g.assemble()
         seg_info = g.get_info()
         # nns = number of maximal consecutive-column runs of the oracle's CRS rows
@@ -231,6 +232,14 @@ def test_format_switch_keeps_results():
         g.assemble()
         check_matrix(g, s)
         check_cg(g, n, 60, 0.0)
+        g.set_format(M.FMT_SYM)
+        g.assemble()
+        check_matrix(g, s)
+        check_cg(g, n, 60, 0.0)
+    with M.Minife(*n, virtual=2) as g:
+        assert g.get_info().format == M.FMT_SEG     # multi-part default
+        with pytest.raises(M.MinifeError):
+            g.set_format(M.FMT_SYM)
 
 
 @pytest.mark.slow
