@@ -88,6 +88,8 @@ typedef struct minife_part_info {
     int64_t slices;           /* SELL-32 slices = ceil(rows/32)                           */
     int64_t sell_entries;     /* sum over slices of 32*width (incl. padding)              */
     int64_t send_total;       /* values this part sends per halo exchange                 */
+    int64_t interior_slices;  /* SELL-32 slices none of whose rows reads a halo column:
+                                 their SpMV runs while the halo is in flight  */
 } minife_part_info;
 
 typedef struct minife_info {

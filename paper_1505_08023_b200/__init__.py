@@ -51,7 +51,8 @@ class minife_part_info(ctypes.Structure):
                 ("n_neighbors", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("rows", ctypes.c_int64), ("externals", ctypes.c_int64),
                 ("nnz", ctypes.c_int64), ("slices", ctypes.c_int64),
-                ("sell_entries", ctypes.c_int64), ("send_total", ctypes.c_int64)]
+                ("sell_entries", ctypes.c_int64), ("send_total", ctypes.c_int64),
+                ("interior_slices", ctypes.c_int64)]
 
 
 class minife_info(ctypes.Structure):

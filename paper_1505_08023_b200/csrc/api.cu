@@ -99,8 +99,13 @@ struct Part {
     // extended column of each halo slot; wire buffers
     int32_t *d_send_col = nullptr, *d_recv_pos = nullptr;
     double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+    // SEG slice storage order (multi-part): interior slices [0, n_int) first, DESIGN.md §7
+    int32_t *d_slice_row = nullptr, *d_slice_pos = nullptr;
+    int64_t n_int = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t cstream = nullptr;               // halo transport, overlapped with the SpMV
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int grid_spmv = 1, grid_upd = 1;
     size_t bytes = 0, matrix_bytes = 0;
     unsigned long long *acc_pAp(int par = 0) const { return d_acc + (2 * (par & 1)) * ACC_WORDS; }
@@ -231,10 +236,13 @@ static void free_part(Part &p) {
     void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width,   p.d_b,        p.d_x,
                     p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
-                    p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf};
+                    p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
+    if (p.ev_fork) cudaEventDestroy(p.ev_fork);
+    if (p.ev_join) cudaEventDestroy(p.ev_join);
+    if (p.cstream) cudaStreamDestroy(p.cstream);
     if (p.stream) cudaStreamDestroy(p.stream);
 }
 
@@ -310,6 +318,20 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
         CUDA_TRY(c, cudaMemcpy(p.d_recv_pos, recv_pos.data(), 4 * recv_pos.size(),
                                cudaMemcpyHostToDevice));
     p.grid_upd = stream_grid(p.rows);
+    // halo/interior overlap: interior-first slice storage order + a transport stream
+    p.n_int = p.nslices;
+    if (plan.n_ext > 0) {
+        std::vector<int32_t> order, pos(p.nslices);
+        p.n_int = plan.slice_order(order);
+        for (int64_t q = 0; q < p.nslices; ++q) pos[order[q]] = (int32_t)q;
+        TRY(dalloc(c, p, &p.d_slice_row, p.nslices));
+        TRY(dalloc(c, p, &p.d_slice_pos, p.nslices));
+        CUDA_TRY(c, cudaMemcpy(p.d_slice_row, order.data(), 4 * p.nslices, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaMemcpy(p.d_slice_pos, pos.data(), 4 * p.nslices, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
+    }
     return MINIFE_OK;
 }
 
@@ -599,6 +621,10 @@ static Matrix matrix_of(const minife_ctx *c, const Part &p) {
     m.col = p.d_col;
     m.seg = p.d_seg;
     m.mask = p.d_mask;
+    if (c->fmt == MINIFE_FMT_SEG) {          // interior-first slice order (null: identity)
+        m.slice_row = p.d_slice_row;
+        m.slice_pos = p.d_slice_pos;
+    }
     return m;
 }
 
@@ -652,6 +678,7 @@ extern "C" int minife_assemble(minife_ctx *c) {
         a.mask = p.d_mask;
         a.val = p.d_val;
         a.b = p.d_b;
+        a.slice_pos = c->fmt == MINIFE_FMT_SEG ? p.d_slice_pos : nullptr;
         CUDA_TRY(c, launch_assemble(a, s));
         p.grid_spmv = spmv_grid(p.nslices, c->fmt);
     }
@@ -669,13 +696,19 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // ----------------------------------------------------------------------------------------
 
 // Fill the halo (shell) columns of vec(part) from the owners' owned values.
+// comm = true: on the transport streams (cstream) instead of the compute streams.
 template <class VecOf>
-static int enqueue_halo(minife_ctx *c, VecOf vec) {
+static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false) {
     if (c->world == 1) return MINIFE_OK;
+    // stream of part p's work: VIRTUAL ctxs use part 0's queue for every part
+    auto sp = [&](Part &p) -> cudaStream_t {
+        Part &q = c->mode == MINIFE_MODE_VIRTUAL ? c->parts[0] : p;
+        return comm ? q.cstream : (c->mode == MINIFE_MODE_VIRTUAL ? q.stream : stream_of(c, q));
+    };
     if (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_DIRECT) {
         // device-local transport: read the owner's columns through its send list, write the
         // receiver's halo columns
-        cudaStream_t s = c->parts[0].stream;
+        cudaStream_t s = sp(c->parts[0]);
         for (auto &dst : c->parts) {
             for (size_t k = 0; k < dst.plan.nbr.size(); ++k) {
                 Part &src = c->parts[dst.plan.nbr[k]];
@@ -693,12 +726,12 @@ static int enqueue_halo(minife_ctx *c, VecOf vec) {
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         CUDA_TRY(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
-                                (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
+                                (int64_t)p.plan.send_idx.size(), sp(p)));
     }
     if (c->mode == MINIFE_MODE_VIRTUAL) {
         // loopback stand-in for ncclSend/ncclRecv: the bytes q sends to p land in p's receive
         // block for q, exactly where ncclRecv would put them
-        cudaStream_t s = c->parts[0].stream;
+        cudaStream_t s = sp(c->parts[0]);
         for (auto &p : c->parts) {
             for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
                 Part &q = c->parts[p.plan.nbr[k]];
@@ -722,7 +755,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec) {
     }
     NCCL_TRY(c, nccl()->GroupStart());
     for (auto &p : c->parts) {
-        cudaStream_t s = stream_of(c, p);
+        cudaStream_t s = sp(p);
         for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
             NCCL_TRY(c, nccl()->Send(p.d_sendbuf + p.plan.send_off[k],
                                      (size_t)p.plan.send_cnt[k], ncclFloat64, p.plan.nbr[k],
@@ -735,8 +768,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec) {
     NCCL_TRY(c, nccl()->GroupEnd());
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext,
-                                stream_of(c, p)));
+        CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, sp(p)));
     }
     return MINIFE_OK;
 }
@@ -796,7 +828,15 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     a.acc = dot ? p.acc_pAp() : nullptr;
     a.acc_zero = dot ? p.acc_rr() : nullptr;
     a.st = dot ? p.d_st : nullptr;
+    a.s_begin = 0;
+    a.s_end = p.nslices;
     return a;
+}
+
+// The halo of p is moved on the parts' transport streams while the interior slices' SpMV
+// runs (SEG, more than one part); the boundary slices follow once it has landed.
+static bool overlap_mode(const minife_ctx *c) {
+    return c->fmt == MINIFE_FMT_SEG && c->world > 1 && c->parts[0].cstream;
 }
 
 struct PhaseTimer {
@@ -832,13 +872,52 @@ static int enqueue_init(minife_ctx *c, double tol) {
     return MINIFE_OK;
 }
 
-static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
-    TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
-    if (t) t->mark(3);
+// a1 + a2 with the halo in flight during the interior SpMV: fork the transport streams off
+// the compute streams (p is final after K7), interior slices, join, boundary slices.  The
+// pAp accumulator is order-independent (C5), so the split changes no bit of the result.
+static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
+    const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
+    for (auto &p : c->parts) {
+        if (virt && &p != &c->parts[0]) break;
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaEventRecord(p.ev_fork, launch_stream(c, p)));
+        CUDA_TRY(c, cudaStreamWaitEvent(p.cstream, p.ev_fork, 0));
+    }
+    TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }, true));
+    for (auto &p : c->parts) {
+        if (virt && &p != &c->parts[0]) break;
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaEventRecord(p.ev_join, p.cstream));
+    }
+    for (auto &p : c->parts) {                     // interior slices: no halo column read
+        DevGuard g(p.dev);
+        SpmvArgs a = spmv_args(c, p, p.d_p, p.d_Ap, true);
+        a.s_end = p.n_int;
+        CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
+    }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
-                                launch_stream(c, p)));
+        Part &q = virt ? c->parts[0] : p;
+        if (!virt || &p == &c->parts[0])
+            CUDA_TRY(c, cudaStreamWaitEvent(launch_stream(c, p), q.ev_join, 0));
+        SpmvArgs a = spmv_args(c, p, p.d_p, p.d_Ap, true);
+        a.s_begin = p.n_int;
+        CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
+    }
+    return MINIFE_OK;
+}
+
+static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
+    if (overlap_mode(c) && !t) {
+        TRY(enqueue_halo_spmv_overlapped(c));
+    } else {
+        TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+        if (t) t->mark(3);
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+                                    launch_stream(c, p)));
+        }
     }
     if (t) t->mark(0);
     TRY(enqueue_allreduce(c, 0));
@@ -1188,6 +1267,8 @@ static void fill_part_info(const Plan &pl, int dev, int64_t entries, minife_part
     o->slices = (pl.n_owned + 31) / 32;
     o->sell_entries = entries;
     o->send_total = (int64_t)pl.send_idx.size();
+    std::vector<int32_t> order;
+    o->interior_slices = pl.slice_order(order);
 }
 
 extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {

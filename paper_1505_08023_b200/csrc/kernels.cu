@@ -149,7 +149,9 @@ __global__ void k_assemble(AsmArgs a) {
     const int64_t nslices = (g.rows + 31) >> 5;
     if ((row >> 5) >= nslices) return;
     const int lane = (int)(row & 31);
-    const int64_t s = row >> 5;
+    // CRS: row slice; SEG/SYM: storage position of the row's slice (interior-first order)
+    const int64_t s = (a.fmt != FMT_CRS && a.slice_pos) ? (int64_t)a.slice_pos[row >> 5]
+                                                        : (row >> 5);
     if (row >= g.rows) {                           // padding lanes of the last slice
         if (a.fmt == FMT_CRS) {
             const int64_t base = a.slice_off[s] + lane;
@@ -162,7 +164,7 @@ __global__ void k_assemble(AsmArgs a) {
             const int nslot = a.fmt == FMT_SYM ? 14 : 27;
             for (int t = 0; t < nslot; ++t) a.val[(nslot * s + t) * 32 + lane] = 0.0;
             for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
-            a.mask[row] = 0u;                      // mask is padded to 32 * slices
+            a.mask[s * 32 + lane] = 0u;            // mask is padded to 32 * slices
         }
         return;
     }
@@ -236,7 +238,7 @@ __global__ void k_assemble(AsmArgs a) {
             a.val[base + 32 * kk] = 0.0;
         }
     } else {
-        a.mask[row] = mask;
+        a.mask[s * 32 + lane] = mask;
     }
     if (row_bc) b = (ix == g.nx) ? 1.0 : 0.0;
     a.b[row] = b;
@@ -269,8 +271,8 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
     const int64_t warps_per_block = blockDim.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * warps_per_block;
     const Matrix &m = a.m;
-    for (int64_t s = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5); s < m.nslices;
-         s += nw) {
+    for (int64_t s = a.s_begin + (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+         s < a.s_end; s += nw) {
         const int64_t off = m.slice_off[s];
         const int w = (int)((m.slice_off[s + 1] - off) >> 5);
         const int64_t row = s * 32 + lane;
@@ -335,11 +337,11 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_seg(SpmvArgs a) {
     const int64_t warps_per_block = blockDim.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * warps_per_block;
     const Matrix &m = a.m;
-    for (int64_t s = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5); s < m.nslices;
-         s += nw) {
-        const int64_t row = s * 32 + lane;
+    for (int64_t s = a.s_begin + (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+         s < a.s_end; s += nw) {
+        const int64_t row = (m.slice_row ? (int64_t)m.slice_row[s] : s) * 32 + lane;
         const bool live = row < m.rows;
-        const unsigned msk = live ? ld_stream(m.mask + row, pol) : 0u;
+        const unsigned msk = live ? ld_stream(m.mask + s * 32 + lane, pol) : 0u;
         const int32_t *sp = m.seg + 9 * s * 32 + lane;
         const double *vp = m.val + 27 * s * 32 + lane;
         int st[9];
@@ -485,7 +487,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
     __syncthreads();
     if (FUSED && s_stop) return;
     const Matrix &m = a.m;
-    const int64_t ntiles = (m.nslices + TILE - 1) / TILE;
+    const int64_t sb = a.s_begin, se = a.s_end;        // storage slices of this launch
+    const int64_t ntiles = (se - sb + TILE - 1) / TILE;
 
     if (warp == TMA_WARPS) {
         // ---------------- producer: one elected lane issues the bulk copies -------------
@@ -495,8 +498,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
                 const int st = (int)(i % STAGES);
                 if (i >= STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / STAGES) & 1) ^ 1));
-                const int64_t s0 = tile * TILE;
-                const int64_t rem = m.nslices - s0;
+                const int64_t s0 = sb + tile * TILE;
+                const int64_t rem = se - s0;
                 const int nsl = rem < TILE ? (int)rem : TILE;
                 unsigned char *buf = smem + (size_t)st * STAGE_B;
                 if (FMT != FMT_CRS) {
@@ -526,10 +529,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
             const int st = (int)(i % STAGES);
             mbar_wait(&full_bar[st], (uint32_t)((i / STAGES) & 1));
-            const int64_t s = tile * TILE + warp;
-            if (s < m.nslices) {
+            const int64_t s = sb + tile * TILE + warp;        // storage slice
+            if (s < se) {
                 const unsigned char *buf = smem + (size_t)st * STAGE_B;
-                const int64_t row = s * 32 + lane;
+                const int64_t row = (m.slice_row ? (int64_t)m.slice_row[s] : s) * 32 + lane;
                 double sum = 0.0, pdiag = 0.0;
                 if (FMT != FMT_CRS) {
                     const double *vs = reinterpret_cast<const double *>(buf) + warp * NV * 32 + lane;
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
                     pdiag = xv[13];
                     if (FUSED && row < m.rows) a.p_new[row] = pdiag;
                 } else {
-                    const int64_t e0 = m.slice_off[tile * TILE];
+                    const int64_t e0 = m.slice_off[sb + tile * TILE];
                     const int64_t so = m.slice_off[s] - e0;
                     const int w = (int)((m.slice_off[s + 1] - m.slice_off[s]) >> 5);
                     const double *vs = reinterpret_cast<const double *>(buf) + so + lane;
@@ -1403,7 +1406,9 @@ __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t row = rows[i];
-    const int64_t s = row >> 5, lane = row & 31;
+    const int64_t lane = row & 31;
+    const int64_t s = (m.fmt != FMT_CRS && m.slice_pos) ? (int64_t)m.slice_pos[row >> 5]
+                                                        : (row >> 5);   // storage slice
     int len = 0;
     if (m.fmt == FMT_CRS) {
         len = m.row_len[row];
@@ -1412,7 +1417,7 @@ __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t
             out_val[27 * i + k] = m.val[m.slice_off[s] + 32 * k + lane];
         }
     } else {
-        const unsigned msk = m.mask[row];
+        const unsigned msk = m.mask[s * 32 + lane];
         for (int t = 0; t < 27; ++t) {
             if (!((msk >> t) & 1u)) continue;
             const int c = m.seg[(9 * s + t / 3) * 32 + lane] + t % 3;
@@ -1487,7 +1492,7 @@ static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
     cudaError_t e = ensure_smem_attr(k_spmv_tma<DOT, FMT, IDENT, FUSED>, SMEM, attr_set);
     if (e != cudaSuccess) return e;
     query_occupancy();
-    const int64_t ntiles = (a.m.nslices + TILE - 1) / TILE;
+    const int64_t ntiles = (a.s_end - a.s_begin + TILE - 1) / TILE;
     const int grid = (int)std::min<int64_t>(ntiles, g_sms);
     k_spmv_tma<DOT, FMT, IDENT, FUSED><<<grid > 0 ? grid : 1, TMA_THREADS, SMEM, s>>>(a);
     return cudaGetLastError();
@@ -1539,6 +1544,7 @@ static int spmv_impl(int fmt) {
 }
 
 cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t s) {
+    if (a.s_end <= a.s_begin) return cudaSuccess;           // empty slice range
     if (a.fused_k > 0) {
         if (a.m.fmt != FMT_SEG || !a.g.ident || !with_dot) return cudaErrorInvalidValue;
         return launch_tma<true, FMT_SEG, true, true>(a, s);

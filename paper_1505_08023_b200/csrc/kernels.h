@@ -52,6 +52,11 @@ struct Matrix {
     const int32_t *col;                 // CRS only
     const int32_t *seg;                 // SEG/SYM: [(9s + j)32 + lane], start column of run j
     const uint32_t *mask;               // SEG/SYM: [32 slices], bit t = slot t present
+    // SEG, multi-part: slices are STORED interior-first.  slice_row[q] = row
+    // slice held at storage position q, slice_pos = its inverse; null = identity.  val, seg
+    // and mask are indexed by storage position, vectors by row.
+    const int32_t *slice_row;
+    const int32_t *slice_pos;
 };
 
 struct AsmArgs {
@@ -64,11 +69,13 @@ struct AsmArgs {
     uint32_t *mask;                     // SEG / SYM
     double *val;
     double *b;                          // [rows]
+    const int32_t *slice_pos;           // SEG: row slice -> storage position (null: identity)
 };
 
 struct SpmvArgs {
     Matrix m;
     Geom g;
+    int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
     unsigned long long *acc;            // pAp accumulator (DOT only)

@@ -67,6 +67,20 @@ int64_t Plan::local_nnz() const {
     return n_owned == 0 ? 0 : prod;
 }
 
+int64_t Plan::slice_order(std::vector<int32_t> &order) const {
+    const int64_t ns = (n_owned + 31) / 32;
+    std::vector<int32_t> inner, outer;
+    for (int64_t s = 0; s < ns; ++s) {
+        bool halo = false;
+        for (int64_t l = 32 * s; l < 32 * s + 32 && l < n_owned && !halo; ++l)
+            halo = row_reads_halo(l);
+        (halo ? outer : inner).push_back((int32_t)s);
+    }
+    order = inner;
+    order.insert(order.end(), outer.begin(), outer.end());
+    return (int64_t)inner.size();
+}
+
 // x-runs per row = (#present y-neighbors) * (#present z-neighbors): 9 inside, fewer on y/z
 // boundary planes; summed separably over the owned box.
 int64_t Plan::local_nns() const {

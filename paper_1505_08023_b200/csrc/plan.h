@@ -72,6 +72,23 @@ struct Plan {
                iz >= own_lo[2] && iz <= own_hi[2];
     }
     int64_t local_nnz() const;            // closed form over the owned box
+
+    // Row l reads a halo column iff its node lies on a face of the owned box beyond which
+    // the domain continues (the node across that face is owned by another rank).
+    bool row_reads_halo(int64_t l) const {
+        const int64_t lc[3] = {l % own_n[0], (l / own_n[0]) % own_n[1],
+                               l / (own_n[0] * own_n[1])};
+        const int n[3] = {mesh.nx, mesh.ny, mesh.nz};
+        for (int k = 0; k < 3; ++k) {
+            if (lc[k] == 0 && own_lo[k] > 0) return true;
+            if (lc[k] == own_n[k] - 1 && own_hi[k] < n[k]) return true;
+        }
+        return false;
+    }
+    // SELL-32 slice storage order for halo/interior overlap: the slices none of
+    // whose rows reads a halo column first (ascending), then the others (ascending).
+    // order[storage position] = row slice; returns the number of interior slices.
+    int64_t slice_order(std::vector<int32_t> &order) const;
 };
 
 // Owned node box of `rank` (S:97 lowest-rank rule; DESIGN §4 shows it is a box: the closed

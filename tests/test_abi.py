@@ -102,3 +102,24 @@ def test_halo_lists_consistent(n, p):
             expect = Ls["ext_gids"][recv_off:recv_off + Ls["recv_cnt"][ks]]
             sent = own_r[Lr["send_idx"][send_off[k]:send_off[k + 1]]]
             assert np.array_equal(sent, expect)
+
+
+@pytest.mark.parametrize("n,p", [((4, 4, 4), 1), ((6, 6, 6), 2), ((9, 4, 5), 5),
+                                 ((6, 6, 6), 8), ((40, 8, 6), 2), ((12, 40, 9), 4)])
+def test_interior_slices_match_brute_force(n, p):
+    """DESIGN §7 overlap split: a SELL-32 slice of owned rows is interior iff none of its rows
+    has a 27-point neighbour owned by another rank (brute force over the oracle's structure
+    and ownership)."""
+    boxes = O.rcb(*n, p)
+    rp, col = O.structure(*n)
+    for r in range(p):
+        info = M.plan(*n, p, r)
+        own = O.owned(*n, boxes, r)
+        owned_set = np.zeros(rp.size - 1, dtype=bool)
+        owned_set[own] = True
+        reads_halo = np.array([not owned_set[col[rp[g]:rp[g + 1]]].all() for g in own])
+        slices = [reads_halo[i:i + 32] for i in range(0, own.size, 32)]
+        interior = sum(1 for s in slices if not s.any())
+        assert info.interior_slices == interior
+        if p == 1:
+            assert interior == info.slices
