@@ -990,7 +990,27 @@ static int ensure_fused_buffers(minife_ctx *c) {   // never called while a strea
     return MINIFE_OK;
 }
 
+// One-CTA solver for small single-part problems (kernels.h: SMALL_MAX_ROWS rows, SEG/SYM);
+// MINIFE_SMALL=0 forces the multi-kernel sequence.  Profile mode always times the latter.
+static bool small_mode(const minife_ctx *c) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("MINIFE_SMALL");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    const Part &p = c->parts[0];
+    return env && c->parts.size() == 1 && c->world == 1 && p.ncols == p.rows &&
+           p.rows <= SMALL_MAX_ROWS && (c->fmt == MINIFE_FMT_SEG || c->fmt == MINIFE_FMT_SYM);
+}
+
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
+    if (!t && small_mode(c)) {
+        Part &p = c->parts[0];
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_cg_small(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
+                                    launch_stream(c, p)));
+        return MINIFE_OK;
+    }
     const bool fused = fused_mode(c);
     TRY(enqueue_init(c, tol));
     if (t) t->mark(-1);

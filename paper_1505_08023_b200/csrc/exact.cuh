@@ -132,6 +132,66 @@ struct Expansion {
     }
 };
 
+// 16-bit digit grid of warp_flush as 32-bit shared counters: dig[D] weighs 2^(16 D - 1074).
+// A warp contributes |sum| < 2^21 per digit, so a CTA of <= 1024 warps stays inside int32,
+// and 32-bit shared atomics are native (the 64-bit ones are CAS loops).
+constexpr int ACC_DIG16 = 2 * ACC_DIGITS;
+
+__device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int *dig,
+                                                       unsigned long long *acc) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int j = 0; j < NEXP; ++j) {
+        const double v = ex.c[j];
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+        const int e = (int)((bits >> 52) & 0x7ff);
+        const unsigned long long frac = bits & 0xfffffffffffffull;
+        const bool nz = (e != 0 || frac != 0) && e != 0x7ff;
+        const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
+        const int pos = e ? e - 1 : 0;
+        const int d16 = pos >> 4, s16 = pos & 15;
+        const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
+        if (e == 0x7ff) acc_add(acc, v);                      // flag word
+        if (dmax1 == 0u) continue;                            // warp-uniform
+        const int lo = (int)dmax1 - 1 - 8;
+        const bool inwin = nz && d16 >= lo;
+        if (nz && !inwin) acc_add(acc, v);                    // far below: slow path
+        const unsigned long long mlo = m << s16;
+        const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
+        int ch[5];
+        ch[0] = (int)(mlo & 0xffff);
+        ch[1] = (int)((mlo >> 16) & 0xffff);
+        ch[2] = (int)((mlo >> 32) & 0xffff);
+        ch[3] = (int)(mlo >> 48);
+        ch[4] = (int)mhi;
+        if (bits >> 63) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
+        }
+#pragma unroll
+        for (int t = 0; t < 13; ++t) {
+            const int D = lo + t;
+            const int q = D - d16;
+            int contrib = 0;
+#pragma unroll
+            for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
+            const int sum = __reduce_add_sync(FULL, contrib);
+            if (lane == 0 && sum != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], sum);
+        }
+    }
+}
+
+// acc[w] += dig[2w] + 2^16 dig[2w+1] (one warp), then dig = 0
+__device__ __forceinline__ void digits_to_words(int *dig, unsigned long long *acc) {
+    for (int w = threadIdx.x & 31; w < ACC_DIGITS; w += 32) {
+        const long long v = (long long)dig[2 * w] + (long long)dig[2 * w + 1] * 65536ll;
+        acc[w] += (unsigned long long)v;
+        dig[2 * w] = 0;
+        dig[2 * w + 1] = 0;
+    }
+}
+
 // CTA helpers: zero the shared words (all threads), merge them into a global accumulator.
 __device__ __forceinline__ void acc_zero_shared(unsigned long long *s) {
     for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = 0ull;

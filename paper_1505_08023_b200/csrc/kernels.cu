@@ -751,29 +751,31 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     acc_merge_to_global(sacc, a.acc_out);
 }
 
+// C6 step 1 decisions: rr_0, hist[0] = sqrt(rr_0), stop threshold fl(tol hist[0]) (one thread)
+__device__ __forceinline__ void cg_state_init(const UpdArgs &a, double rr0, double tol) {
+    const double h0 = __dsqrt_rn(rr0);
+    a.rr[0] = rr0;
+    a.hist[0] = h0;
+    CgState st;
+    st.done = 0;
+    st.status = 0;
+    st.iters = 0;
+    st.converged = 0;
+    st.stop = __dmul_rn(tol, h0);
+    st.pAp = 0.0;
+    st.alpha = 0.0;
+    st.beta = 0.0;
+    st.alpha_iter = 0;
+    st.x_done = 0;
+    *a.st = st;
+}
+
 __global__ void k_init_finalize(UpdArgs a, double tol) {
     __shared__ unsigned long long s_in[ACC_WORDS];
     acc_load_shared(s_in, a.acc_out);
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
-    if (threadIdx.x == 0) {
-        const double rr0 = fin;
-        const double h0 = __dsqrt_rn(rr0);
-        a.rr[0] = rr0;
-        a.hist[0] = h0;
-        CgState st;
-        st.done = 0;
-        st.status = 0;
-        st.iters = 0;
-        st.converged = 0;
-        st.stop = __dmul_rn(tol, h0);
-        st.pAp = 0.0;
-        st.alpha = 0.0;
-        st.beta = 0.0;
-        st.alpha_iter = 0;
-        st.x_done = 0;
-        *a.st = st;
-    }
+    if (threadIdx.x == 0) cg_state_init(a, fin, tol);
     if (a.acc_zero)
         for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
 }
@@ -925,6 +927,148 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
 
 // ----------------------------------------------------------------------------------------
 // a5 + a6: finalise rr' -> hist[k], stop tests, beta; p = r + beta p
+// ----------------------------------------------------------------------------------------
+// Small problems: the whole CG solve in ONE CTA of 1024 threads, one
+// launch.  At 10^3 (1331 rows) the three-kernel iteration is bound by launch and grid-wide
+// latency (~18 us/iteration); here an iteration is three CTA barriers apart.  p lives in
+// shared memory (the SpMV gathers it), x, r, Ap in registers (rows tid + 1024 j); the matrix
+// (SEG or SYM, L2-resident) is read from global memory.  Every dot goes through the same
+// exact expansion -> shared superaccumulator -> warp-parallel rounding, and every decision
+// through the same C6 code as the multi-kernel path: results are bit-identical.
+// ----------------------------------------------------------------------------------------
+
+template <int FMT>
+__device__ __forceinline__ double small_row_spmv(const Matrix &m, int64_t row,
+                                                 const double *ps) {
+    const int64_t s = row >> 5;
+    const int lane = (int)(row & 31);
+    const unsigned msk = m.mask[s * 32 + lane];
+    int sg[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) sg[j] = m.seg[(9 * s + j) * 32 + lane];
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < 27; ++t) {
+        if (!((msk >> t) & 1u)) continue;
+        const int c = sg[t / 3] + (t % 3);
+        double v;
+        if (FMT == FMT_SEG) v = m.val[(27 * s + t) * 32 + lane];
+        else if (t >= 13) v = m.val[(14 * s + (t - 13)) * 32 + lane];
+        else v = m.val[((int64_t)(c >> 5) * 14 + (13 - t)) * 32 + (c & 31)];   // mirror
+        sum = __dadd_rn(sum, __dmul_rn(v, ps[c]));
+    }
+    return sum;
+}
+
+// One exact block-wide dot: every thread's expansion -> 32-bit digit counters -> words ->
+// warp-parallel rounding (warp 0; the value is returned to thread 0 only).
+__device__ __forceinline__ double small_block_dot(const Expansion &ex, int *dig,
+                                                  unsigned long long *sacc) {
+    expansion_flush_digits(ex, dig, sacc);
+    __syncthreads();
+    double v = 0.0;
+    if (threadIdx.x < 32) {
+        digits_to_words(dig, sacc);
+        __syncwarp();
+        v = acc_finalize_warp(sacc);
+        __syncwarp();
+        for (int i = threadIdx.x; i < ACC_WORDS; i += 32) sacc[i] = 0ull;
+    }
+    return v;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs a, int K,
+                                                               double tol) {
+    __shared__ double ps[SMALL_MAX_ROWS + 32];
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int dig[ACC_DIG16];
+    __shared__ double s_coef;
+    __shared__ int s_stop;
+    const int tid = threadIdx.x;
+    const int64_t rows = m.rows;
+    double xv[SMALL_RPT], rv[SMALL_RPT], apv[SMALL_RPT];
+    // C6 step 1: x = 0, r = b, p = b, rr_0 = dot(r, r)
+    acc_zero_shared(sacc);
+    for (int i = tid; i < ACC_DIG16; i += blockDim.x) dig[i] = 0;
+    __syncthreads();
+    Expansion ex;
+    ex.init();
+#pragma unroll
+    for (int j = 0; j < SMALL_RPT; ++j) {
+        const int64_t row = tid + (int64_t)SMALL_THREADS * j;
+        xv[j] = rv[j] = apv[j] = 0.0;
+        if (row < rows) {
+            const double b = a.b[row];
+            rv[j] = b;
+            ps[row] = b;
+            ex.add(__dmul_rn(b, b), sacc);
+        }
+    }
+    {
+        const double rr0 = small_block_dot(ex, dig, sacc);
+        if (tid == 0) cg_state_init(a, rr0, tol);
+    }
+    __syncthreads();
+    for (int k = 1; k <= K; ++k) {
+        // a2 + a3: Ap = A p, pAp, alpha (stop tests of K6)
+        ex.init();
+#pragma unroll
+        for (int j = 0; j < SMALL_RPT; ++j) {
+            const int64_t row = tid + (int64_t)SMALL_THREADS * j;
+            if (row < rows) {
+                apv[j] = small_row_spmv<FMT>(m, row, ps);
+                ex.add(__dmul_rn(ps[row], apv[j]), sacc);
+            }
+        }
+        {
+            const double pAp = small_block_dot(ex, dig, sacc);
+            if (tid == 0) {
+                double alpha;
+                s_stop = xr_prologue(a, pAp, k, alpha);
+                s_coef = alpha;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        // a4 + a5: x += alpha p, r -= alpha Ap, rr', beta (stop tests of K7)
+        const double alpha = s_coef;
+        ex.init();
+#pragma unroll
+        for (int j = 0; j < SMALL_RPT; ++j) {
+            const int64_t row = tid + (int64_t)SMALL_THREADS * j;
+            if (row < rows) xr_step(xv[j], rv[j], ps[row], apv[j], alpha, ex, sacc);
+        }
+        {
+            const double rrn = small_block_dot(ex, dig, sacc);
+            if (tid == 0) {
+                double beta;
+                s_stop = rr_decision(rrn, k, a.hist, a.rr, a.st, beta);
+                s_coef = beta;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        // a6: p = r + beta p
+        const double beta = s_coef;
+#pragma unroll
+        for (int j = 0; j < SMALL_RPT; ++j) {
+            const int64_t row = tid + (int64_t)SMALL_THREADS * j;
+            if (row < rows) ps[row] = __dadd_rn(rv[j], __dmul_rn(beta, ps[row]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < SMALL_RPT; ++j) {
+        const int64_t row = tid + (int64_t)SMALL_THREADS * j;
+        if (row < rows) {
+            a.x[row] = xv[j];
+            a.r[row] = rv[j];
+            a.p[row] = ps[row];
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------------------
 
 template <bool IDENT>
@@ -1573,6 +1717,16 @@ cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t
         if (with_dot) k_spmv_crs<true, false><<<grid, SPMV_THREADS, 0, s>>>(a);
         else k_spmv_crs<false, false><<<grid, SPMV_THREADS, 0, s>>>(a);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_small(const Matrix &m, const UpdArgs &a, int K, double tol,
+                            cudaStream_t s) {
+    if (m.rows > SMALL_MAX_ROWS || !a.g.ident || (m.fmt != FMT_SEG && m.fmt != FMT_SYM) ||
+        m.slice_row)
+        return cudaErrorInvalidValue;
+    if (m.fmt == FMT_SEG) k_cg_small<FMT_SEG><<<1, SMALL_THREADS, 0, s>>>(m, a, K, tol);
+    else k_cg_small<FMT_SYM><<<1, SMALL_THREADS, 0, s>>>(m, a, K, tol);
     return cudaGetLastError();
 }
 

@@ -122,6 +122,12 @@ cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp
 cudaError_t launch_cg_finish(const UpdArgs &a, int K, const double *p_even, const double *p_odd,
                              int grid, cudaStream_t s);
 
+// Whole CG solve (init + up to K iterations, C6) in one CTA: one part, FMT_SEG or FMT_SYM,
+// rows <= SMALL_MAX_ROWS.  Same state, history and vectors as the multi-kernel sequence.
+constexpr int SMALL_THREADS = 1024, SMALL_RPT = 2, SMALL_MAX_ROWS = SMALL_THREADS * SMALL_RPT;
+cudaError_t launch_cg_small(const Matrix &m, const UpdArgs &a, int K, double tol,
+                            cudaStream_t s);
+
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
                         const int32_t *didx, int64_t n, cudaStream_t s);
