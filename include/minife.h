@@ -58,8 +58,9 @@ extern "C" {
                                   (their default); results identical to the other formats.    */
 
 /* ---- CG iteration schemes ------------------------------------------------- */
-#define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | x/r update + rr | p update.      */
-                               /* Default.  12 nnz-class bytes + 88 B per row.               */
+#define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | r update + rr | x and p update   */
+                               /* (x += alpha p with the p read for the p update).  Default. */
+                               /* 12 nnz-class bytes + 80 B per row.                         */
 #define MINIFE_SCHEME_FUSED 1  /* SURVEY §8(f) NEXT #2, one part + MINIFE_FMT_SEG only (other */
                                /* ctxs run 3K): the p update is formed at gather time inside  */
                                /* the SpMV and x is updated one iteration late there; a second */

@@ -854,7 +854,14 @@ __device__ __forceinline__ int p_prologue(const UpdArgs &a, double rr_new, int k
     return rr_decision(rr_new, k, a.hist, a.rr, a.st, beta);
 }
 
-template <bool IDENT>
+// XL: x is updated by K7 (see launch_update_xr); K6 touches r only: 24 instead of 48 B/row.
+__device__ __forceinline__ void r_step(double &r, double ap, double alpha, Expansion &ex,
+                                       unsigned long long *sacc) {
+    r = __dsub_rn(r, __dmul_rn(alpha, ap));
+    ex.add(__dmul_rn(r, r), sacc);
+}
+
+template <bool IDENT, bool XL>
 __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) {
     __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
     __shared__ double s_alpha;
@@ -877,7 +884,33 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t rows = a.g.rows;
-    if (IDENT) {
+    if (XL) {
+        // r -= alpha Ap, exact rr (16-byte accesses, two pairs in flight per thread)
+        const int64_t n2 = rows >> 1;
+        double2 *r2 = reinterpret_cast<double2 *>(a.r);
+        const double2 *q2 = reinterpret_cast<const double2 *>(a.Ap);
+        int64_t i = tid;
+        for (; i + stride < n2; i += 2 * stride) {
+            double2 ra = r2[i], qa = q2[i], rb = r2[i + stride], qb = q2[i + stride];
+            r_step(ra.x, qa.x, alpha, ex, sacc);
+            r_step(ra.y, qa.y, alpha, ex, sacc);
+            r_step(rb.x, qb.x, alpha, ex, sacc);
+            r_step(rb.y, qb.y, alpha, ex, sacc);
+            r2[i] = ra;
+            r2[i + stride] = rb;
+        }
+        for (; i < n2; i += stride) {
+            double2 ra = r2[i], qa = q2[i];
+            r_step(ra.x, qa.x, alpha, ex, sacc);
+            r_step(ra.y, qa.y, alpha, ex, sacc);
+            r2[i] = ra;
+        }
+        if ((rows & 1) && tid == 0) {
+            double rj = a.r[rows - 1];
+            r_step(rj, a.Ap[rows - 1], alpha, ex, sacc);
+            a.r[rows - 1] = rj;
+        }
+    } else if (IDENT) {
         // 16-byte vector accesses, two pairs in flight per thread
         const int64_t n2 = rows >> 1;
         double2 *x2 = reinterpret_cast<double2 *>(a.x);
@@ -1071,35 +1104,51 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs
 
 // ----------------------------------------------------------------------------------------
 
-template <bool IDENT>
+// XL: also x += fl(alpha_k p_k) with the p_k read for the p update -- also when K7's own
+// stop test fires (C6 updates x before the rr test), then without the p update.
+template <bool IDENT, bool XL>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     __shared__ unsigned long long s_in[ACC_WORDS];
-    __shared__ double s_beta;
+    __shared__ double s_beta, s_alpha;
     __shared__ int s_stop;
-    if (a.st->done) return;
+    if (a.st->done) return;              // K6 stopped (pAp test): no x update for this k
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
+        if (XL) s_alpha = a.st->alpha;   // alpha_k, written by K6 before this launch
         double beta;
         s_stop = p_prologue(a, fin, k, beta);
         s_beta = beta;
     }
     __syncthreads();
-    if (s_stop) return;
-    if (blockIdx.x == 0 && a.acc_zero)
+    const bool stop = s_stop;
+    if (stop && !XL) return;
+    if (!stop && blockIdx.x == 0 && a.acc_zero)
         for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
-    const double beta = s_beta;
+    const double beta = s_beta, alpha = XL ? s_alpha : 0.0;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t rows = a.g.rows;
     if (IDENT) {
         const int64_t n2 = rows >> 1;
         double2 *p2 = reinterpret_cast<double2 *>(a.p);
+        double2 *x2 = reinterpret_cast<double2 *>(a.x);
         const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
         int64_t i = tid;
         for (; i + stride < n2; i += 2 * stride) {
-            double2 pa = p2[i], ra = r2[i], pb = p2[i + stride], rb = r2[i + stride];
+            double2 pa = p2[i], pb = p2[i + stride];
+            if (XL) {
+                double2 xa = x2[i], xb = x2[i + stride];
+                xa.x = __dadd_rn(xa.x, __dmul_rn(alpha, pa.x));
+                xa.y = __dadd_rn(xa.y, __dmul_rn(alpha, pa.y));
+                xb.x = __dadd_rn(xb.x, __dmul_rn(alpha, pb.x));
+                xb.y = __dadd_rn(xb.y, __dmul_rn(alpha, pb.y));
+                x2[i] = xa;
+                x2[i + stride] = xb;
+                if (stop) continue;
+            }
+            const double2 ra = r2[i], rb = r2[i + stride];
             pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
             pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
             pb.x = __dadd_rn(rb.x, __dmul_rn(beta, pb.x));
@@ -1108,19 +1157,31 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             p2[i + stride] = pb;
         }
         for (; i < n2; i += stride) {
-            double2 pa = p2[i], ra = r2[i];
+            double2 pa = p2[i];
+            if (XL) {
+                double2 xa = x2[i];
+                xa.x = __dadd_rn(xa.x, __dmul_rn(alpha, pa.x));
+                xa.y = __dadd_rn(xa.y, __dmul_rn(alpha, pa.y));
+                x2[i] = xa;
+                if (stop) continue;
+            }
+            const double2 ra = r2[i];
             pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
             pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
             p2[i] = pa;
         }
         if ((rows & 1) && tid == 0) {
             const int64_t j = rows - 1;
-            a.p[j] = __dadd_rn(a.r[j], __dmul_rn(beta, a.p[j]));
+            const double pj = a.p[j];
+            if (XL) a.x[j] = __dadd_rn(a.x[j], __dmul_rn(alpha, pj));
+            if (!stop) a.p[j] = __dadd_rn(a.r[j], __dmul_rn(beta, pj));
         }
     } else {
         for (int64_t i = tid; i < rows; i += stride) {
             const int64_t c = row_to_col(a.g, i);
-            a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[c]));
+            const double pc = a.p[c];
+            if (XL) a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc));
+            if (!stop) a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, pc));
         }
     }
 }
@@ -1238,106 +1299,7 @@ constexpr int UT_STAGES = 6;                          // 6 x 32 KB in flight per
 constexpr int UT_CWARPS = 8;                          // consumer warps
 constexpr int UT_THREADS = 32 * (UT_CWARPS + 1);      // + producer warp
 constexpr int UT_CONS = 32 * UT_CWARPS;
-constexpr int XR_SMEM = UT_STAGES * 4 * UT_ROWS * 8;  // x, r, p, Ap   = 192 KB
-constexpr int P_SMEM = UT_STAGES * 2 * UT_ROWS * 8;   // r, p          =  96 KB
 
-// XR = true: K6 (x += alpha p, r -= alpha Ap, exact rr);  XR = false: K7 (p = r + beta p)
-template <bool XR>
-__global__ void __launch_bounds__(UT_THREADS, 1) k_update_tma(UpdArgs a, int k) {
-    constexpr int NIN = XR ? 4 : 2;
-    constexpr int STAGE_D = NIN * UT_ROWS;            // doubles per stage
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sm = reinterpret_cast<double *>(smem_raw);
-    __shared__ __align__(8) uint64_t full_bar[UT_STAGES], empty_bar[UT_STAGES];
-    __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
-    __shared__ double s_coef;
-    __shared__ int s_stop;
-    if (a.st->done) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    acc_load_shared(s_in, a.acc_in);
-    __syncthreads();
-    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < UT_STAGES; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], UT_CWARPS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        double coef;
-        s_stop = XR ? xr_prologue(a, fin, k, coef) : p_prologue(a, fin, k, coef);
-        s_coef = coef;
-    }
-    if (XR) acc_zero_shared(sacc);
-    __syncthreads();
-    if (s_stop) return;
-    if (!XR && blockIdx.x == 0 && a.acc_zero)
-        for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
-    const double coef = s_coef;
-    const int64_t rows = a.g.rows;
-    const int64_t ntiles = (rows + UT_ROWS - 1) / UT_ROWS;
-
-    if (warp == UT_CWARPS) {
-        if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
-            int64_t i = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-                const int st = (int)(i % UT_STAGES);
-                if (i >= UT_STAGES) mbar_wait(&empty_bar[st], (uint32_t)(((i / UT_STAGES) & 1) ^ 1));
-                const int64_t r0 = t * UT_ROWS;
-                const int64_t n = min((int64_t)UT_ROWS, rows - r0);
-                const uint32_t bytes = (uint32_t)(((n + 1) & ~(int64_t)1) * 8);   // 16 B multiple
-                double *buf = sm + (size_t)st * STAGE_D;
-                mbar_expect_tx(&full_bar[st], NIN * bytes);
-                if (XR) {
-                    bulk_g2s(buf, a.x + r0, bytes, &full_bar[st], pol);
-                    bulk_g2s(buf + UT_ROWS, a.r + r0, bytes, &full_bar[st], pol);
-                    bulk_g2s(buf + 2 * UT_ROWS, a.p + r0, bytes, &full_bar[st], pol);
-                    bulk_g2s(buf + 3 * UT_ROWS, a.Ap + r0, bytes, &full_bar[st], pol);
-                } else {
-                    bulk_g2s(buf, a.r + r0, bytes, &full_bar[st], pol);
-                    bulk_g2s(buf + UT_ROWS, a.p + r0, bytes, &full_bar[st], pol);
-                }
-            }
-        }
-    } else {
-        // two independent expansions per thread: two TwoSum dependency chains in flight
-        Expansion ex[2];
-        ex[0].init();
-        ex[1].init();
-        int64_t i = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-            const int st = (int)(i % UT_STAGES);
-            mbar_wait(&full_bar[st], (uint32_t)((i / UT_STAGES) & 1));
-            const double *buf = sm + (size_t)st * STAGE_D;
-            const int64_t r0 = t * UT_ROWS;
-#pragma unroll
-            for (int j = 0; j < UT_ROWS / UT_CONS; ++j) {
-                const int l = threadIdx.x + j * UT_CONS;
-                if (r0 + l < rows) {
-                    if (XR) {
-                        double xi = buf[l], ri = buf[UT_ROWS + l];
-                        xr_step(xi, ri, buf[2 * UT_ROWS + l], buf[3 * UT_ROWS + l], coef,
-                                ex[j & 1], sacc);
-                        __stcs(a.x + r0 + l, xi);
-                        __stcs(a.r + r0 + l, ri);
-                    } else {
-                        __stcs(a.p + r0 + l, __dadd_rn(buf[l], __dmul_rn(coef, buf[UT_ROWS + l])));
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[st]);
-        }
-        if (XR) {
-            ex[0].warp_flush(sacc);
-            ex[1].warp_flush(sacc);
-        }
-    }
-    if (XR) {
-        __syncthreads();
-        acc_merge_to_global(sacc, a.acc_out);
-    }
-}
 
 // Pure-read probe with the same bulk-copy engine (B_read for the TMA kernels).
 __global__ void __launch_bounds__(UT_THREADS, 1) k_read_tma(const double *src, int64_t n,
@@ -1591,8 +1553,8 @@ static void query_occupancy() {
                                                   SPMV_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_spmv_bps[1], k_spmv_seg<true>,
                                                   SPMV_THREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_bps, k_update_xr<true>, UPD_THREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updp_bps, k_update_p<true>, UPD_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_upd_bps, k_update_xr<true, true>, UPD_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updp_bps, k_update_p<true, true>, UPD_THREADS, 0);
     if (g_updp_bps <= 0) g_updp_bps = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_updr_bps, k_update_r, UPD_THREADS, 0);
     if (g_updr_bps <= 0) g_updr_bps = 1;
@@ -1741,60 +1703,42 @@ cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-static int tma_update_grid(int64_t rows) {
-    query_occupancy();
-    const int64_t nt = (rows + UT_ROWS - 1) / UT_ROWS;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(nt, g_sms));
-}
-
-// Update kernels: register streaming by default (B200, 300^3: 0.375 ms/iteration for K6+K7
-// vs 0.417 ms for the TMA-pipelined variant, profiles/r01); MINIFE_UPD_IMPL=tma selects it.
-static bool upd_tma() {
+// x/r and p updates.  XL (default; MINIFE_X_LATE=0 restores the textbook split): K6 updates
+// r only and K7 applies x += alpha_k p_k while it reads p_k for p_(k+1) = r + beta p_k, so p
+// is read once per iteration (64 instead of 72 B per row).  Same values, same operations.
+static bool x_late() {
     static int v = -1;
     if (v < 0) {
-        const char *e = getenv("MINIFE_UPD_IMPL");
-        v = (e && e[0] == 't') ? 1 : 0;
+        const char *e = getenv("MINIFE_X_LATE");
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }
 
-// one part (rows == columns): TMA-pipelined streams; otherwise the register kernels that
-// map rows into the extended-box p
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    if (!a.g.ident || !upd_tma()) {
-        if (a.g.ident) k_update_xr<true><<<grid, UPD_THREADS, 0, s>>>(a, k);
-        else k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
-        return cudaGetLastError();
-    }
+    const bool xl = x_late();
     if (a.g.ident) {
-        static unsigned long long m = 0;
-        cudaError_t e = ensure_smem_attr(k_update_tma<true>, XR_SMEM, m);
-        if (e != cudaSuccess) return e;
-        k_update_tma<true><<<tma_update_grid(a.g.rows), UT_THREADS, XR_SMEM, s>>>(a, k);
+        if (xl) k_update_xr<true, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_xr<true, false><<<grid, UPD_THREADS, 0, s>>>(a, k);
     } else {
-        k_update_xr<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        if (xl) k_update_xr<false, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_xr<false, false><<<grid, UPD_THREADS, 0, s>>>(a, k);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    if (!a.g.ident || !upd_tma()) {
-        if (a.g.ident) {
-            // K7 has its own (higher) occupancy than K6, whose grid is passed in
-            const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
-            const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
-            k_update_p<true><<<g7, UPD_THREADS, 0, s>>>(a, k);
-        }
-        else k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
-        return cudaGetLastError();
-    }
+    const bool xl = x_late();
     if (a.g.ident) {
-        static unsigned long long m = 0;
-        cudaError_t e = ensure_smem_attr(k_update_tma<false>, P_SMEM, m);
-        if (e != cudaSuccess) return e;
-        k_update_tma<false><<<tma_update_grid(a.g.rows), UT_THREADS, P_SMEM, s>>>(a, k);
+        // K7 has its own (higher) occupancy than K6, whose grid is passed in
+        const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
+        const int g7 =
+            (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
+        if (xl) k_update_p<true, true><<<g7, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_p<true, false><<<g7, UPD_THREADS, 0, s>>>(a, k);
     } else {
-        k_update_p<false><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        if (xl) k_update_p<false, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
+        else k_update_p<false, false><<<grid, UPD_THREADS, 0, s>>>(a, k);
     }
     return cudaGetLastError();
 }
