@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libminife_b200.so")
+# MINIFE_LIB_PATH: an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("MINIFE_LIB_PATH") or os.path.join(_HERE, "lib", "libminife_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -9,6 +9,8 @@
 // stored k-major so a warp's load of entry k is one contiguous 256 B (val) / 128 B (index)
 // segment.  Entries of a row are kept in ascending GLOBAL column (C4 order); absent/padding
 // entries are never added (row-length predicate or presence mask).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -708,6 +710,155 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
 #pragma unroll
                 for (int t = 0; t < 13; ++t)
                     if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(lv[t], xv[t]));
+#pragma unroll
+                for (int t = 13; t < 27; ++t)
+                    if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
+                if (row < m.rows) {
+                    a.y[row] = sum;
+                    if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+        if (DOT) ex.warp_flush(sacc);
+    }
+    if (DOT) {
+        __syncthreads();
+        acc_merge_to_global(sacc, a.acc);
+    }
+}
+
+// SYM with the mirrored values staged by the tensor engine.  Lower run j of a row (j = 0..3:
+// (dz,dy) = (-1,-1), (-1,0), (-1,1), (0,-1); group 4 = slot 12, (0,0,-1)) reads stored slots
+// 11-3j..13-3j (group 4: slot 1) of rows i - 1 + e + off_j.  For a tile [r0, r0 + 32 NW) those
+// rows lie in the NW + 2 slices from floor((r0 - 1 + off_j) / 32): one 3-D box {32 lanes,
+// 3 slots, NW + 2 slices} of the value array viewed as [slices][14][32], fetched with one
+// cp.async.bulk.tensor per group (zero fill outside the matrix) -- from L2: the rows were
+// streamed about one plane (or one line) earlier.  Consumers read every matrix value from
+// shared memory; only the x gathers go through L1.
+template <int NW, int NST> struct SymmCfg {
+    static constexpr int THREADS = 32 * (NW + 1);
+    static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
+    static constexpr int GS = NW + 2;                          // slices per mirror box
+    static constexpr int MIR3_B = GS * 3 * 32 * 8;             // one 3-slot box
+    static constexpr int MIR1_B = GS * 32 * 8;                 // the slot-12 box
+    static constexpr int MIR0 = (VAL_B + SEG_B + MSK_B + 127) / 128 * 128;
+    static constexpr int STAGE_B = (MIR0 + 4 * MIR3_B + MIR1_B + 127) / 128 * 128;
+    static constexpr int SMEM = NST * STAGE_B;
+};
+
+// first slice of mirror box g (0..4) of the tile whose first row is r0 (may be negative)
+__device__ __forceinline__ int symm_box_slice(int64_t r0, int g, int64_t N0, int64_t P) {
+    const int dz = g < 3 ? -1 : 0, dy = g < 3 ? g - 1 : (g == 3 ? -1 : 0);
+    const int64_t lo = r0 - 1 + dy * N0 + dz * P;
+    return (int)(lo >> 5);                                     // floor division
+}
+
+__device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <bool DOT, int NW, int NST>
+__global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
+    k_spmv_symm(SpmvArgs a, const __grid_constant__ CUtensorMap tm3,
+                const __grid_constant__ CUtensorMap tm1) {
+    using C = SymmCfg<NW, NST>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST];
+    __shared__ unsigned long long sacc[ACC_WORDS];
+    if (DOT && a.st && a.st->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (DOT) {
+        acc_zero_shared(sacc);
+        if (blockIdx.x == 0 && a.acc_zero)
+            for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    }
+    __syncthreads();
+    const Matrix &m = a.m;
+    const int64_t ntiles = (m.nslices + NW - 1) / NW;
+    const int64_t N0 = a.g.ext_n[0], P = (int64_t)a.g.ext_n[0] * a.g.ext_n[1];
+
+    if (warp == NW) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm1)) : "memory");
+            const uint64_t pol = evict_first_policy();
+            uint64_t pol_keep;
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+            int64_t i = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int st = (int)(i % NST);
+                if (i >= NST) mbar_wait(&empty_bar[st], (uint32_t)(((i / NST) & 1) ^ 1));
+                const int64_t s0 = tile * NW;
+                const int64_t rem = m.nslices - s0;
+                const int nsl = rem < NW ? (int)rem : NW;
+                unsigned char *buf = smem + (size_t)st * C::STAGE_B;
+                const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
+                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B);
+                bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &full_bar[st], pol_keep);
+                bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
+                bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
+                const int64_t r0 = s0 * 32;
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, 11 - 3 * g,
+                             symm_box_slice(r0, g, N0, P), &full_bar[st]);
+                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, 1, symm_box_slice(r0, 4, N0, P),
+                         &full_bar[st]);
+            }
+        }
+    } else {
+        Expansion ex;
+        ex.init();
+        int64_t i = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int st = (int)(i % NST);
+            mbar_wait(&full_bar[st], (uint32_t)((i / NST) & 1));
+            const int64_t s = tile * NW + warp;
+            if (s < m.nslices) {
+                const unsigned char *buf = smem + (size_t)st * C::STAGE_B;
+                const double *vs = reinterpret_cast<const double *>(buf) + warp * 14 * 32 + lane;
+                const int32_t *ss =
+                    reinterpret_cast<const int32_t *>(buf + C::VAL_B) + warp * 9 * 32 + lane;
+                const unsigned msk =
+                    reinterpret_cast<const uint32_t *>(buf + C::VAL_B + C::SEG_B)[warp * 32 + lane];
+                const double *mir = reinterpret_cast<const double *>(buf + C::MIR0);
+                const int64_t row = s * 32 + lane;
+                const int64_t r0 = tile * NW * 32;
+                int sg[9];
+#pragma unroll
+                for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
+                double xv[27];
+#pragma unroll
+                for (int t = 0; t < 27; ++t)
+                    xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
+                double sum = 0.0;
+#pragma unroll
+                for (int t = 0; t < 13; ++t) {
+                    const int g = t < 12 ? t / 3 : 4;
+                    const int q = t < 12 ? 2 - t % 3 : 0;              // slot 13-t - first slot
+                    const int nq = t < 12 ? 3 : 1;
+                    if ((msk >> t) & 1u) {
+                        const int c = sg[t / 3] + (t % 3);
+                        const int ga = symm_box_slice(r0, g, N0, P);
+                        const double lv = mir[g * (C::MIR3_B / 8) + ((c >> 5) - ga) * nq * 32 +
+                                              q * 32 + (c & 31)];
+                        sum = __dadd_rn(sum, __dmul_rn(lv, xv[t]));
+                    }
+                }
 #pragma unroll
                 for (int t = 13; t < 27; ++t)
                     if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
@@ -1604,10 +1755,65 @@ static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// 3-D tensor maps of the SYM value array [nslices][14][32] doubles: boxes of {32, 3, gs} and
+// {32, 1, gs}.  cuTensorMapEncodeTiled comes from the driver through the runtime (no -lcuda).
+static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000,
+                                             cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {32, 14, (cuuint64_t)m.nslices};
+    const cuuint64_t strides[2] = {32 * 8, 14 * 32 * 8};
+    const cuuint32_t box3[3] = {32, 3, (cuuint32_t)gs}, box1[3] = {32, 1, (cuuint32_t)gs};
+    const cuuint32_t es[3] = {1, 1, 1};
+    void *base = const_cast<double *>(m.val);
+    return enc(m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box3, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS &&
+           enc(m1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box1, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS;
+}
+
+template <bool DOT, int NW, int NST>
+static cudaError_t launch_symm(const SpmvArgs &a, cudaStream_t s) {
+    using C = SymmCfg<NW, NST>;
+    CUtensorMap m3, m1;
+    if (!sym_maps(a.m, C::GS, &m3, &m1)) return cudaErrorNotSupported;
+    static unsigned long long attr_set = 0;
+    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST>, C::SMEM, attr_set);
+    if (e != cudaSuccess) return e;
+    query_occupancy();
+    const int64_t ntiles = (a.m.nslices + NW - 1) / NW;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
+    k_spmv_symm<DOT, NW, NST><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
+    return cudaGetLastError();
+}
+
 // SYM tile shape (B200, 300^3: 16 consumer warps x 2 stages 0.90 ms/launch, 12 x 3 0.95 ms,
 // 8 x 4 1.31 ms -- the kernel is bound by the latency of its L2 gathers, so warps beat stages)
 template <bool DOT>
 static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
+    // default: mirrored values staged by tensor-map TMA (13 consumer warps, 2 stages; B200,
+    // 300^3: 1.196 ms per CG iteration vs 1.243 with L1 mirror gathers, profiles/r01/session2);
+    // MINIFE_SYM_CFG=0 (or no tensor-map support) selects the L1-gather kernel
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char *e = getenv("MINIFE_SYM_CFG");
+        cfg = e ? atoi(e) : 1;
+    }
+    if (cfg == 1) {
+        const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
     using C = SyCfg<16, 2>;
     static unsigned long long attr_set = 0;
     cudaError_t e = ensure_smem_attr(k_spmv_sym<DOT, 16, 2>, C::SMEM, attr_set);
