@@ -990,25 +990,38 @@ static int ensure_fused_buffers(minife_ctx *c) {   // never called while a strea
     return MINIFE_OK;
 }
 
-// One-CTA solver for small single-part problems (kernels.h: SMALL_MAX_ROWS rows, SEG/SYM);
-// MINIFE_SMALL=0 forces the multi-kernel sequence.  Profile mode always times the latter.
-static bool small_mode(const minife_ctx *c) {
-    static int env = -1;
-    if (env < 0) {
+// Single-launch solvers for small single-part problems (SEG/SYM): 0 = none, 1 = one CTA
+// (k_cg_small, <= SMALL_MAX_ROWS rows), 2 = one thread-block cluster (k_cg_cluster, <=
+// CL_MAX_ROWS rows).  MINIFE_SMALL=0/1/2 forces a choice (where it fits).  Profile mode always
+// times the multi-kernel sequence.
+static int small_mode(const minife_ctx *c) {
+    static int env = -2;
+    if (env == -2) {
         const char *e = getenv("MINIFE_SMALL");
-        env = (e && e[0] == '0') ? 0 : 1;
+        env = e ? atoi(e) : -1;
     }
     const Part &p = c->parts[0];
-    return env && c->parts.size() == 1 && c->world == 1 && p.ncols == p.rows &&
-           p.rows <= SMALL_MAX_ROWS && (c->fmt == MINIFE_FMT_SEG || c->fmt == MINIFE_FMT_SYM);
+    if (env == 0 || c->parts.size() != 1 || c->world != 1 || p.ncols != p.rows ||
+        (c->fmt != MINIFE_FMT_SEG && c->fmt != MINIFE_FMT_SYM))
+        return 0;
+    const bool fits1 = p.rows <= SMALL_MAX_ROWS;
+    const bool fits2 = p.rows <= CL_MAX_ROWS && (p.nslices + CL_CTAS - 1) / CL_CTAS <= CL_MAX_SL;
+    if (env == 1) return fits1 ? 1 : 0;
+    if (env == 2) return fits2 ? 2 : 0;
+    return fits2 ? 2 : (fits1 ? 1 : 0);
 }
 
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
-    if (!t && small_mode(c)) {
+    const int sm = t ? 0 : small_mode(c);
+    if (sm) {
         Part &p = c->parts[0];
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_cg_small(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
-                                    launch_stream(c, p)));
+        if (sm == 1)
+            CUDA_TRY(c, launch_cg_small(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
+                                        launch_stream(c, p)));
+        else
+            CUDA_TRY(c, launch_cg_cluster(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
+                                          launch_stream(c, p)));
         return MINIFE_OK;
     }
     const bool fused = fused_mode(c);

@@ -11,6 +11,7 @@
 // entries are never added (row-length predicate or presence mask).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1254,6 +1255,228 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs
 }
 
 // ----------------------------------------------------------------------------------------
+// Cluster-resident solver: the whole solve in ONE thread-block cluster
+// of CL_CTAS CTAs, one launch.  CTA q owns a contiguous block of slices; its matrix rows (all
+// 27 value slots, SYM mirrors resolved once at start) live in its shared memory, and every
+// CTA keeps a full copy of p, refreshed after each p update by distributed-shared-memory
+// stores.  A dot: each CTA reduces its expansions into 32-bit digit counters, pushes the
+// nonzero ones into EVERY CTA's receive counters (DSMEM atomics), one cluster barrier, then
+// every CTA rounds the same integers and takes the same C6 decision (CTA 0 records it).
+// Three cluster barriers per iteration; results bit-identical to every other path.
+// ----------------------------------------------------------------------------------------
+
+namespace cgx = cooperative_groups;
+
+constexpr int CL_NDIG = ACC_DIG16 + 4;            // + 4 digits for the top word's high part
+constexpr int CL_FLAG = CL_NDIG;                  // non-finite counter slot
+
+struct ClusterSmem {
+    double val[CL_MAX_SL][27][32];
+    int32_t seg[CL_MAX_SL][9][32];
+    uint32_t mask[CL_MAX_SL][32];
+    double pfull[CL_MAX_ROWS + 32];
+    int recv[2][CL_NDIG + 1];            // cluster sums, parity double-buffered
+    int dig[CL_NDIG + 1];                // this CTA's digit counters
+    unsigned long long sacc[ACC_WORDS];
+    unsigned long long fin[ACC_WORDS];
+    double coef;
+    int stop;
+};
+
+// Exact cluster-wide dot of the CTAs' expansions (all threads of every CTA call it); the
+// rounded value is returned to warp 0 of every CTA.  Each CTA reduces into its own digit
+// counters and adds the nonzero ones into EVERY CTA's receive counters (DSMEM atomics);
+// after one cluster barrier every CTA rounds the same integers.  recv[par] is cleared right
+// after use: it is written again two dots later, behind a barrier this CTA has not yet passed.
+// (Pulling all CTAs' counters after the barrier instead measured 1 us slower at 10^3.)
+__device__ __forceinline__ double cluster_dot(const Expansion &ex, ClusterSmem &S,
+                                              cgx::cluster_group &cl, int par) {
+    expansion_flush_digits(ex, S.dig, S.sacc);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        // words of the slow path (far-below values): as 16-bit digits, the top one signed
+        for (int w = lane; w < ACC_DIGITS; w += 32) {
+            const long long v = (long long)S.sacc[w];
+            S.sacc[w] = 0ull;
+            if (v) {
+                atomicAdd(&S.dig[2 * w], (int)(v & 0xffff));
+                atomicAdd(&S.dig[2 * w + 1], (int)((v >> 16) & 0xffff));
+                atomicAdd(&S.dig[2 * w + 2], (int)((v >> 32) & 0xffff));
+                atomicAdd(&S.dig[2 * w + 3], (int)(v >> 48));
+            }
+        }
+        if (lane == 0 && S.sacc[ACC_FLAG]) {
+            S.dig[CL_FLAG] += 1;
+            S.sacc[ACC_FLAG] = 0ull;
+        }
+        __syncwarp();
+        const int C = (int)cl.num_blocks();
+        for (int d = lane; d <= CL_NDIG; d += 32) {
+            const int v = S.dig[d];
+            S.dig[d] = 0;
+            if (v)
+                for (int r = 0; r < C; ++r) atomicAdd(cl.map_shared_rank(&S.recv[par][d], r), v);
+        }
+    }
+    cl.sync();
+    double v = 0.0;
+    if (threadIdx.x < 32) {
+        const int *rc = S.recv[par];
+        for (int w = lane; w < ACC_DIGITS; w += 32) {
+            long long x = (long long)rc[2 * w] + (long long)rc[2 * w + 1] * 65536ll;
+            if (w == ACC_DIGITS - 1)
+                x += ((long long)rc[2 * w + 2] << 32) + ((long long)rc[2 * w + 3] << 48);
+            S.fin[w] = (unsigned long long)x;
+        }
+        if (lane == 0) S.fin[ACC_FLAG] = rc[CL_FLAG] ? 1ull : 0ull;
+        __syncwarp();
+        v = acc_finalize_warp(S.fin);
+        __syncwarp();
+        for (int d = lane; d <= CL_NDIG; d += 32) S.recv[par][d] = 0;
+    }
+    return v;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs a, int K,
+                                                             double tol) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ClusterSmem &S = *reinterpret_cast<ClusterSmem *>(smem_raw);
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int q = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t rows = m.rows, ns = m.nslices;
+    const int64_t s_lo = ns * q / C, s_hi = ns * (q + 1) / C;
+    const int nsl = (int)(s_hi - s_lo);
+    // own rows' matrix into shared memory: 27 value slots (SYM: mirrors resolved here)
+    for (int e = tid; e < nsl * 27 * 32; e += CL_THREADS) {
+        const int sl = e / (27 * 32), t = (e / 32) % 27, ln = e % 32;
+        const int64_t sg = s_lo + sl;
+        const unsigned msk = m.mask[sg * 32 + ln];
+        double v = 0.0;
+        if ((msk >> t) & 1u) {
+            if (FMT == FMT_SEG) {
+                v = m.val[(27 * sg + t) * 32 + ln];
+            } else if (t >= 13) {
+                v = m.val[(14 * sg + (t - 13)) * 32 + ln];
+            } else {
+                const int c = m.seg[(9 * sg + t / 3) * 32 + ln] + t % 3;
+                v = m.val[((int64_t)(c >> 5) * 14 + (13 - t)) * 32 + (c & 31)];
+            }
+        }
+        S.val[sl][t][ln] = v;
+    }
+    for (int e = tid; e < nsl * 9 * 32; e += CL_THREADS) {
+        const int sl = e / (9 * 32), j = (e / 32) % 9, ln = e % 32;
+        S.seg[sl][j][ln] = m.seg[(9 * (s_lo + sl) + j) * 32 + ln];
+    }
+    for (int e = tid; e < nsl * 32; e += CL_THREADS) S.mask[e / 32][e % 32] = m.mask[s_lo * 32 + e];
+
+    for (int e = tid; e <= CL_NDIG; e += CL_THREADS) {
+        S.recv[0][e] = S.recv[1][e] = 0;
+        S.dig[e] = 0;
+    }
+    for (int e = tid; e < ACC_WORDS; e += CL_THREADS) S.sacc[e] = 0ull;
+    // C6 step 1: x = 0, r = b, p = b (every CTA holds all of p), rr_0
+    for (int64_t i = tid; i < rows; i += CL_THREADS) S.pfull[i] = a.b[i];
+    double xv[CL_RPT], rv[CL_RPT], apv[CL_RPT];
+    Expansion ex;
+    ex.init();
+#pragma unroll
+    for (int j = 0; j < CL_RPT; ++j) {
+        const int sl = warp + CL_WARPS * j;
+        const int64_t row = (s_lo + sl) * 32 + lane;
+        xv[j] = rv[j] = apv[j] = 0.0;
+        if (sl < nsl && row < rows) {
+            rv[j] = a.b[row];
+            ex.add(__dmul_rn(rv[j], rv[j]), S.sacc);
+        }
+    }
+    cl.sync();                                     // matrix, counters and p in place everywhere
+    int par = 0;
+    {
+        const double rr0 = cluster_dot(ex, S, cl, par);
+        par ^= 1;
+        if (q == 0 && tid == 0) cg_state_init(a, rr0, tol);
+    }
+    for (int k = 1; k <= K; ++k) {
+        // a2 + a3: Ap = A p (own rows), exact pAp, alpha
+        ex.init();
+#pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+            const int sl = warp + CL_WARPS * j;
+            const int64_t row = (s_lo + sl) * 32 + lane;
+            if (sl < nsl && row < rows) {
+                const unsigned msk = S.mask[sl][lane];
+                double sum = 0.0;
+#pragma unroll
+                for (int t = 0; t < 27; ++t)
+                    if ((msk >> t) & 1u)
+                        sum = __dadd_rn(sum, __dmul_rn(S.val[sl][t][lane],
+                                                       S.pfull[S.seg[sl][t / 3][lane] + t % 3]));
+                apv[j] = sum;
+                ex.add(__dmul_rn(S.pfull[row], sum), S.sacc);
+            }
+        }
+        {
+            const double pAp = cluster_dot(ex, S, cl, par);
+            par ^= 1;
+            if (tid == 0) {
+                double alpha;
+                S.stop = xr_prologue(a, pAp, k, alpha);   // CTA 0 records (blockIdx.x == 0)
+                S.coef = alpha;
+            }
+        }
+        __syncthreads();
+        if (S.stop) break;
+        // a4 + a5: x += alpha p, r -= alpha Ap, exact rr, beta
+        const double alpha = S.coef;
+        ex.init();
+#pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+            const int sl = warp + CL_WARPS * j;
+            const int64_t row = (s_lo + sl) * 32 + lane;
+            if (sl < nsl && row < rows) xr_step(xv[j], rv[j], S.pfull[row], apv[j], alpha, ex, S.sacc);
+        }
+        {
+            const double rrn = cluster_dot(ex, S, cl, par);
+            par ^= 1;
+            if (tid == 0) {
+                double beta;
+                S.stop = rr_decision(rrn, k, a.hist, a.rr, a.st, beta);
+                S.coef = beta;
+            }
+        }
+        __syncthreads();
+        if (S.stop) break;
+        // a6: p = r + beta p for own rows, stored into every CTA's copy
+        const double beta = S.coef;
+#pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+            const int sl = warp + CL_WARPS * j;
+            const int64_t row = (s_lo + sl) * 32 + lane;
+            if (sl < nsl && row < rows) {
+                const double pn = __dadd_rn(rv[j], __dmul_rn(beta, S.pfull[row]));
+                for (int r = 0; r < C; ++r) *cl.map_shared_rank(&S.pfull[row], r) = pn;
+            }
+        }
+        cl.sync();
+    }
+#pragma unroll
+    for (int j = 0; j < CL_RPT; ++j) {
+        const int sl = warp + CL_WARPS * j;
+        const int64_t row = (s_lo + sl) * 32 + lane;
+        if (sl < nsl && row < rows) {
+            a.x[row] = xv[j];
+            a.r[row] = rv[j];
+            a.p[row] = S.pfull[row];
+        }
+    }
+    cl.sync();                                     // no CTA exits while others may write to it
+}
+
+// ----------------------------------------------------------------------------------------
 
 // XL: also x += fl(alpha_k p_k) with the p_k read for the p update -- also when K7's own
 // stop test fires (C6 updates x before the rr test), then without the p update.
@@ -1896,6 +2119,46 @@ cudaError_t launch_cg_small(const Matrix &m, const UpdArgs &a, int K, double tol
     if (m.fmt == FMT_SEG) k_cg_small<FMT_SEG><<<1, SMALL_THREADS, 0, s>>>(m, a, K, tol);
     else k_cg_small<FMT_SYM><<<1, SMALL_THREADS, 0, s>>>(m, a, K, tol);
     return cudaGetLastError();
+}
+
+cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double tol,
+                              cudaStream_t s) {
+    if (m.rows > CL_MAX_ROWS || (m.nslices + CL_CTAS - 1) / CL_CTAS > CL_MAX_SL ||
+        !a.g.ident || (m.fmt != FMT_SEG && m.fmt != FMT_SYM) || m.slice_row)
+        return cudaErrorInvalidValue;
+    auto kern = m.fmt == FMT_SEG ? k_cg_cluster<FMT_SEG> : k_cg_cluster<FMT_SYM>;
+    const int smem = (int)sizeof(ClusterSmem);
+    static unsigned long long set = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!((set >> (dev & 63)) & 1ull)) {
+        cudaError_t e = cudaFuncSetAttribute(k_cg_cluster<FMT_SEG>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SEG>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        set |= 1ull << (dev & 63);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL_CTAS, 1, 1);
+    cfg.blockDim = dim3(CL_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL_CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, m, a, K, tol);
 }
 
 cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s) {

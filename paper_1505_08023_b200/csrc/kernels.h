@@ -128,6 +128,13 @@ constexpr int SMALL_THREADS = 1024, SMALL_RPT = 2, SMALL_MAX_ROWS = SMALL_THREAD
 cudaError_t launch_cg_small(const Matrix &m, const UpdArgs &a, int K, double tol,
                             cudaStream_t s);
 
+// Whole CG solve in ONE thread-block cluster of CL_CTAS CTAs (DSMEM): one part, FMT_SEG or
+// FMT_SYM, rows <= CL_MAX_ROWS and ceil(slices / CL_CTAS) <= CL_MAX_SL.
+constexpr int CL_CTAS = 16, CL_THREADS = 256, CL_WARPS = CL_THREADS / 32, CL_MAX_SL = 16,
+              CL_RPT = CL_MAX_SL / CL_WARPS, CL_MAX_ROWS = CL_CTAS * CL_MAX_SL * 32;
+cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double tol,
+                              cudaStream_t s);
+
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
                         const int32_t *didx, int64_t n, cudaStream_t s);

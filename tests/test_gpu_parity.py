@@ -133,6 +133,26 @@ def test_overlapped_halo_split_bit_identical(n, p, transport):
         check_cg(g, n, 200, 0.0)
 
 
+@pytest.mark.parametrize("small", ["0", "1", "2"])
+@pytest.mark.parametrize("n,fmt", [((10, 10, 10), "sym"), ((10, 10, 10), "seg"),
+                                   ((23, 17, 9), "sym"), ((7, 1, 3), "seg")])
+def test_single_launch_solvers_bit_identical(n, fmt, small):
+    """MINIFE_SMALL=1 one-CTA solver, 2 one-cluster solver (DSMEM),
+    0 the three-kernel graph -- each bitwise the oracle (subprocess: the selection is read
+    once per process)."""
+    import os
+    import subprocess
+    import sys
+    if small == "1" and (n[0] + 1) * (n[1] + 1) * (n[2] + 1) > 2048:
+        pytest.skip("one-CTA solver holds <= 2048 rows")
+    env = dict(os.environ, MINIFE_SMALL=small)
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
+                          *map(str, n), fmt], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 def test_plan_on_device_matches_host_plan():
     n, p = (12, 11, 10), 8
     with M.Minife(*n, virtual=p) as g:
