@@ -148,6 +148,10 @@ __device__ void element_operator(int nx, int ny, int nz, double K[8]) {
 // global order b = fl(b - fl(A v)), then A = +0.0.  The pattern (incl. zeros) is kept.
 __global__ void k_assemble(AsmArgs a) {
     const Geom &g = a.g;
+    // C1 once per CTA (24 divisions), shared by its rows
+    __shared__ double sK[8];
+    if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
+    __syncthreads();
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nslices = (g.rows + 31) >> 5;
     if ((row >> 5) >= nslices) return;
@@ -178,7 +182,8 @@ __global__ void k_assemble(AsmArgs a) {
         return sym ? a.val + (14 * s + (t - 13)) * 32 + lane : a.val + (27 * s + t) * 32 + lane;
     };
     double K[8];
-    element_operator(g.nx, g.ny, g.nz, K);
+#pragma unroll
+    for (int d = 0; d < 8; ++d) K[d] = sK[d];
     int lx, ly, lz;
     row_coords(g, row, lx, ly, lz);
     const int ix = g.own_lo[0] + lx, iy = g.own_lo[1] + ly, iz = g.own_lo[2] + lz;
@@ -1961,7 +1966,7 @@ cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width
 
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
     const int64_t threads = ((a.g.rows + 31) >> 5) * 32;
-    k_assemble<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(a);
+    k_assemble<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
