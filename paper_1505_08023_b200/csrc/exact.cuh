@@ -182,6 +182,21 @@ __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int 
     }
 }
 
+// CTA accumulator = 64-bit words (slow path, flag) + 32-bit digit counters (warp flushes):
+// zero both (all threads), and add their sum into a global accumulator (all threads).
+__device__ __forceinline__ void acc_zero_shared(unsigned long long *s, int *dig) {
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = 0ull;
+    for (int i = threadIdx.x; i < ACC_DIG16; i += blockDim.x) dig[i] = 0;
+}
+__device__ __forceinline__ void acc_merge_to_global(const unsigned long long *s, const int *dig,
+                                                    unsigned long long *g) {
+    for (int w = threadIdx.x; w < ACC_WORDS; w += blockDim.x) {
+        long long v = (long long)s[w];
+        if (w < ACC_DIGITS) v += (long long)dig[2 * w] + (long long)dig[2 * w + 1] * 65536ll;
+        if (v) atomicAdd(&g[w], (unsigned long long)v);
+    }
+}
+
 // acc[w] += dig[2w] + 2^16 dig[2w+1] (one warp), then dig = 0
 __device__ __forceinline__ void digits_to_words(int *dig, unsigned long long *acc) {
     for (int w = threadIdx.x & 31; w < ACC_DIGITS; w += 32) {

@@ -265,9 +265,10 @@ __global__ void k_assemble(AsmArgs a) {
 template <bool DOT, bool IDENT>
 __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     if (DOT) {
         if (a.st && a.st->done) return;
-        acc_zero_shared(sacc);
+        acc_zero_shared(sacc, sdig);
         if (blockIdx.x == 0 && a.acc_zero)
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
         __syncthreads();
@@ -319,9 +320,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
         }
     }
     if (DOT) {
-        ex.warp_flush(sacc);
+        expansion_flush_digits(ex, sdig, sacc);
         __syncthreads();
-        acc_merge_to_global(sacc, a.acc);
+        acc_merge_to_global(sacc, sdig, a.acc);
     }
 }
 
@@ -331,9 +332,10 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_crs(SpmvArgs a) {
 template <bool DOT>
 __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_seg(SpmvArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     if (DOT) {
         if (a.st && a.st->done) return;
-        acc_zero_shared(sacc);
+        acc_zero_shared(sacc, sdig);
         if (blockIdx.x == 0 && a.acc_zero)
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
         __syncthreads();
@@ -372,9 +374,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_seg(SpmvArgs a) {
         }
     }
     if (DOT) {
-        ex.warp_flush(sacc);
+        expansion_flush_digits(ex, sdig, sacc);
         __syncthreads();
-        acc_merge_to_global(sacc, a.acc);
+        acc_merge_to_global(sacc, sdig, a.acc);
     }
 }
 
@@ -458,6 +460,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     __shared__ unsigned long long s_in[FUSED ? ACC_WORDS : 1];
     __shared__ double s_beta, s_alpha_prev;
     __shared__ int s_stop;
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
         }
     }
     if (DOT) {
-        acc_zero_shared(sacc);
+        acc_zero_shared(sacc, sdig);
         if (blockIdx.x == 0 && a.acc_zero)
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     }
@@ -611,11 +614,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
-        if (DOT) ex.warp_flush(sacc);
+        if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
     if (DOT) {
         __syncthreads();
-        acc_merge_to_global(sacc, a.acc);
+        acc_merge_to_global(sacc, sdig, a.acc);
     }
 }
 
@@ -643,6 +646,7 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[SY_STAGES], empty_bar[SY_STAGES];
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     if (DOT && a.st && a.st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (DOT) {
-        acc_zero_shared(sacc);
+        acc_zero_shared(sacc, sdig);
         if (blockIdx.x == 0 && a.acc_zero)
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     }
@@ -727,11 +731,11 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
-        if (DOT) ex.warp_flush(sacc);
+        if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
     if (DOT) {
         __syncthreads();
-        acc_merge_to_global(sacc, a.acc);
+        acc_merge_to_global(sacc, sdig, a.acc);
     }
 }
 
@@ -778,6 +782,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST];
     __shared__ unsigned long long sacc[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     if (DOT && a.st && a.st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (DOT) {
-        acc_zero_shared(sacc);
+        acc_zero_shared(sacc, sdig);
         if (blockIdx.x == 0 && a.acc_zero)
             for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     }
@@ -876,11 +881,11 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
-        if (DOT) ex.warp_flush(sacc);
+        if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
     if (DOT) {
         __syncthreads();
-        acc_merge_to_global(sacc, a.acc);
+        acc_merge_to_global(sacc, sdig, a.acc);
     }
 }
 
@@ -891,7 +896,8 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
-    acc_zero_shared(sacc);
+    __shared__ int sdig[ACC_DIG16];
+    acc_zero_shared(sacc, sdig);
     __syncthreads();
     Expansion ex;
     ex.init();
@@ -903,9 +909,9 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
         a.p[IDENT ? i : row_to_col(a.g, i)] = bi;
         ex.add(__dmul_rn(bi, bi), sacc);
     }
-    ex.warp_flush(sacc);
+    expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
-    acc_merge_to_global(sacc, a.acc_out);
+    acc_merge_to_global(sacc, sdig, a.acc_out);
 }
 
 // C6 step 1 decisions: rr_0, hist[0] = sqrt(rr_0), stop threshold fl(tol hist[0]) (one thread)
@@ -1021,10 +1027,11 @@ __device__ __forceinline__ void r_step(double &r, double ap, double alpha, Expan
 template <bool IDENT, bool XL>
 __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) {
     __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     __shared__ double s_alpha;
     __shared__ int s_stop;
     if (a.st->done) return;
-    acc_zero_shared(sacc);
+    acc_zero_shared(sacc, sdig);
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
@@ -1110,9 +1117,9 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
             a.r[i] = ri;
         }
     }
-    ex.warp_flush(sacc);
+    expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
-    acc_merge_to_global(sacc, a.acc_out);
+    acc_merge_to_global(sacc, sdig, a.acc_out);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1574,10 +1581,11 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
 __global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
                                                           unsigned long long *acc_pAp_next) {
     __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
+    __shared__ int sdig[ACC_DIG16];
     __shared__ double s_alpha;
     __shared__ int s_stop;
     if (a.st->done) return;
-    acc_zero_shared(sacc);
+    acc_zero_shared(sacc, sdig);
     acc_load_shared(s_in, a.acc_in);
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
@@ -1630,7 +1638,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
     ex[0].warp_flush(sacc);
     ex[1].warp_flush(sacc);
     __syncthreads();
-    acc_merge_to_global(sacc, a.acc_out);
+    acc_merge_to_global(sacc, sdig, a.acc_out);
 }
 
 // After the last iteration K: finalise rr_K (hist[K], stop flags) unless a stop test already
@@ -1865,16 +1873,17 @@ __global__ void __launch_bounds__(UPD_THREADS) k_dot(const double *__restrict__ 
                                                      const double *__restrict__ v, int64_t n,
                                                      unsigned long long *acc) {
     __shared__ unsigned long long sacc[ACC_WORDS];
-    acc_zero_shared(sacc);
+    __shared__ int sdig[ACC_DIG16];
+    acc_zero_shared(sacc, sdig);
     __syncthreads();
     Expansion ex;
     ex.init();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         ex.add(__dmul_rn(u[i], v[i]), sacc);
-    ex.warp_flush(sacc);
+    expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
-    acc_merge_to_global(sacc, acc);
+    acc_merge_to_global(sacc, sdig, acc);
 }
 
 // *out = RN(value of the accumulator), one warp.

@@ -93,6 +93,19 @@ def test_single_gpu_matrix_spmv_cg(n, fmt):
         check_cg(g, n, 7, 0.0)          # graph re-capture with another iteration count
 
 
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
+@pytest.mark.parametrize("n", [(800, 3, 3), (3, 3, 800), (2, 900, 2), (61, 1, 97)])
+def test_elongated_meshes(n, fmt):
+    """Lines much longer / shorter than a tile (SYM mirror boxes, segment runs, SELL tails)
+    and too many rows for the single-launch solvers: the multi-kernel path."""
+    s = oracle_system(n)
+    with M.Minife(*n, fmt=fmt) as g:
+        g.assemble()
+        check_matrix(g, s)
+        check_spmv(g, s, 2)
+        check_cg(g, n, 200, 0.0)
+
+
 @pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
                                  ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4)])
