@@ -1049,11 +1049,26 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t rows = a.g.rows;
     if (XL) {
-        // r -= alpha Ap, exact rr (16-byte accesses, two pairs in flight per thread)
+        // r -= alpha Ap, exact rr (16-byte accesses, four pairs in flight per thread: K6
+        // moves only 24 B per row, so it needs the deeper queue to cover DRAM latency)
         const int64_t n2 = rows >> 1;
         double2 *r2 = reinterpret_cast<double2 *>(a.r);
         const double2 *q2 = reinterpret_cast<const double2 *>(a.Ap);
         int64_t i = tid;
+        for (; i + 3 * stride < n2; i += 4 * stride) {
+            double2 rv[4], qv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                rv[u] = r2[i + u * stride];
+                qv[u] = q2[i + u * stride];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                r_step(rv[u].x, qv[u].x, alpha, ex, sacc);
+                r_step(rv[u].y, qv[u].y, alpha, ex, sacc);
+                r2[i + u * stride] = rv[u];
+            }
+        }
         for (; i + stride < n2; i += 2 * stride) {
             double2 ra = r2[i], qa = q2[i], rb = r2[i + stride], qb = q2[i + stride];
             r_step(ra.x, qa.x, alpha, ex, sacc);
