@@ -50,12 +50,13 @@ extern "C" {
 #define MINIFE_FMT_SEG 1       /* SELL-32, 27 value slots per row + one int32 start column per
                                   x-run ("non-zero segment") + a 27-bit presence mask: the
                                   paper's BCRS (Fig 3.2) on the GPU; 8 B per entry
-                                  + 4 B per segment.  Default of multi-part ctxs.             */
+                                  + 4 B per segment.                                          */
 #define MINIFE_FMT_SYM 2       /* MINIFE_FMT_SEG storing only the upper-triangle value slots
                                   (14 per row incl. the diagonal); a lower entry a_ij is read
                                   from row j's mirror slot (a_ij == a_ji bitwise: the assembled
-                                  system is exactly symmetric, C2/C3).  Single-part ctxs only
-                                  (their default); results identical to the other formats.    */
+                                  system is exactly symmetric, C2/C3).  Default.  With a halo
+                                  the storage covers the extended box: halo nodes are ghost
+                                  rows holding the mirrors.  Results identical to the others. */
 
 /* ---- CG iteration schemes ------------------------------------------------- */
 #define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | r update + rr | x and p update   */
@@ -168,8 +169,7 @@ const char *minife_last_error(const minife_ctx *ctx);
 
 /* ---- the hot path ---------------------------------------------------------------------- */
 
-/* Select the storage format used by the next minife_assemble (default: MINIFE_FMT_SYM for a
- * single-part ctx, MINIFE_FMT_SEG otherwise; SYM is refused for multi-part ctxs).  The
+/* Select the storage format used by the next minife_assemble (default MINIFE_FMT_SYM).  The
  * ctx becomes unassembled.  Results are bit-identical in both formats (same values, same
  * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
 int minife_set_format(minife_ctx *ctx, int format);

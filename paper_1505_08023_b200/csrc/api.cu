@@ -98,6 +98,7 @@ struct Part {
     // halo: send_col = extended columns of the send lists (neighbor order), recv_pos =
     // extended column of each halo slot; wire buffers
     int32_t *d_send_col = nullptr, *d_recv_pos = nullptr;
+    int32_t *d_send_row = nullptr;                // send lists as local rows (SYM pre-pack)
     double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
     // SEG slice storage order (multi-part): interior slices [0, n_int) first, DESIGN.md §7
     int32_t *d_slice_row = nullptr, *d_slice_pos = nullptr;
@@ -236,7 +237,8 @@ static void free_part(Part &p) {
     void *bufs[] = {p.d_slice_off, p.d_row_len, p.d_width,   p.d_b,        p.d_x,
                     p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
-                    p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos};
+                    p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
+                    p.d_send_row};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
@@ -307,6 +309,11 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     for (size_t i = 0; i < plan.send_idx.size(); ++i)
         send_col[i] = (int32_t)plan.row_to_col(plan.send_idx[i]);
     for (int64_t i = 0; i < plan.n_ext; ++i) recv_pos[i] = (int32_t)plan.ext_pos[i];
+    std::vector<int32_t> send_row(plan.send_idx.begin(), plan.send_idx.end());
+    TRY(dalloc(c, p, &p.d_send_row, send_row.size()));
+    if (!send_row.empty())
+        CUDA_TRY(c, cudaMemcpy(p.d_send_row, send_row.data(), 4 * send_row.size(),
+                               cudaMemcpyHostToDevice));
     TRY(dalloc(c, p, &p.d_send_col, send_col.size()));
     TRY(dalloc(c, p, &p.d_sendbuf, send_col.size()));
     TRY(dalloc(c, p, &p.d_recv_pos, recv_pos.size()));
@@ -364,10 +371,9 @@ static int create_common(minife_ctx *c, int nx, int ny, int nz, int nparts,
         }
         TRY(setup_part(c, c->parts[q], devs[q], plan));
     }
-    // default format: SYM where the mirror rows are local (one part, rows == columns),
-    // else SEG (B200, 300^3: SYM SpMV 0.90 ms vs SEG 1.07 ms; profiles/r01/session2)
-    c->fmt = (nparts == 1 && c->world == 1 && c->parts[0].ncols == c->parts[0].rows)
-                 ? MINIFE_FMT_SYM : MINIFE_FMT_SEG;
+    // default format: SYM (B200, 300^3: SYM SpMV 0.88 ms vs SEG 1.07 ms; with a halo the
+    // halo nodes are stored as ghost rows, profiles/r01/session2)
+    c->fmt = MINIFE_FMT_SYM;
     DevGuard g(c->parts[0].dev);
     CUDA_TRY(c, cudaEventCreate(&c->ev0));
     CUDA_TRY(c, cudaEventCreate(&c->ev1));
@@ -514,10 +520,7 @@ extern "C" int minife_set_scheme(minife_ctx *c, int scheme) {
 extern "C" int minife_set_format(minife_ctx *c, int format) {
     if (!c || (format != MINIFE_FMT_CRS && format != MINIFE_FMT_SEG && format != MINIFE_FMT_SYM))
         return MINIFE_EINVAL;
-    if (format == MINIFE_FMT_SYM && !(c->parts.size() == 1 && c->parts[0].ncols == c->parts[0].rows)) {
-        set_err(c, "MINIFE_FMT_SYM needs a single part (mirror rows must be local)");
-        return MINIFE_EINVAL;
-    }
+
     if (format != c->fmt) {
         c->fmt = format;
         c->assembled = false;
@@ -610,11 +613,19 @@ extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
 // assembly (a0.2 - a0.5)
 // ----------------------------------------------------------------------------------------
 
+// SYM storage: by extended column (ghost rows for the halo nodes) -- slices over ncols
+static int64_t sym_slices(const Part &p) { return (p.ncols + 31) / 32; }
+
 static Matrix matrix_of(const minife_ctx *c, const Part &p) {
     Matrix m{};
     m.fmt = c->fmt;
     m.rows = p.rows;
     m.nslices = p.nslices;
+    if (c->fmt == MINIFE_FMT_SYM) {
+        m.ext = p.ncols != p.rows;
+        m.rows = p.ncols;
+        m.nslices = sym_slices(p);
+    }
     m.val = p.d_val;
     m.slice_off = p.d_slice_off;
     m.row_len = p.d_row_len;
@@ -658,16 +669,18 @@ extern "C" int minife_assemble(minife_ctx *c) {
                                         cudaMemcpyHostToDevice, s));
             CUDA_TRY(c, cudaStreamSynchronize(s));
         } else {
-            // SEG: 27 value slots per row; SYM: the 14 upper slots
-            const int64_t entries = (c->fmt == MINIFE_FMT_SYM ? 14 : 27) * 32 * p.nslices;
+            // SEG: 27 value slots per row; SYM: the 14 upper slots, stored for every node of
+            // the extended box (ghost rows for the halo nodes; = the rows with one part)
+            const bool sym = c->fmt == MINIFE_FMT_SYM;
+            const int64_t ns = sym ? sym_slices(p) : p.nslices;
+            const int64_t entries = (sym ? 14 : 27) * 32 * ns;
             if (!p.d_seg || entries != p.entries) {
                 free_matrix(p);
                 TRY(dalloc(c, p, &p.d_val, entries));
                 const size_t vbytes = 8 * (size_t)entries;
-                TRY(dalloc(c, p, &p.d_seg, 9 * 32 * p.nslices));
-                TRY(dalloc(c, p, &p.d_mask, 32 * p.nslices));   // padded: whole-slice copies
-                p.matrix_bytes = vbytes + 4 * (size_t)(9 * 32 * p.nslices) +
-                                 4 * (size_t)(32 * p.nslices);
+                TRY(dalloc(c, p, &p.d_seg, 9 * 32 * ns));
+                TRY(dalloc(c, p, &p.d_mask, 32 * ns));           // padded: whole-slice copies
+                p.matrix_bytes = vbytes + 4 * (size_t)(9 * 32 * ns) + 4 * (size_t)(32 * ns);
                 p.entries = entries;
             }
         }
@@ -697,15 +710,17 @@ extern "C" int minife_assemble(minife_ctx *c) {
 
 // Fill the halo (shell) columns of vec(part) from the owners' owned values.
 // comm = true: on the transport streams (cstream) instead of the compute streams.
+// prepacked = true: the send buffers already hold the values (k_pack_next_p); the wire
+// protocol is used in every mode.
 template <class VecOf>
-static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false) {
+static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepacked = false) {
     if (c->world == 1) return MINIFE_OK;
     // stream of part p's work: VIRTUAL ctxs use part 0's queue for every part
     auto sp = [&](Part &p) -> cudaStream_t {
         Part &q = c->mode == MINIFE_MODE_VIRTUAL ? c->parts[0] : p;
         return comm ? q.cstream : (c->mode == MINIFE_MODE_VIRTUAL ? q.stream : stream_of(c, q));
     };
-    if (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_DIRECT) {
+    if (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_DIRECT && !prepacked) {
         // device-local transport: read the owner's columns through its send list, write the
         // receiver's halo columns
         cudaStream_t s = sp(c->parts[0]);
@@ -724,6 +739,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false) {
     }
     // wire protocol: pack each part's send lists, exchange per neighbor, unpack the slots
     for (auto &p : c->parts) {
+        if (prepacked) break;
         DevGuard g(p.dev);
         CUDA_TRY(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
                                 (int64_t)p.plan.send_idx.size(), sp(p)));
@@ -829,7 +845,7 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     a.acc_zero = dot ? p.acc_rr() : nullptr;
     a.st = dot ? p.d_st : nullptr;
     a.s_begin = 0;
-    a.s_end = p.nslices;
+    a.s_end = a.m.nslices;
     return a;
 }
 
@@ -837,6 +853,45 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
 // runs (SEG, more than one part); the boundary slices follow once it has landed.
 static bool overlap_mode(const minife_ctx *c) {
     return c->fmt == MINIFE_FMT_SEG && c->world > 1 && c->parts[0].cstream;
+}
+
+// SYM with a halo: the values p_(k+1) sends are computed ahead of K7 (k_pack_next_p); their
+// exchange runs on the transport streams while K7 updates p, so the SpMV finds the halo in
+// place.  (SYM stores rows by extended column, so the slices are not reordered.)
+static bool overlap_sym(const minife_ctx *c) {
+    return c->fmt == MINIFE_FMT_SYM && c->world > 1 && c->parts[0].cstream;
+}
+
+static int enqueue_k7_with_halo(minife_ctx *c, int k) {
+    const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        UpdArgs a = upd_args(c, p, 1);
+        CUDA_TRY(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
+                                       (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
+    }
+    for (auto &p : c->parts) {
+        if (virt && &p != &c->parts[0]) break;
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaEventRecord(p.ev_fork, launch_stream(c, p)));
+        CUDA_TRY(c, cudaStreamWaitEvent(p.cstream, p.ev_fork, 0));
+    }
+    TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }, true, true));
+    for (auto &p : c->parts) {
+        if (virt && &p != &c->parts[0]) break;
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaEventRecord(p.ev_join, p.cstream));
+    }
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+    }
+    for (auto &p : c->parts) {
+        if (virt && &p != &c->parts[0]) break;
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaStreamWaitEvent(launch_stream(c, p), p.ev_join, 0));
+    }
+    return MINIFE_OK;
 }
 
 struct PhaseTimer {
@@ -908,8 +963,15 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
 }
 
 static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
+    const bool osym = overlap_sym(c) && !t;
     if (overlap_mode(c) && !t) {
         TRY(enqueue_halo_spmv_overlapped(c));
+    } else if (osym) {                               // halo already in place (previous K7)
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+                                    launch_stream(c, p)));
+        }
     } else {
         TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
         if (t) t->mark(3);
@@ -929,9 +991,13 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     if (t) t->mark(1);
     TRY(enqueue_allreduce(c, 1));
     if (t) t->mark(3);
-    for (auto &p : c->parts) {
-        DevGuard g(p.dev);
-        CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+    if (osym) {
+        TRY(enqueue_k7_with_halo(c, k));
+    } else {
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+        }
     }
     if (t) t->mark(2);
     return MINIFE_OK;
@@ -1026,6 +1092,7 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
     }
     const bool fused = fused_mode(c);
     TRY(enqueue_init(c, tol));
+    if (!t && overlap_sym(c)) TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));  // p_1 = b
     if (t) t->mark(-1);
     for (int k = 1; k <= max_iters; ++k)
         TRY(fused ? enqueue_iteration_fused(c, k, t) : enqueue_iteration(c, k, t));
@@ -1362,7 +1429,8 @@ static int extract_part_rows(minife_ctx *c, Part &p, const std::vector<int64_t> 
         const int64_t n = std::min(chunk, k - b);
         cudaError_t e = cudaMemcpy(d_rows, loc.data() + b, 8 * n, cudaMemcpyHostToDevice);
         if (e == cudaSuccess)
-            e = launch_extract_rows(matrix_of(c, p), d_rows, n, d_oc, d_ov, d_ol, p.stream);
+            e = launch_extract_rows(matrix_of(c, p), geom_of(c, p), d_rows, n, d_oc, d_ov, d_ol,
+                                    p.stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(p.stream);
         if (e == cudaSuccess)
             e = cudaMemcpy(oc.data() + 27 * b, d_oc, 4 * 27 * n, cudaMemcpyDeviceToHost);

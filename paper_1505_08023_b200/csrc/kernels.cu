@@ -84,6 +84,19 @@ __device__ __forceinline__ void row_coords(const Geom &g, int64_t l, int &lx, in
     lz = (int)plane;
 }
 
+// extended-box column c -> owned row, or -1 for a halo node
+__device__ __forceinline__ int64_t col_to_row(const Geom &g, int64_t c) {
+    const unsigned u = (unsigned)c;
+    const unsigned line = u / (unsigned)g.ext_n[0];
+    const int ex = (int)(u - line * (unsigned)g.ext_n[0]);
+    const unsigned plane = line / (unsigned)g.ext_n[1];
+    const int ey = (int)(line - plane * (unsigned)g.ext_n[1]), ez = (int)plane;
+    const int lx = ex - g.off[0], ly = ey - g.off[1], lz = ez - g.off[2];
+    if (lx < 0 || lx >= g.own_n[0] || ly < 0 || ly >= g.own_n[1] || lz < 0 || lz >= g.own_n[2])
+        return -1;
+    return (int64_t)lx + (int64_t)g.own_n[0] * ((int64_t)ly + (int64_t)g.own_n[1] * lz);
+}
+
 // owned row l -> extended-box column
 __device__ __forceinline__ int64_t row_to_col(const Geom &g, int64_t l) {
     int lx, ly, lz;
@@ -250,6 +263,81 @@ __global__ void k_assemble(AsmArgs a) {
     }
     if (row_bc) b = (ix == g.nx) ? 1.0 : 0.0;
     a.b[row] = b;
+}
+
+// a0.2-a0.5 for FMT_SYM on a part with a halo: one thread per EXTENDED-box node (storage
+// row = its column).  Same C1-C3 arithmetic as k_assemble; only the upper slots t >= 13 are
+// stored.  A halo (ghost) node gets its upper entries towards nodes inside the extended box
+// -- exactly the mirrors the owned rows read; slots leaving the extended box are absent.
+// mask bit 31 marks owned nodes; b is written for owned rows only.
+__global__ void k_assemble_symx(AsmArgs a) {
+    const Geom &g = a.g;
+    __shared__ double sK[8];
+    if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
+    __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nslices = (g.ncols + 31) >> 5;
+    if ((c >> 5) >= nslices) return;
+    const int lane = (int)(c & 31);
+    const int64_t s = c >> 5;
+    if (c >= g.ncols) {                            // padding lanes of the last slice
+        for (int t = 0; t < 14; ++t) a.val[(14 * s + t) * 32 + lane] = 0.0;
+        for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
+        a.mask[c] = 0u;
+        return;
+    }
+    double K[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) K[d] = sK[d];
+    const unsigned u = (unsigned)c;
+    const unsigned line = u / (unsigned)g.ext_n[0];
+    const int ex = (int)(u - line * (unsigned)g.ext_n[0]);
+    const unsigned plane = line / (unsigned)g.ext_n[1];
+    const int ey = (int)(line - plane * (unsigned)g.ext_n[1]), ez = (int)plane;
+    const int ix = g.ext_lo[0] + ex, iy = g.ext_lo[1] + ey, iz = g.ext_lo[2] + ez;
+    const int64_t row = col_to_row(g, c);
+    const bool row_bc = on_boundary(ix, iy, iz, g.nx, g.ny, g.nz);
+    const int n_el[3] = {(ix > 0) + (ix < g.nx), (iy > 0) + (iy < g.ny), (iz > 0) + (iz < g.nz)};
+    double b = 0.0;
+    uint32_t mask = row >= 0 ? SYM_OWNED : 0u;
+    for (int dz = -1; dz <= 1; ++dz) {
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int jgrp = (dz + 1) * 3 + (dy + 1);
+            const int jy = iy + dy, jz = iz + dz;
+            const bool grp_in = jy >= 0 && jy <= g.ny && jz >= 0 && jz <= g.nz;
+            const int64_t start = (int64_t)(ex - 1) +
+                                  (int64_t)g.ext_n[0] * ((int64_t)(ey + dy) +
+                                                         (int64_t)g.ext_n[1] * (ez + dz));
+            a.seg[(9 * s + jgrp) * 32 + lane] = grp_in ? (int32_t)start : 0;
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int t = jgrp * 3 + (dx + 1);
+                const int jx = ix + dx;
+                // inside the domain AND inside the extended box (ghost rows stop at its edge)
+                const bool in = grp_in && jx >= 0 && jx <= g.nx && ex + dx >= 0 &&
+                                ex + dx < g.ext_n[0] && ey + dy >= 0 && ey + dy < g.ext_n[1] &&
+                                ez + dz >= 0 && ez + dz < g.ext_n[2];
+                if (!in) {
+                    if (t >= 13) a.val[(14 * s + (t - 13)) * 32 + lane] = 0.0;
+                    continue;
+                }
+                const int cnt = (dx ? 1 : n_el[0]) * (dy ? 1 : n_el[1]) * (dz ? 1 : n_el[2]);
+                const double Kd = K[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)];
+                double v = 0.0;
+                for (int q = 0; q < cnt; ++q) v = __dadd_rn(v, Kd);
+                if (row_bc) {
+                    v = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
+                } else if (on_boundary(jx, jy, jz, g.nx, g.ny, g.nz)) {
+                    const double bv = (jx == g.nx) ? 1.0 : 0.0;
+                    b = __dsub_rn(b, __dmul_rn(v, bv));
+                    v = 0.0;
+                }
+                if (t >= 13) a.val[(14 * s + (t - 13)) * 32 + lane] = v;
+                mask |= 1u << t;
+            }
+        }
+    }
+    a.mask[c] = mask;
+    if (row >= 0) a.b[row] = row_bc ? ((ix == g.nx) ? 1.0 : 0.0) : b;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -632,6 +720,18 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
 // warps per SM keep the mirrored and x reads in flight.
 // ----------------------------------------------------------------------------------------
 
+// SYM storage row c -> computed row (or -1); clears the presence bits of a ghost row
+__device__ __forceinline__ int64_t sym_row(const Matrix &m, const Geom &g, int64_t c,
+                                           unsigned &msk) {
+    if (!m.ext) return c < m.rows ? c : -1;
+    if (!(msk & SYM_OWNED)) {
+        msk = 0u;
+        return -1;
+    }
+    msk &= ~SYM_OWNED;
+    return col_to_row(g, c);
+}
+
 template <int NW, int NST> struct SyCfg {                     // NW slices per tile = consumers
     static constexpr int TILE = NW, THREADS = 32 * (NW + 1), STAGES = NST;
     static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
@@ -699,9 +799,10 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
                 const double *vs = reinterpret_cast<const double *>(buf) + warp * 14 * 32 + lane;
                 const int32_t *ss =
                     reinterpret_cast<const int32_t *>(buf + SY_VAL_B) + warp * 9 * 32 + lane;
-                const unsigned msk =
+                unsigned msk =
                     reinterpret_cast<const uint32_t *>(buf + SY_VAL_B + SY_SEG_B)[warp * 32 + lane];
-                const int64_t row = s * 32 + lane;
+                // storage row s*32+lane; SYM-ext: only owned nodes are computed rows
+                const int64_t row = sym_row(m, a.g, s * 32 + lane, msk);
                 int sg[9];
 #pragma unroll
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
@@ -723,7 +824,7 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
 #pragma unroll
                 for (int t = 13; t < 27; ++t)
                     if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
-                if (row < m.rows) {
+                if (row >= 0) {
                     a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);
                 }
@@ -844,10 +945,11 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 const double *vs = reinterpret_cast<const double *>(buf) + warp * 14 * 32 + lane;
                 const int32_t *ss =
                     reinterpret_cast<const int32_t *>(buf + C::VAL_B) + warp * 9 * 32 + lane;
-                const unsigned msk =
+                unsigned msk =
                     reinterpret_cast<const uint32_t *>(buf + C::VAL_B + C::SEG_B)[warp * 32 + lane];
                 const double *mir = reinterpret_cast<const double *>(buf + C::MIR0);
-                const int64_t row = s * 32 + lane;
+                // storage row s*32+lane; SYM-ext: only owned nodes are computed rows
+                const int64_t row = sym_row(m, a.g, s * 32 + lane, msk);
                 const int64_t r0 = tile * NW * 32;
                 int sg[9];
 #pragma unroll
@@ -873,7 +975,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 #pragma unroll
                 for (int t = 13; t < 27; ++t)
                     if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
-                if (row < m.rows) {
+                if (row >= 0) {
                     a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);
                 }
@@ -1587,6 +1689,29 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     }
 }
 
+// Halo values of p_(k+1) computed ahead of K7 (SYM with a halo): the packed
+// send buffer gets sendbuf[i] = fl(r[row_i] + fl(beta_k p_k[col_i])) -- K7's formula on K7's
+// inputs, beta_k from the same exact rr -- so the exchange can run while K7 updates p.
+__global__ void __launch_bounds__(UPD_THREADS) k_pack_next_p(UpdArgs a, int k,
+                                                             const int32_t *send_row,
+                                                             const int32_t *send_col,
+                                                             double *sendbuf, int64_t n) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    __shared__ double s_beta;
+    if (a.st->done) return;
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const double rr_new = acc_finalize_warp(s_in);
+        if (threadIdx.x == 0) s_beta = __ddiv_rn(rr_new, a.rr[k - 1]);   // as rr_decision
+    }
+    __syncthreads();
+    const double beta = s_beta;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        sendbuf[i] = __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, a.p[send_col[i]]));
+}
+
 // ----------------------------------------------------------------------------------------
 // fused scheme, second kernel of iteration k (K6'): alpha_k, r -= alpha Ap, exact rr_k.
 // x is not touched here (its update for iteration k is applied by the next fused SpMV or by
@@ -1910,14 +2035,16 @@ __global__ void k_acc_round(const unsigned long long *acc, double *out) {
     if (threadIdx.x == 0) *out = v;
 }
 
-__global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t *out_col,
-                               double *out_val, int32_t *out_len) {
+__global__ void k_extract_rows(Matrix m, Geom g, const int64_t *rows, int64_t n,
+                               int32_t *out_col, double *out_val, int32_t *out_len) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t row = rows[i];
-    const int64_t lane = row & 31;
-    const int64_t s = (m.fmt != FMT_CRS && m.slice_pos) ? (int64_t)m.slice_pos[row >> 5]
-                                                        : (row >> 5);   // storage slice
+    // storage row: SYM-ext stores rows by extended column
+    const int64_t srow = m.ext ? row_to_col(g, row) : row;
+    const int64_t lane = srow & 31;
+    const int64_t s = (m.fmt != FMT_CRS && m.slice_pos) ? (int64_t)m.slice_pos[srow >> 5]
+                                                        : (srow >> 5);   // storage slice
     int len = 0;
     if (m.fmt == FMT_CRS) {
         len = m.row_len[row];
@@ -1926,7 +2053,7 @@ __global__ void k_extract_rows(Matrix m, const int64_t *rows, int64_t n, int32_t
             out_val[27 * i + k] = m.val[m.slice_off[s] + 32 * k + lane];
         }
     } else {
-        const unsigned msk = m.mask[s * 32 + lane];
+        const unsigned msk = m.mask[s * 32 + lane] & ~SYM_OWNED;
         for (int t = 0; t < 27; ++t) {
             if (!((msk >> t) & 1u)) continue;
             const int c = m.seg[(9 * s + t / 3) * 32 + lane] + t % 3;
@@ -1989,6 +2116,11 @@ cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width
 }
 
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
+    if (a.fmt == FMT_SYM && !a.g.ident) {
+        const int64_t threads = ((a.g.ncols + 31) >> 5) * 32;
+        k_assemble_symx<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     const int64_t threads = ((a.g.rows + 31) >> 5) * 32;
     k_assemble<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
     return cudaGetLastError();
@@ -2114,7 +2246,6 @@ cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t
         return launch_tma<true, FMT_SEG, true, true>(a, s);
     }
     if (a.m.fmt == FMT_SYM) {
-        if (!a.g.ident) return cudaErrorInvalidValue;        // one part only
         return with_dot ? launch_sym<true>(a, s) : launch_sym<false>(a, s);
     }
     if (spmv_impl(a.m.fmt) == 1) {
@@ -2188,6 +2319,15 @@ cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double t
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, m, a, K, tol);
+}
+
+cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
+                               const int32_t *send_col, double *sendbuf, int64_t n,
+                               cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
+    k_pack_next_p<<<g, UPD_THREADS, 0, s>>>(a, k, send_row, send_col, sendbuf, n);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s) {
@@ -2270,11 +2410,11 @@ cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
+cudaError_t launch_extract_rows(const Matrix &m, const Geom &g, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,
                                 cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    k_extract_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(m, rows, n, out_col, out_val,
+    k_extract_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(m, g, rows, n, out_col, out_val,
                                                                out_len);
     return cudaGetLastError();
 }

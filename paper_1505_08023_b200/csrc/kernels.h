@@ -57,7 +57,14 @@ struct Matrix {
     // and mask are indexed by storage position, vectors by row.
     const int32_t *slice_row;
     const int32_t *slice_pos;
+    // SYM on a part with a halo (ext = 1): storage covers the EXTENDED box (rows = its ncols
+    // nodes, in column order), so every mirror row is local; halo nodes are ghost rows whose
+    // upper slots are stored but never computed.  mask bit 31 = owned node (computed row).
+    int ext;
 };
+
+// SYM-ext: mask bit of an owned (computed) row
+constexpr unsigned SYM_OWNED = 1u << 31;
 
 struct AsmArgs {
     Geom g;
@@ -135,6 +142,12 @@ constexpr int CL_CTAS = 16, CL_THREADS = 256, CL_WARPS = CL_THREADS / 32, CL_MAX
 cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double tol,
                               cudaStream_t s);
 
+// SYM with a halo: sendbuf[i] = r[send_row[i]] + beta_k p[send_col[i]] (p_(k+1) at the send
+// list, ahead of K7), beta_k from the rr accumulator a.acc_in and a.rr[k-1].
+cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
+                               const int32_t *send_col, double *sendbuf, int64_t n,
+                               cudaStream_t s);
+
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
                         const int32_t *didx, int64_t n, cudaStream_t s);
@@ -147,7 +160,7 @@ cudaError_t launch_dot(const double *u, const double *v, int64_t n, unsigned lon
 cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStream_t s);
 
 // Parity helper: rows[] (local) -> up to 27 (extended column, value) pairs each
-cudaError_t launch_extract_rows(const Matrix &m, const int64_t *rows, int64_t n,
+cudaError_t launch_extract_rows(const Matrix &m, const Geom &g, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,
                                 cudaStream_t s);
 

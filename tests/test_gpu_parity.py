@@ -73,8 +73,8 @@ def check_cg(g, n, iters, tol):
     assert _same(x, o.x)
 
 
-FORMATS = [M.FMT_SEG, M.FMT_CRS]           # every process model
-ALL_FORMATS = FORMATS + [M.FMT_SYM]         # single-part ctxs
+FORMATS = [M.FMT_SEG, M.FMT_CRS]
+ALL_FORMATS = FORMATS + [M.FMT_SYM]         # every process model
 
 
 @pytest.mark.parametrize("fmt", ALL_FORMATS)
@@ -106,7 +106,7 @@ def test_elongated_meshes(n, fmt):
         check_cg(g, n, 200, 0.0)
 
 
-@pytest.mark.parametrize("fmt", FORMATS)
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
                                  ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4)])
 @pytest.mark.parametrize("transport", [0, 1])
@@ -124,19 +124,20 @@ def test_virtual_ranks_bit_identical(n, p, fmt, transport):
         check_cg(g, n, 100, 1e-10)
 
 
+@pytest.mark.parametrize("fmt", [M.FMT_SEG, M.FMT_SYM])
 @pytest.mark.parametrize("n,p", [((40, 8, 6), 2), ((12, 40, 9), 4), ((33, 32, 31), 8)])
 @pytest.mark.parametrize("transport", [0, 1])
-def test_overlapped_halo_split_bit_identical(n, p, transport):
+def test_overlapped_halo_split_bit_identical(n, p, transport, fmt):
     """SEG parts store interior slices first; the interior SpMV runs while the halo
-    is in flight on a second stream, the boundary slices after it lands.  Both launches are
-    non-empty here, and the results are bitwise the oracle's (graph mode and profile mode,
-    which runs the unsplit SpMV)."""
+    is in flight on a second stream, the boundary slices after it lands.  SYM parts compute
+    the halo values of p_(k+1) ahead of K7 and exchange them while K7 runs.  Results are
+    bitwise the oracle's (graph mode and profile mode, which runs the unsplit sequence)."""
     s = oracle_system(n)
-    with M.Minife(*n, virtual=p, fmt=M.FMT_SEG) as g:
+    with M.Minife(*n, virtual=p, fmt=fmt) as g:
         g.set_transport(transport)
         g.assemble()
         parts = [g.part_info(q) for q in range(p)]
-        if p <= 4:     # at p = 8 every slice of these small parts touches an x cut
+        if p <= 4 and fmt == M.FMT_SEG:   # at p = 8 every slice of these parts touches an x cut
             assert any(0 < q.interior_slices < q.slices for q in parts)
         check_matrix(g, s)
         check_spmv(g, s, 1)
@@ -270,7 +271,7 @@ def test_format_switch_keeps_results():
     n = (14, 13, 12)
     s = oracle_system(n)
     with M.Minife(*n) as g:
-        assert g.get_info().format == M.FMT_SYM     # single-part default
+        assert g.get_info().format == M.FMT_SYM     # default
         g.set_format(M.FMT_SEG)
         g.assemble()
         seg_info = g.get_info()
@@ -293,9 +294,10 @@ def test_format_switch_keeps_results():
         check_matrix(g, s)
         check_cg(g, n, 60, 0.0)
     with M.Minife(*n, virtual=2) as g:
-        assert g.get_info().format == M.FMT_SEG     # multi-part default
-        with pytest.raises(M.MinifeError):
-            g.set_format(M.FMT_SYM)
+        assert g.get_info().format == M.FMT_SYM     # default everywhere: ghost rows hold
+        g.assemble()                                # the halo's mirrors
+        check_matrix(g, s)
+        check_cg(g, n, 60, 0.0)
 
 
 @pytest.mark.slow
