@@ -846,6 +846,16 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     a.st = dot ? p.d_st : nullptr;
     a.s_begin = 0;
     a.s_end = a.m.nslices;
+    // SYM value stream evict-first in L2 when the CG vectors (5 x 8 B per row) fit beside it
+    // in the 126 MB L2 and so stay resident across the iteration's kernels (B200, 100^3:
+    // 62.9 -> 60.9 us per iteration); at 300^3 the mirrored reads need the normal policy
+    // (evict-first there: 1.207 -> 1.301 ms).  MINIFE_VAL_EF=0/1 forces it.
+    static int vef = -2;
+    if (vef == -2) {
+        const char *e = getenv("MINIFE_VAL_EF");
+        vef = e ? atoi(e) : -1;
+    }
+    a.val_evict_first = vef >= 0 ? vef : (40.0 * (double)p.ncols < 64e6 ? 1 : 0);
     return a;
 }
 

@@ -909,7 +909,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm1)) : "memory");
             const uint64_t pol = evict_first_policy();
             uint64_t pol_keep;
-            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+            if (a.val_evict_first)
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_keep));
+            else
+                asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
             int64_t i = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
                 const int st = (int)(i % NST);
