@@ -108,7 +108,8 @@ def test_elongated_meshes(n, fmt):
 
 @pytest.mark.parametrize("fmt", ALL_FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
-                                 ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4)])
+                                 ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4),
+                                 ((1, 1, 12), 4), ((12, 1, 1), 3), ((40, 3, 2), 6)])
 @pytest.mark.parametrize("transport", [0, 1])
 def test_virtual_ranks_bit_identical(n, p, fmt, transport):
     """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results.  transport 1
