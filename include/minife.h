@@ -74,6 +74,10 @@ extern "C" {
                                       each neighbor block into the receiver's contiguous
                                       receive buffer (device copies standing in for
                                       ncclSend/ncclRecv), unpack into the halo columns.       */
+#define MINIFE_TRANSPORT_PUSH 2    /* device-initiated: one kernel per
+                                      part stores every send slot straight into the receiver's
+                                      halo column.  MULTI ctxs use it over NVLink when every
+                                      device pair has peer access.                            */
 
 typedef struct minife_ctx minife_ctx;
 

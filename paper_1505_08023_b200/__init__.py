@@ -43,7 +43,7 @@ MINIFE_ENOMEM, MINIFE_ENOTSPD, MINIFE_EDIVERGED, MINIFE_ENODEV = 5, 6, 7, 8
 MODE_SINGLE, MODE_VIRTUAL, MODE_MULTI, MODE_RANK = 0, 1, 2, 3
 FMT_CRS, FMT_SEG, FMT_SYM = 0, 1, 2
 SCHEME_3K, SCHEME_FUSED = 0, 1
-TRANSPORT_DIRECT, TRANSPORT_WIRE = 0, 1
+TRANSPORT_DIRECT, TRANSPORT_WIRE, TRANSPORT_PUSH = 0, 1, 2
 
 
 class minife_part_info(ctypes.Structure):

@@ -99,6 +99,12 @@ struct Part {
     // extended column of each halo slot; wire buffers
     int32_t *d_send_col = nullptr, *d_recv_pos = nullptr;
     int32_t *d_send_row = nullptr;                // send lists as local rows (SYM pre-pack)
+    // push transport: per send slot the neighbor index and the receiver's halo column; per
+    // neighbor the receiver's p (this device's view: local or peer pointer)
+    uint8_t *d_push_nbr = nullptr;
+    int32_t *d_push_dst = nullptr;
+    double **d_push_ptr = nullptr;
+    cudaEvent_t ev_push = nullptr;
     double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
     // SEG slice storage order (multi-part): interior slices [0, n_int) first, DESIGN.md §7
     int32_t *d_slice_row = nullptr, *d_slice_pos = nullptr;
@@ -134,7 +140,8 @@ struct minife_ctx {
     int mode = MINIFE_MODE_SINGLE;
     int fmt = MINIFE_FMT_SEG;
     int scheme = MINIFE_SCHEME_3K;
-    int transport = MINIFE_TRANSPORT_DIRECT;   // VIRTUAL ctxs only
+    int transport = MINIFE_TRANSPORT_DIRECT;   // VIRTUAL ctxs (MULTI: PUSH if peer access)
+    bool push_ready = false;                     // push tables built
     int world = 1, rank = 0;
     std::vector<Part> parts;
     cudaStream_t user_stream = nullptr;
@@ -238,10 +245,11 @@ static void free_part(Part &p) {
                     p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
-                    p.d_send_row};
+                    p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
+    if (p.ev_push) cudaEventDestroy(p.ev_push);
     if (p.ev_fork) cudaEventDestroy(p.ev_fork);
     if (p.ev_join) cudaEventDestroy(p.ev_join);
     if (p.cstream) cudaStreamDestroy(p.cstream);
@@ -342,6 +350,78 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     return MINIFE_OK;
 }
 
+// Push tables (MINIFE_TRANSPORT_PUSH): part p's slot j of its block for neighbor q lands in
+// q's halo slot recv_off_q[p] + j, i.e. q's extended column ext_pos_q[...]; the store goes
+// through q's p array (a peer pointer when q is on another device).
+static int setup_push(minife_ctx *c) {
+    for (auto &p : c->parts) {
+        const size_t ns = p.plan.send_idx.size();
+        std::vector<uint8_t> nb(ns);
+        std::vector<int32_t> dst(ns);
+        std::vector<double *> ptr(p.plan.nbr.size());
+        for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
+            Part &q = c->parts[p.plan.nbr[k]];
+            auto it = std::lower_bound(q.plan.nbr.begin(), q.plan.nbr.end(), p.plan.rank);
+            const size_t kq = (size_t)(it - q.plan.nbr.begin());
+            if (kq >= q.plan.nbr.size() || q.plan.nbr[kq] != p.plan.rank ||
+                q.plan.recv_cnt[kq] != p.plan.send_cnt[k] || k > 255) {
+                set_err(c, "push plan mismatch between parts %d and %d", p.plan.rank, q.plan.rank);
+                return MINIFE_ESTATE;
+            }
+            for (int64_t j = 0; j < p.plan.send_cnt[k]; ++j) {
+                nb[p.plan.send_off[k] + j] = (uint8_t)k;
+                dst[p.plan.send_off[k] + j] = (int32_t)q.plan.ext_pos[q.plan.recv_off[kq] + j];
+            }
+            ptr[k] = q.d_p;
+        }
+        DevGuard g(p.dev);
+        TRY(dalloc(c, p, &p.d_push_nbr, ns));
+        TRY(dalloc(c, p, &p.d_push_dst, ns));
+        TRY(dalloc(c, p, &p.d_push_ptr, ptr.size()));
+        if (ns) {
+            CUDA_TRY(c, cudaMemcpy(p.d_push_nbr, nb.data(), ns, cudaMemcpyHostToDevice));
+            CUDA_TRY(c, cudaMemcpy(p.d_push_dst, dst.data(), 4 * ns, cudaMemcpyHostToDevice));
+        }
+        if (!ptr.empty())
+            CUDA_TRY(c, cudaMemcpy(p.d_push_ptr, ptr.data(), sizeof(double *) * ptr.size(),
+                                   cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_push, cudaEventDisableTiming));
+    }
+    c->push_ready = true;
+    return MINIFE_OK;
+}
+
+// MULTI ctxs: peer access between every device pair -> push transport over NVLink
+static bool enable_peers(minife_ctx *c) {
+    for (auto &a : c->parts)
+        for (auto &b : c->parts) {
+            if (a.dev == b.dev) continue;
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, a.dev, b.dev) != cudaSuccess || !ok) return false;
+            DevGuard g(a.dev);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b.dev, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return false;
+            cudaGetLastError();
+        }
+    return true;
+}
+
+static bool push_mode(const minife_ctx *c) {
+    return c->world > 1 && c->push_ready &&
+           (c->mode == MINIFE_MODE_MULTI ||
+            (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_PUSH));
+}
+
+// MULTI: each part's compute stream waits for its neighbors' push kernels
+static int push_wait(minife_ctx *c) {
+    if (c->mode != MINIFE_MODE_MULTI) return MINIFE_OK;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        for (int q : p.plan.nbr) CUDA_TRY(c, cudaStreamWaitEvent(p.stream, c->parts[q].ev_push, 0));
+    }
+    return MINIFE_OK;
+}
+
 static int validate_mesh(int nx, int ny, int nz) {
     if (nx < 1 || ny < 1 || nz < 1) return MINIFE_EINVAL;
     return MINIFE_OK;
@@ -405,6 +485,7 @@ extern "C" int minife_create(int nx, int ny, int nz, int ngpu, minife_ctx **out)
             for (int q = 0; q < ngpu; ++q) c->parts[q].comm = comms[q];
         }
     }
+    if (st == MINIFE_OK && ngpu > 1 && enable_peers(c)) st = setup_push(c);
     if (st != MINIFE_OK) {
         minife_destroy(c);
         return st;
@@ -423,6 +504,7 @@ extern "C" int minife_create_virtual(int nx, int ny, int nz, int nparts, minife_
     c->world = nparts;
     std::vector<int> devs(nparts, 0);
     int st = create_common(c, nx, ny, nz, nparts, devs, -1);
+    if (st == MINIFE_OK && nparts > 1) st = setup_push(c);
     if (st != MINIFE_OK) {
         minife_destroy(c);
         return st;
@@ -498,7 +580,8 @@ extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
 }
 
 extern "C" int minife_set_transport(minife_ctx *c, int transport) {
-    if (!c || (transport != MINIFE_TRANSPORT_DIRECT && transport != MINIFE_TRANSPORT_WIRE))
+    if (!c || (transport != MINIFE_TRANSPORT_DIRECT && transport != MINIFE_TRANSPORT_WIRE &&
+               transport != MINIFE_TRANSPORT_PUSH))
         return MINIFE_EINVAL;
     if (c->mode != MINIFE_MODE_VIRTUAL) return MINIFE_ESTATE;
     if (transport != c->transport) {
@@ -708,6 +791,27 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // transports: halo exchange (a1) and accumulator all-reduce (a3/a5)
 // ----------------------------------------------------------------------------------------
 
+// Push the halo of p (mode 0: current p; mode 1: p_(k+1) ahead of K7) from every part, then
+// (MULTI) make every part's compute stream wait for its neighbors' pushes.  With mode 1 the
+// waits are placed by the caller after K7 (wait_now = false).
+static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now) {
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        UpdArgs a{};
+        a.p = p.d_p;
+        a.r = p.d_r;
+        a.rr = p.d_rr;
+        a.st = p.d_st;
+        a.acc_in = p.acc_rr();
+        CUDA_TRY(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr,
+                                p.d_push_dst, p.d_push_ptr, (int64_t)p.plan.send_idx.size(),
+                                launch_stream(c, p)));
+        if (c->mode == MINIFE_MODE_MULTI) CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
+    }
+    if (wait_now) return push_wait(c);
+    return MINIFE_OK;
+}
+
 // Fill the halo (shell) columns of vec(part) from the owners' owned values.
 // comm = true: on the transport streams (cstream) instead of the compute streams.
 // prepacked = true: the send buffers already hold the values (k_pack_next_p); the wire
@@ -874,6 +978,14 @@ static bool overlap_sym(const minife_ctx *c) {
 
 static int enqueue_k7_with_halo(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
+    if (push_mode(c)) {                  // device-initiated: p_(k+1) halo stored by the sender
+        TRY(enqueue_push(c, k, 1, false));
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+        }
+        return push_wait(c);
+    }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 1);
@@ -974,7 +1086,7 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
 
 static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     const bool osym = overlap_sym(c) && !t;
-    if (overlap_mode(c) && !t) {
+    if (overlap_mode(c) && !t && !push_mode(c)) {
         TRY(enqueue_halo_spmv_overlapped(c));
     } else if (osym) {                               // halo already in place (previous K7)
         for (auto &p : c->parts) {
@@ -983,7 +1095,8 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
                                     launch_stream(c, p)));
         }
     } else {
-        TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+        if (push_mode(c)) TRY(enqueue_push(c, k, 0, true));
+        else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
         if (t) t->mark(3);
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
@@ -1102,7 +1215,10 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
     }
     const bool fused = fused_mode(c);
     TRY(enqueue_init(c, tol));
-    if (!t && overlap_sym(c)) TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));  // p_1 = b
+    if (!t && overlap_sym(c)) {                      // halo of p_1 = b
+        if (push_mode(c)) TRY(enqueue_push(c, 0, 0, true));
+        else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+    }
     if (t) t->mark(-1);
     for (int k = 1; k <= max_iters; ++k)
         TRY(fused ? enqueue_iteration_fused(c, k, t) : enqueue_iteration(c, k, t));

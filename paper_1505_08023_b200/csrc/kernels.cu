@@ -1715,6 +1715,37 @@ __global__ void __launch_bounds__(UPD_THREADS) k_pack_next_p(UpdArgs a, int k,
         sendbuf[i] = __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, a.p[send_col[i]]));
 }
 
+// a1, device-initiated (MINIFE_TRANSPORT_PUSH): every send slot's value is stored straight
+// into the receiving part's halo column -- another part's array on this GPU (VIRTUAL) or a
+// peer GPU's array over NVLink (MULTI, peer access).  No pack, no wire, no unpack.
+// mode 0: the value is p[send_col]; mode 1: p_(k+1) = fl(r + fl(beta_k p)) as k_pack_next_p.
+__global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode,
+                                                      const int32_t *send_row,
+                                                      const int32_t *send_col,
+                                                      const uint8_t *slot_nbr,
+                                                      const int32_t *dst_col,
+                                                      double *const *dst_ptr, int64_t n) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    __shared__ double s_beta;
+    if (mode == 1) {
+        if (a.st->done) return;
+        acc_load_shared(s_in, a.acc_in);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const double rr_new = acc_finalize_warp(s_in);
+            if (threadIdx.x == 0) s_beta = __ddiv_rn(rr_new, a.rr[k - 1]);   // as rr_decision
+        }
+        __syncthreads();
+    }
+    const double beta = mode == 1 ? s_beta : 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double pv = a.p[send_col[i]];
+        const double v = mode == 1 ? __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, pv)) : pv;
+        dst_ptr[slot_nbr[i]][dst_col[i]] = v;
+    }
+}
+
 // ----------------------------------------------------------------------------------------
 // fused scheme, second kernel of iteration k (K6'): alpha_k, r -= alpha Ap, exact rr_k.
 // x is not touched here (its update for iteration k is applied by the next fused SpMV or by
@@ -2330,6 +2361,16 @@ cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
     if (n <= 0) return cudaSuccess;
     const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
     k_pack_next_p<<<g, UPD_THREADS, 0, s>>>(a, k, send_row, send_col, sendbuf, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_row,
+                        const int32_t *send_col, const uint8_t *slot_nbr, const int32_t *dst_col,
+                        double *const *dst_ptr, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
+    k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, send_row, send_col, slot_nbr, dst_col, dst_ptr,
+                                     n);
     return cudaGetLastError();
 }
 

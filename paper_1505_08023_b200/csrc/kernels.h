@@ -149,6 +149,12 @@ cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
                                const int32_t *send_col, double *sendbuf, int64_t n,
                                cudaStream_t s);
 
+// Halo push (a1, device-initiated): dst_ptr[slot_nbr[i]][dst_col[i]] = value of slot i, with
+// value = p[send_col[i]] (mode 0) or r[send_row[i]] + beta_k p[send_col[i]] (mode 1).
+cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_row,
+                        const int32_t *send_col, const uint8_t *slot_nbr, const int32_t *dst_col,
+                        double *const *dst_ptr, int64_t n, cudaStream_t s);
+
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
                         const int32_t *didx, int64_t n, cudaStream_t s);

@@ -110,10 +110,11 @@ def test_elongated_meshes(n, fmt):
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
                                  ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4),
                                  ((1, 1, 12), 4), ((12, 1, 1), 3), ((40, 3, 2), 6)])
-@pytest.mark.parametrize("transport", [0, 1])
+@pytest.mark.parametrize("transport", [0, 1, 2])
 def test_virtual_ranks_bit_identical(n, p, fmt, transport):
     """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results.  transport 1
-    runs the multi-GPU wire protocol (pack -> per-neighbor receive blocks -> unpack)."""
+    runs the multi-GPU wire protocol (pack -> per-neighbor receive blocks -> unpack), 2 the
+    device-initiated push (each sender stores into the receivers' halo columns)."""
     s = oracle_system(n)
     with M.Minife(*n, virtual=p, fmt=fmt) as g:
         g.set_transport(transport)
@@ -127,7 +128,7 @@ def test_virtual_ranks_bit_identical(n, p, fmt, transport):
 
 @pytest.mark.parametrize("fmt", [M.FMT_SEG, M.FMT_SYM])
 @pytest.mark.parametrize("n,p", [((40, 8, 6), 2), ((12, 40, 9), 4), ((33, 32, 31), 8)])
-@pytest.mark.parametrize("transport", [0, 1])
+@pytest.mark.parametrize("transport", [0, 1, 2])
 def test_overlapped_halo_split_bit_identical(n, p, transport, fmt):
     """SEG parts store interior slices first; the interior SpMV runs while the halo
     is in flight on a second stream, the boundary slices after it lands.  SYM parts compute
