@@ -162,8 +162,15 @@ __device__ void element_operator(int nx, int ny, int nz, double K[8]) {
 __global__ void k_assemble(AsmArgs a) {
     const Geom &g = a.g;
     // C1 once per CTA (24 divisions), shared by its rows
-    __shared__ double sK[8];
+    // C1 once per CTA, and C2's folds of c copies of K(d) (c = 0..8) as a table
+    __shared__ double sK[8], sKc[8][9];
     if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        double v = 0.0;
+        sKc[threadIdx.x][0] = v;
+        for (int q = 1; q <= 8; ++q) sKc[threadIdx.x][q] = v = __dadd_rn(v, sK[threadIdx.x]);
+    }
     __syncthreads();
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nslices = (g.rows + 31) >> 5;
@@ -194,9 +201,6 @@ __global__ void k_assemble(AsmArgs a) {
     auto vptr = [&](int t) -> double * {
         return sym ? a.val + (14 * s + (t - 13)) * 32 + lane : a.val + (27 * s + t) * 32 + lane;
     };
-    double K[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) K[d] = sK[d];
     int lx, ly, lz;
     row_coords(g, row, lx, ly, lz);
     const int ix = g.own_lo[0] + lx, iy = g.own_lo[1] + ly, iz = g.own_lo[2] + lz;
@@ -227,9 +231,7 @@ __global__ void k_assemble(AsmArgs a) {
                     continue;
                 }
                 const int c = (dx ? 1 : n_el[0]) * (dy ? 1 : n_el[1]) * (dz ? 1 : n_el[2]);
-                const double Kd = K[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)];
-                double v = 0.0;
-                for (int q = 0; q < c; ++q) v = __dadd_rn(v, Kd);
+                double v = sKc[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)][c];
                 if (row_bc) {
                     v = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
                 } else if (on_boundary(jx, jy, jz, g.nx, g.ny, g.nz)) {
@@ -272,8 +274,15 @@ __global__ void k_assemble(AsmArgs a) {
 // mask bit 31 marks owned nodes; b is written for owned rows only.
 __global__ void k_assemble_symx(AsmArgs a) {
     const Geom &g = a.g;
-    __shared__ double sK[8];
+    // C1 once per CTA, and C2's folds of c copies of K(d) (c = 0..8) as a table
+    __shared__ double sK[8], sKc[8][9];
     if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        double v = 0.0;
+        sKc[threadIdx.x][0] = v;
+        for (int q = 1; q <= 8; ++q) sKc[threadIdx.x][q] = v = __dadd_rn(v, sK[threadIdx.x]);
+    }
     __syncthreads();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nslices = (g.ncols + 31) >> 5;
@@ -286,9 +295,6 @@ __global__ void k_assemble_symx(AsmArgs a) {
         a.mask[c] = 0u;
         return;
     }
-    double K[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) K[d] = sK[d];
     const unsigned u = (unsigned)c;
     const unsigned line = u / (unsigned)g.ext_n[0];
     const int ex = (int)(u - line * (unsigned)g.ext_n[0]);
@@ -321,9 +327,7 @@ __global__ void k_assemble_symx(AsmArgs a) {
                     continue;
                 }
                 const int cnt = (dx ? 1 : n_el[0]) * (dy ? 1 : n_el[1]) * (dz ? 1 : n_el[2]);
-                const double Kd = K[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)];
-                double v = 0.0;
-                for (int q = 0; q < cnt; ++q) v = __dadd_rn(v, Kd);
+                double v = sKc[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)][cnt];
                 if (row_bc) {
                     v = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
                 } else if (on_boundary(jx, jy, jz, g.nx, g.ny, g.nz)) {
@@ -1473,7 +1477,7 @@ __device__ __forceinline__ double cluster_dot(const Expansion &ex, ClusterSmem &
 template <int FMT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs a, int K,
                                                              double tol) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     ClusterSmem &S = *reinterpret_cast<ClusterSmem *>(smem_raw);
     cgx::cluster_group cl = cgx::this_cluster();
     const int q = (int)cl.block_rank(), C = (int)cl.num_blocks();
@@ -1859,7 +1863,6 @@ constexpr int UT_ROWS = 1024;                         // rows per tile
 constexpr int UT_STAGES = 6;                          // 6 x 32 KB in flight per SM (K6)
 constexpr int UT_CWARPS = 8;                          // consumer warps
 constexpr int UT_THREADS = 32 * (UT_CWARPS + 1);      // + producer warp
-constexpr int UT_CONS = 32 * UT_CWARPS;
 
 
 // Pure-read probe with the same bulk-copy engine (B_read for the TMA kernels).
