@@ -41,7 +41,9 @@ extern "C" {
 /* ---- context modes ---------------------------------------------------------------------- */
 #define MINIFE_MODE_SINGLE 0   /* one process, one GPU, one part */
 #define MINIFE_MODE_VIRTUAL 1  /* one process, one GPU, p RCB parts ("virtual ranks") */
-#define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1, NCCL comms */
+#define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1: NCCL all-reduce;
+                                  halo by peer push over NVLink when every device pair has
+                                  peer access (else NCCL send/recv) */
 #define MINIFE_MODE_RANK 3     /* SPMD: this process is rank r of w (torchrun), NCCL comm */
 
 /* ---- matrix storage formats ---------------------------------------------- */
@@ -196,7 +198,10 @@ int minife_assemble(minife_ctx *ctx);
 /* Unpreconditioned CG (C6): x0 = 0, r0 = b, p0 = r0; at most max_iters
  * iterations; stops when hist[k] <= tol*hist[0] or rr == 0.  tol == 0 runs exactly
  * max_iters (benchmark mode).  Dots are exactly rounded (C5), so the result is independent
- * of the partition and bit-identical to the oracle.  Blocks until the solve has finished.
+ * of the partition and bit-identical to the oracle.  Execution: one CUDA graph per (ctx,
+ * max_iters, tol) with three kernels per iteration; single-part SEG/SYM ctxs of <= 8192 rows
+ * run the whole solve in one thread-block-cluster launch instead (same results).  Blocks
+ * until the solve has finished.
  * `res` may be NULL.  Returns MINIFE_OK, MINIFE_ENOTSPD or MINIFE_EDIVERGED (also stored in
  * res->status); the cap reached is MINIFE_OK with converged = 0.
  * Errors: MINIFE_ESTATE (not assembled), MINIFE_EINVAL (max_iters < 1, tol < 0 or NaN),
