@@ -283,7 +283,8 @@ class Minife:
                     "minife_set_stream")
 
     def set_format(self, fmt: int):
-        """FMT_SEG (default, the paper's BCRS on SELL-32) or FMT_CRS (one index per entry)."""
+        """FMT_SYM (default: BCRS segments + upper-triangle values), FMT_SEG (the paper's BCRS
+        on SELL-32) or FMT_CRS (one index per entry); the ctx becomes unassembled."""
         self._check(minife_set_format(self.h, fmt), "minife_set_format")
         self.info = self.get_info()
 
