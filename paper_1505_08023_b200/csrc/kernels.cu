@@ -1413,11 +1413,39 @@ struct ClusterSmem {
     double pfull[CL_MAX_ROWS + 32];
     int recv[2][CL_NDIG + 1];            // cluster sums, parity double-buffered
     int dig[CL_NDIG + 1];                // this CTA's digit counters
+    int nzd[CL_NDIG + 1], nzv[CL_NDIG + 1], nnz;   // its nonzero ones, compacted
     unsigned long long sacc[ACC_WORDS];
     unsigned long long fin[ACC_WORDS];
     double coef;
     int stop;
 };
+
+// A product added straight to the CTA's 16-bit digit counters (shared 32-bit atomics): its
+// exact value m 2^(pos-1074) cut into <= 5 signed 16-bit chunks on the global grid.  For the
+// cluster solver's few products per thread this is cheaper than a TwoSum expansion plus a
+// warp flush.  A CTA adds <= 2^10 chunks < 2^16 per digit, 16 CTAs < 2^31.  Non-finite
+// values count in the flag slot.
+__device__ __forceinline__ void dig_add(double v, int *dig) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    const unsigned long long frac = bits & 0xfffffffffffffull;
+    if (e == 0x7ff) {
+        atomicAdd(&dig[CL_FLAG], 1);
+        return;
+    }
+    if (e == 0 && frac == 0) return;
+    const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
+    const int pos = e ? e - 1 : 0;
+    const int d16 = pos >> 4, s16 = pos & 15;
+    const unsigned long long mlo = m << s16;
+    const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
+    int ch[5] = {(int)(mlo & 0xffff), (int)((mlo >> 16) & 0xffff), (int)((mlo >> 32) & 0xffff),
+                 (int)(mlo >> 48), (int)mhi};
+    const bool neg = bits >> 63;
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (ch[q]) atomicAdd(&dig[d16 + q], neg ? -ch[q] : ch[q]);
+}
 
 // Exact cluster-wide dot of the CTAs' expansions (all threads of every CTA call it); the
 // rounded value is returned to warp 0 of every CTA.  Each CTA reduces into its own digit
@@ -1425,9 +1453,10 @@ struct ClusterSmem {
 // after one cluster barrier every CTA rounds the same integers.  recv[par] is cleared right
 // after use: it is written again two dots later, behind a barrier this CTA has not yet passed.
 // (Pulling all CTAs' counters after the barrier instead measured 1 us slower at 10^3.)
+template <bool DD>
 __device__ __forceinline__ double cluster_dot(const Expansion &ex, ClusterSmem &S,
                                               cgx::cluster_group &cl, int par) {
-    expansion_flush_digits(ex, S.dig, S.sacc);
+    if (!DD) expansion_flush_digits(ex, S.dig, S.sacc);   // DD: products already in S.dig
     __syncthreads();
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
@@ -1447,12 +1476,29 @@ __device__ __forceinline__ double cluster_dot(const Expansion &ex, ClusterSmem &
             S.sacc[ACC_FLAG] = 0ull;
         }
         __syncwarp();
-        const int C = (int)cl.num_blocks();
-        for (int d = lane; d <= CL_NDIG; d += 32) {
-            const int v = S.dig[d];
-            S.dig[d] = 0;
-            if (v)
-                for (int r = 0; r < C; ++r) atomicAdd(cl.map_shared_rank(&S.recv[par][d], r), v);
+        // compact the nonzero counters (ascending digit) for the push below
+        int nnz = 0;
+        for (int d0 = 0; d0 <= CL_NDIG; d0 += 32) {
+            const int d = d0 + lane;
+            const int v = d <= CL_NDIG ? S.dig[d] : 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, v != 0);
+            if (v) {
+                const int at = nnz + __popc(bal & ((1u << lane) - 1u));
+                S.nzd[at] = d;
+                S.nzv[at] = v;
+                S.dig[d] = 0;
+            }
+            nnz += __popc(bal);
+        }
+        if (lane == 0) S.nnz = nnz;
+    }
+    __syncthreads();
+    // every (nonzero digit, CTA) pair by its own thread: one remote atomic each
+    {
+        const int C = (int)cl.num_blocks(), nnz = S.nnz;
+        for (int e = threadIdx.x; e < nnz * C; e += blockDim.x) {
+            const int q = e % nnz, r = e / nnz;
+            atomicAdd(cl.map_shared_rank(&S.recv[par][S.nzd[q]], r), S.nzv[q]);
         }
     }
     cl.sync();
@@ -1474,7 +1520,7 @@ __device__ __forceinline__ double cluster_dot(const Expansion &ex, ClusterSmem &
     return v;
 }
 
-template <int FMT>
+template <int FMT, bool DD = true>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs a, int K,
                                                              double tol) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1526,13 +1572,14 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
         xv[j] = rv[j] = apv[j] = 0.0;
         if (sl < nsl && row < rows) {
             rv[j] = a.b[row];
-            ex.add(__dmul_rn(rv[j], rv[j]), S.sacc);
+            if (DD) dig_add(__dmul_rn(rv[j], rv[j]), S.dig);
+            else ex.add(__dmul_rn(rv[j], rv[j]), S.sacc);
         }
     }
     cl.sync();                                     // matrix, counters and p in place everywhere
     int par = 0;
     {
-        const double rr0 = cluster_dot(ex, S, cl, par);
+        const double rr0 = cluster_dot<DD>(ex, S, cl, par);
         par ^= 1;
         if (q == 0 && tid == 0) cg_state_init(a, rr0, tol);
     }
@@ -1552,11 +1599,12 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
                         sum = __dadd_rn(sum, __dmul_rn(S.val[sl][t][lane],
                                                        S.pfull[S.seg[sl][t / 3][lane] + t % 3]));
                 apv[j] = sum;
-                ex.add(__dmul_rn(S.pfull[row], sum), S.sacc);
+                if (DD) dig_add(__dmul_rn(S.pfull[row], sum), S.dig);
+                else ex.add(__dmul_rn(S.pfull[row], sum), S.sacc);
             }
         }
         {
-            const double pAp = cluster_dot(ex, S, cl, par);
+            const double pAp = cluster_dot<DD>(ex, S, cl, par);
             par ^= 1;
             if (tid == 0) {
                 double alpha;
@@ -1573,10 +1621,18 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
         for (int j = 0; j < CL_RPT; ++j) {
             const int sl = warp + CL_WARPS * j;
             const int64_t row = (s_lo + sl) * 32 + lane;
-            if (sl < nsl && row < rows) xr_step(xv[j], rv[j], S.pfull[row], apv[j], alpha, ex, S.sacc);
+            if (sl < nsl && row < rows) {
+                if (DD) {
+                    xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha, S.pfull[row]));
+                    rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha, apv[j]));
+                    dig_add(__dmul_rn(rv[j], rv[j]), S.dig);
+                } else {
+                    xr_step(xv[j], rv[j], S.pfull[row], apv[j], alpha, ex, S.sacc);
+                }
+            }
         }
         {
-            const double rrn = cluster_dot(ex, S, cl, par);
+            const double rrn = cluster_dot<DD>(ex, S, cl, par);
             par ^= 1;
             if (tid == 0) {
                 double beta;
@@ -2323,24 +2379,28 @@ cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double t
     if (m.rows > CL_MAX_ROWS || (m.nslices + CL_CTAS - 1) / CL_CTAS > CL_MAX_SL ||
         !a.g.ident || (m.fmt != FMT_SEG && m.fmt != FMT_SYM) || m.slice_row)
         return cudaErrorInvalidValue;
-    auto kern = m.fmt == FMT_SEG ? k_cg_cluster<FMT_SEG> : k_cg_cluster<FMT_SYM>;
+    static int dd = -1;
+    if (dd < 0) {
+        const char *e = getenv("MINIFE_CL_DD");
+        dd = (e && e[0] == '0') ? 0 : 1;
+    }
+    auto kern = m.fmt == FMT_SEG ? (dd ? k_cg_cluster<FMT_SEG, true> : k_cg_cluster<FMT_SEG, false>)
+                                 : (dd ? k_cg_cluster<FMT_SYM, true> : k_cg_cluster<FMT_SYM, false>);
     const int smem = (int)sizeof(ClusterSmem);
     static unsigned long long set = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!((set >> (dev & 63)) & 1ull)) {
-        cudaError_t e = cudaFuncSetAttribute(k_cg_cluster<FMT_SEG>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SEG>,
-                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM>,
-                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
+        void (*ks[4])(Matrix, UpdArgs, int, double) = {
+            k_cg_cluster<FMT_SEG, true>, k_cg_cluster<FMT_SYM, true>,
+            k_cg_cluster<FMT_SEG, false>, k_cg_cluster<FMT_SYM, false>};
+        for (auto kf : ks) {
+            cudaError_t e =
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
         set |= 1ull << (dev & 63);
     }
     cudaLaunchConfig_t cfg = {};
