@@ -94,6 +94,7 @@ struct Part {
     unsigned long long *d_acc = nullptr;
     CgState *d_st = nullptr;
     double *d_hist = nullptr, *d_rr = nullptr;
+    double *d_alpha = nullptr;                    // alpha_k history (x every second iteration)
     int hist_cap = 0;
     // halo: send_col = extended columns of the send lists (neighbor order), recv_pos =
     // extended column of each halo slot; wire buffers
@@ -245,7 +246,7 @@ static void free_part(Part &p) {
                     p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
-                    p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr};
+                    p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
@@ -282,8 +283,10 @@ static int alloc_hist(minife_ctx *c, Part &p, int cap) {
     DevGuard g(p.dev);
     dfree(p, p.d_hist, p.hist_cap);
     dfree(p, p.d_rr, p.hist_cap);
+    dfree(p, p.d_alpha, p.hist_cap);
     TRY(dalloc(c, p, &p.d_hist, cap));
     TRY(dalloc(c, p, &p.d_rr, cap));
+    TRY(dalloc(c, p, &p.d_alpha, cap));
     p.hist_cap = cap;
     return MINIFE_OK;
 }
@@ -1170,8 +1173,25 @@ static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
 }
 
 // init + max_iters iterations (+ the fused scheme's finish kernel), enqueued on the streams
+// x every second iteration (one part, three-kernel scheme): K7 of an odd iteration leaves x
+// alone and writes p_(k+1) into the other p buffer; the next (even) K7 applies
+// alpha_(k-1) p_(k-1) and alpha_k p_k in one pass over x.  x then costs 16 B per row every
+// second iteration (36 instead of 40 B/row per K7 on average); same operations, same order:
+// bit-identical.  MINIFE_X2=0 disables.
+static bool x2_mode(const minife_ctx *c) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("MINIFE_X2");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    // only where the vectors stream from HBM anyway (B200: 300^3 -1.0 % per iteration; at
+    // 100^3, whose vectors sit in L2, the second p buffer costs +0.7 %)
+    return env && c->parts.size() == 1 && c->world == 1 && !fused_mode(c) &&
+           40.0 * (double)c->parts[0].ncols >= 64e6;
+}
+
 static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
-    if (fused_mode(c) && !c->parts[0].d_p2) {
+    if ((fused_mode(c) || x2_mode(c)) && !c->parts[0].d_p2) {
         Part &p = c->parts[0];
         DevGuard g(p.dev);
         TRY(alloc_colvec(c, p, &p.d_p2));
@@ -1200,7 +1220,34 @@ static int small_mode(const minife_ctx *c) {
     return fits2 ? 2 : (fits1 ? 1 : 0);
 }
 
+// p_k of the x-every-2 scheme: p_1 (written by the init kernels) in d_p, then alternating
+static double *x2_pbuf(const Part &p, int k) { return (k & 1) ? p.d_p : p.d_p2; }
+
+static int enqueue_iteration_x2(minife_ctx *c, int k) {
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    cudaStream_t s = launch_stream(c, p);
+    CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(p, k), p.d_Ap, true), true, p.grid_spmv, s));
+    UpdArgs u6 = upd_args(c, p, 0);
+    u6.alpha_hist = p.d_alpha;
+    CUDA_TRY(c, launch_update_xr(u6, k, p.grid_upd, s));
+    UpdArgs u7 = upd_args(c, p, 1);
+    u7.alpha_hist = p.d_alpha;
+    CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(p, k), x2_pbuf(p, k + 1), p.grid_upd, s));
+    return MINIFE_OK;
+}
+
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
+    if (!t && x2_mode(c) && !small_mode(c)) {
+        TRY(enqueue_init(c, tol));
+        for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration_x2(c, k));
+        Part &p = c->parts[0];
+        DevGuard g(p.dev);
+        UpdArgs u = upd_args(c, p, 0);
+        u.alpha_hist = p.d_alpha;
+        CUDA_TRY(c, launch_x2_finish(u, p.d_p, p.d_p2, launch_stream(c, p)));
+        return MINIFE_OK;
+    }
     const int sm = t ? 0 : small_mode(c);
     if (sm) {
         Part &p = c->parts[0];

@@ -1081,6 +1081,7 @@ __device__ __forceinline__ int xr_prologue(const UpdArgs &a, double pAp, int k, 
     if (blockIdx.x == 0) {
         a.st->pAp = pAp;
         a.st->alpha = alpha;
+        if (a.alpha_hist) a.alpha_hist[k] = alpha;
         if (stop) {
             a.st->status = status;
             a.st->converged = conv;
@@ -1750,6 +1751,75 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             if (!stop) a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, pc));
         }
     }
+}
+
+// K7 of the x-every-second-iteration scheme (one part, launch_update_p2).  The x update of
+// iteration k is fl(x + fl(alpha_k p_k)) exactly as in K7; it is only deferred by one
+// iteration on odd k, so p_(k+1) goes to the other buffer and p_(k-1) survives until the
+// next (even) K7, which applies both updates in order with one pass over x.
+__global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, const double *pk,
+                                                           double *po) {
+    __shared__ unsigned long long s_in[ACC_WORDS];
+    __shared__ double s_beta;
+    __shared__ int s_stop;
+    if (a.st->done) return;              // K6 stopped: x_finish applies what is pending
+    acc_load_shared(s_in, a.acc_in);
+    __syncthreads();
+    const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
+    if (threadIdx.x == 0) {
+        double beta;
+        s_stop = p_prologue(a, fin, k, beta);
+        s_beta = beta;
+    }
+    __syncthreads();
+    const bool stop = s_stop, even = !(k & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (even || stop)) a.st->x_done = k;
+    if (!stop && blockIdx.x == 0 && a.acc_zero)
+        for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    const double beta = s_beta, ak = a.alpha_hist[k], ak1 = even ? a.alpha_hist[k - 1] : 0.0;
+    const bool upx = even || stop;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t rows = a.g.rows, n2 = rows >> 1;
+    double2 *x2 = reinterpret_cast<double2 *>(a.x);
+    const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
+    const double2 *pk2 = reinterpret_cast<const double2 *>(pk);
+    double2 *po2 = reinterpret_cast<double2 *>(po);
+    auto step = [&](double &x, double &po_, double r, double p) {
+        if (even) x = __dadd_rn(x, __dmul_rn(ak1, po_));       // alpha_(k-1) p_(k-1)
+        if (upx) x = __dadd_rn(x, __dmul_rn(ak, p));           // alpha_k p_k
+        if (!stop) po_ = __dadd_rn(r, __dmul_rn(beta, p));     // p_(k+1)
+    };
+    for (int64_t i = tid; i < n2; i += stride) {
+        const double2 pv = pk2[i];
+        double2 ov = make_double2(0.0, 0.0), xv = make_double2(0.0, 0.0), rv = make_double2(0.0, 0.0);
+        if (even) ov = po2[i];                              // p_(k-1), still pending
+        if (upx) xv = x2[i];
+        if (!stop) rv = r2[i];
+        step(xv.x, ov.x, rv.x, pv.x);
+        step(xv.y, ov.y, rv.y, pv.y);
+        if (upx) x2[i] = xv;
+        if (!stop) po2[i] = ov;
+    }
+    if ((rows & 1) && tid == 0) {
+        const int64_t j = rows - 1;
+        double xj = upx ? a.x[j] : 0.0, oj = even ? po[j] : 0.0;
+        step(xj, oj, stop ? 0.0 : a.r[j], pk[j]);
+        if (upx) a.x[j] = xj;
+        if (!stop) po[j] = oj;
+    }
+}
+
+// After the loop: the x update of the last iteration with an alpha, if still pending.
+__global__ void __launch_bounds__(UPD_THREADS) k_x2_finish(UpdArgs a, const double *p_odd,
+                                                           const double *p_even) {
+    const int j = a.st->x_done + 1;
+    if (j > a.st->alpha_iter) return;
+    const double alpha = a.alpha_hist[j];
+    const double *p = (j & 1) ? p_odd : p_even;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride)
+        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, p[i]));
 }
 
 // Halo values of p_(k+1) computed ahead of K7 (SYM with a halo): the packed
@@ -2437,6 +2507,22 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
     return cudaGetLastError();
 }
 
+cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *po, int grid,
+                             cudaStream_t s) {
+    query_occupancy();
+    const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
+    const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
+    (void)grid;
+    k_update_p2<<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_x2_finish(const UpdArgs &a, const double *p_odd, const double *p_even,
+                             cudaStream_t s) {
+    k_x2_finish<<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s) {
     if (a.g.ident) k_init_vectors<true><<<grid, UPD_THREADS, 0, s>>>(a);
     else k_init_vectors<false><<<grid, UPD_THREADS, 0, s>>>(a);
@@ -2461,7 +2547,7 @@ static bool x_late() {
 }
 
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    const bool xl = x_late();
+    const bool xl = x_late() || a.alpha_hist;     // x-every-2 scheme: K6 updates r only
     if (a.g.ident) {
         if (xl) k_update_xr<true, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
         else k_update_xr<true, false><<<grid, UPD_THREADS, 0, s>>>(a, k);

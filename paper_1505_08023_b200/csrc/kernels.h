@@ -111,6 +111,7 @@ struct UpdArgs {
     unsigned long long *acc_zero;       // cleared by CTA 0 (may be null)
     double *hist, *rr;                  // [max_iters+1]
     CgState *st;
+    double *alpha_hist;                 // [max_iters+1]: alpha_k recorded by K6 (may be null)
 };
 
 // Setup (a0.2-a0.5)
@@ -124,6 +125,13 @@ cudaError_t launch_init_vectors(const UpdArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s);
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s);
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s);
+// x every second iteration (one part): K7 of iteration k with p_k in pk and p_(k-1) in po;
+// writes p_(k+1) into po; even k: x += alpha_(k-1) p_(k-1), then += alpha_k p_k (odd k: only
+// on a stop).  x2_finish applies an x update still pending after the loop.
+cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *po, int grid,
+                             cudaStream_t s);
+cudaError_t launch_x2_finish(const UpdArgs &a, const double *p_odd, const double *p_even,
+                             cudaStream_t s);
 // fused scheme: K6' (alpha_k; r -= alpha Ap; exact rr) and the finish kernel (rr_K, pending x)
 cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp_next_zero,
                             int grid, cudaStream_t s);
