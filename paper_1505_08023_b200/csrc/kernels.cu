@@ -2255,6 +2255,9 @@ static void query_occupancy() {
     for (int f = 0; f < 2; ++f)
         if (g_spmv_bps[f] <= 0) g_spmv_bps[f] = 1;
     if (g_upd_bps <= 0) g_upd_bps = 1;
+    // A/B: CTAs per SM of the update kernels (grid = SMs x this), capped by the occupancy
+    if (const char *e = getenv("MINIFE_K6_BPS")) g_upd_bps = std::max(1, std::min(g_upd_bps, atoi(e)));
+    if (const char *e = getenv("MINIFE_K7_BPS")) g_updp_bps = std::max(1, std::min(g_updp_bps, atoi(e)));
 }
 
 int spmv_grid(int64_t nslices, int fmt) {
