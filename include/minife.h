@@ -213,6 +213,19 @@ int minife_cg_solve(minife_ctx *ctx, int max_iters, double tol, minife_cg_result
  * state valid.  Errors as minife_cg_solve. */
 int minife_cg_profile(minife_ctx *ctx, int max_iters, minife_kernel_times *out);
 
+/* Timing window inside later minife_cg_solve calls: CUDA events (graph nodes) are recorded on
+ * part 0's stream right before and after the SpMV launches of iterations first_iter ..
+ * first_iter + n_iters - 1, so the dominant kernel is timed in the solve itself, not in a
+ * separate profile run.  n_iters = 0 removes the window.  Rebuilds the solve graph.
+ * Errors: MINIFE_EINVAL (NULL, first_iter < 1, n_iters < 0), MINIFE_ECUDA. */
+int minife_set_timing_window(minife_ctx *ctx, int first_iter, int n_iters);
+
+/* Averages over the window of the last solve: SpMV duration (start to end event of each
+ * iteration's SpMV) and iteration period (start to start), milliseconds.
+ * Errors: MINIFE_EINVAL (NULL), MINIFE_ESTATE (no window, or the last solve stopped before
+ * its end), MINIFE_ECUDA. */
+int minife_get_timing_window(minife_ctx *ctx, double *spmv_ms, double *iter_ms);
+
 /* y = A x for the assembled, Dirichlet-imposed A (C4).  SINGLE/VIRTUAL/MULTI: x, y are host
  * arrays of `rows` doubles in global id order.  RANK: x, y hold this rank's owned rows in
  * ascending global id (minife_get_owned_ids); the halo is exchanged with the other ranks.

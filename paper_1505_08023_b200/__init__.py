@@ -122,6 +122,8 @@ SIGNATURES = {
     "minife_bandwidth_probe": (_I, [_I, _I64, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_probe_l2_read_gbs": (_D, []),
     "minife_dot": (_I, [_I, _I64, _P, _P, ctypes.POINTER(_D)]),
+    "minife_set_timing_window": (_I, [_P, _I, _I]),
+    "minife_get_timing_window": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_exact_round": (_I, [_I, _P, ctypes.POINTER(_D)]),
     "minife_version": (ctypes.c_char_p, []),
 }
@@ -306,6 +308,18 @@ class Minife:
         if st not in (MINIFE_OK, MINIFE_ENOTSPD, MINIFE_EDIVERGED):
             self._check(st, "minife_cg_solve")
         return res
+
+    def set_timing_window(self, first_iter: int, n_iters: int):
+        """Time the SpMV of iterations [first_iter, first_iter + n_iters) inside later solves."""
+        self._check(minife_set_timing_window(self.h, first_iter, n_iters),
+                    "minife_set_timing_window")
+
+    def timing_window(self):
+        """(SpMV ms, iteration ms) averaged over the window of the last solve."""
+        a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        self._check(minife_get_timing_window(self.h, ctypes.byref(a), ctypes.byref(b)),
+                    "minife_get_timing_window")
+        return a.value, b.value
 
     def cg_profile(self, max_iters: int = 200) -> minife_kernel_times:
         out = minife_kernel_times()

@@ -153,6 +153,11 @@ struct minife_ctx {
     int g_iters = -1;
     double g_tol = -1.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // timing window (minife_set_timing_window): events around the SpMV launches of
+    // iterations [tw_k0, tw_k0 + tw_n) inside the solve itself (graph nodes)
+    int tw_k0 = 0, tw_n = 0;
+    std::vector<cudaEvent_t> tw_ev;              // [2 * tw_n]: start, end of each SpMV
+    bool tw_armed = false;                       // the enqueued solve records the window
     // last solve
     int last_iters = 0;
     bool solved = false;
@@ -571,6 +576,10 @@ extern "C" void minife_destroy(minife_ctx *c) {
     drop_graph(c);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (!c->parts.empty()) {
+        DevGuard g(c->parts[0].dev);
+        for (cudaEvent_t e : c->tw_ev) cudaEventDestroy(e);
+    }
     for (auto &p : c->parts) free_part(p);
     delete c;
 }
@@ -966,6 +975,18 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     return a;
 }
 
+// Timing window: mark the start (end = false) or end of iteration k's SpMV on part 0's stream
+static int tw_mark(minife_ctx *c, int k, bool end) {
+    if (!c->tw_n || k < c->tw_k0 || k >= c->tw_k0 + c->tw_n) return MINIFE_OK;
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    // External: a real event-record node when the stream is being captured into the graph
+    CUDA_TRY(c, cudaEventRecordWithFlags(c->tw_ev[2 * (k - c->tw_k0) + (end ? 1 : 0)],
+                                         launch_stream(c, p), cudaEventRecordExternal));
+    if (end && k == c->tw_k0 + c->tw_n - 1) c->tw_armed = true;
+    return MINIFE_OK;
+}
+
 // The halo of p is moved on the parts' transport streams while the interior slices' SpMV
 // runs (SEG, more than one part); the boundary slices follow once it has landed.
 static bool overlap_mode(const minife_ctx *c) {
@@ -1055,7 +1076,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
 // a1 + a2 with the halo in flight during the interior SpMV: fork the transport streams off
 // the compute streams (p is final after K7), interior slices, join, boundary slices.  The
 // pAp accumulator is order-independent (C5), so the split changes no bit of the result.
-static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
+static int enqueue_halo_spmv_overlapped(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
     for (auto &p : c->parts) {
         if (virt && &p != &c->parts[0]) break;
@@ -1069,6 +1090,7 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
         DevGuard g(p.dev);
         CUDA_TRY(c, cudaEventRecord(p.ev_join, p.cstream));
     }
+    TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {                     // interior slices: no halo column read
         DevGuard g(p.dev);
         SpmvArgs a = spmv_args(c, p, p.d_p, p.d_Ap, true);
@@ -1084,28 +1106,33 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c) {
         a.s_begin = p.n_int;
         CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
     }
+    TRY(tw_mark(c, k, true));
     return MINIFE_OK;
 }
 
 static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     const bool osym = overlap_sym(c) && !t;
     if (overlap_mode(c) && !t && !push_mode(c)) {
-        TRY(enqueue_halo_spmv_overlapped(c));
+        TRY(enqueue_halo_spmv_overlapped(c, k));
     } else if (osym) {                               // halo already in place (previous K7)
+        TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
             CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
                                     launch_stream(c, p)));
         }
+        TRY(tw_mark(c, k, true));
     } else {
         if (push_mode(c)) TRY(enqueue_push(c, k, 0, true));
         else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
         if (t) t->mark(3);
+        if (!t) TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
             CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
                                     launch_stream(c, p)));
         }
+        if (!t) TRY(tw_mark(c, k, true));
     }
     if (t) t->mark(0);
     TRY(enqueue_allreduce(c, 0));
@@ -1161,7 +1188,9 @@ static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
     a.hist = p.d_hist;
     a.rr = p.d_rr;
     a.stw = p.d_st;
+    if (!t) TRY(tw_mark(c, k, false));
     CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, s));
+    if (!t) TRY(tw_mark(c, k, true));
     if (t) t->mark(0);
     // K6'(k): alpha_k, r -= alpha_k Ap_k, exact rr_k
     UpdArgs u = upd_args(c, p, 0);
@@ -1227,7 +1256,9 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
     Part &p = c->parts[0];
     DevGuard g(p.dev);
     cudaStream_t s = launch_stream(c, p);
+    TRY(tw_mark(c, k, false));
     CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(p, k), p.d_Ap, true), true, p.grid_spmv, s));
+    TRY(tw_mark(c, k, true));
     UpdArgs u6 = upd_args(c, p, 0);
     u6.alpha_hist = p.d_alpha;
     CUDA_TRY(c, launch_update_xr(u6, k, p.grid_upd, s));
@@ -1238,6 +1269,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
 }
 
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
+    if (!t) c->tw_armed = false;
     if (!t && x2_mode(c) && !small_mode(c)) {
         TRY(enqueue_init(c, tol));
         for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration_x2(c, k));
@@ -1380,6 +1412,52 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     float ms = 0.f;
     CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     return read_result(c, max_iters, res, ms * 1e-3);
+}
+
+extern "C" int minife_set_timing_window(minife_ctx *c, int first_iter, int n_iters) {
+    if (!c || first_iter < 1 || n_iters < 0) return MINIFE_EINVAL;
+    DevGuard g(c->parts[0].dev);
+    for (cudaEvent_t e : c->tw_ev) cudaEventDestroy(e);
+    c->tw_ev.assign(2 * (size_t)n_iters, nullptr);
+    for (auto &e : c->tw_ev) CUDA_TRY(c, cudaEventCreate(&e));
+    c->tw_k0 = first_iter;
+    c->tw_n = n_iters;
+    drop_graph(c);
+    return MINIFE_OK;
+}
+
+extern "C" int minife_get_timing_window(minife_ctx *c, double *spmv_ms, double *iter_ms) {
+    if (!c || !spmv_ms || !iter_ms) return MINIFE_EINVAL;
+    if (!c->tw_n || !c->tw_armed || !c->solved || c->last_iters < c->tw_k0 + c->tw_n - 1) {
+        set_err(c, "no solve has run through the whole timing window (single-launch solvers "
+                   "have none)");
+        return MINIFE_ESTATE;
+    }
+    DevGuard g(c->parts[0].dev);
+    double sum = 0.0;
+    for (int j = 0; j < c->tw_n; ++j) {
+        float ms = 0.f;
+        const cudaError_t e = cudaEventElapsedTime(&ms, c->tw_ev[2 * j], c->tw_ev[2 * j + 1]);
+        if (e != cudaSuccess) {
+            cudaGetLastError();                  // not sticky: do not poison later launches
+            set_err(c, "cudaEventElapsedTime on the timing window: %s", cudaGetErrorString(e));
+            return MINIFE_ECUDA;
+        }
+        sum += ms;
+    }
+    *spmv_ms = sum / c->tw_n;
+    *iter_ms = 0.0;
+    if (c->tw_n >= 2) {
+        float ms = 0.f;
+        const cudaError_t e = cudaEventElapsedTime(&ms, c->tw_ev[0], c->tw_ev[2 * (c->tw_n - 1)]);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            set_err(c, "cudaEventElapsedTime on the timing window: %s", cudaGetErrorString(e));
+            return MINIFE_ECUDA;
+        }
+        *iter_ms = ms / (c->tw_n - 1);
+    }
+    return MINIFE_OK;
 }
 
 extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_times *out) {

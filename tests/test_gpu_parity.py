@@ -185,6 +185,27 @@ def test_x_every_second_iteration_bit_identical(n, fmt):
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
+def test_timing_window_inside_the_solve():
+    """minife_set_timing_window: events around the SpMVs of a range of iterations are part of
+    the solve graph; the results stay bitwise the oracle's; the window needs a solve that ran
+    through it."""
+    n = (33, 32, 31)
+    with M.Minife(*n) as g:
+        g.assemble()
+        g.set_timing_window(5, 10)
+        with pytest.raises(M.MinifeError):
+            g.timing_window()                        # no solve yet
+        check_cg(g, n, 200, 0.0)
+        spmv_ms, iter_ms = g.timing_window()
+        assert 0.0 < spmv_ms < iter_ms < 50.0
+        g.set_timing_window(150, 100)                # beyond the solve
+        check_cg(g, n, 200, 0.0)
+        with pytest.raises(M.MinifeError):
+            g.timing_window()
+        g.set_timing_window(1, 0)                    # removed
+        check_cg(g, n, 30, 0.0)
+
+
 def test_plan_on_device_matches_host_plan():
     n, p = (12, 11, 10), 8
     with M.Minife(*n, virtual=p) as g:
