@@ -5,10 +5,19 @@
 // is also built with -fmad=false), subnormals kept.  Dots are exactly rounded (exact.cuh).
 //
 // Layout: rows = owned nodes (owned-box order), columns = extended box
-// (owned + one-node halo shell).  Both matrix formats are SELL-32: slice s = rows 32s..32s+31,
+// (owned + one-node halo shell).  All matrix formats are SELL-32: slice s = rows 32s..32s+31,
 // stored k-major so a warp's load of entry k is one contiguous 256 B (val) / 128 B (index)
 // segment.  Entries of a row are kept in ascending GLOBAL column (C4 order); absent/padding
 // entries are never added (row-length predicate or presence mask).
+//
+// Sections, in file order:
+//   helpers (cache policies, coordinates)          a0.2-a0.5 assembly (CRS/SEG/SYM, SYM ghost rows)
+//   a2 SpMV: CRS / SEG register kernels, k_spmv_tma (SEG/CRS/fused), k_spmv_sym, k_spmv_symm
+//   a3-a6: init, K6 (k_update_xr), single-launch solvers (k_cg_small, k_cg_cluster),
+//          K7 (k_update_p, k_update_p2 + k_x2_finish), halo (k_pack_next_p, k_push),
+//          fused scheme (k_update_r, k_cg_finish)
+//   probes (read / copy / L2), k_move, k_vsum, k_dot, k_acc_round, k_extract_rows
+//   host launchers (occupancy, grids, format / scheme dispatch)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cooperative_groups.h>
