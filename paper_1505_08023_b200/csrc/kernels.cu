@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "exact.cuh"
@@ -857,10 +858,15 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
 // (dz,dy) = (-1,-1), (-1,0), (-1,1), (0,-1); group 4 = slot 12, (0,0,-1)) reads stored slots
 // 11-3j..13-3j (group 4: slot 1) of rows i - 1 + e + off_j.  For a tile [r0, r0 + 32 NW) those
 // rows lie in the NW + 2 slices from floor((r0 - 1 + off_j) / 32): one 3-D box {32 lanes,
-// 3 slots, NW + 2 slices} of the value array viewed as [slices][14][32], fetched with one
-// cp.async.bulk.tensor per group (zero fill outside the matrix) -- from L2: the rows were
-// streamed about one plane (or one line) earlier.  Consumers read every matrix value from
-// shared memory; only the x gathers go through L1.
+// NW + 2 slices, 3 slots} of the value array viewed SLOT-MAJOR ([14][slices][32] by strides),
+// fetched with one cp.async.bulk.tensor per group (zero fill outside the matrix) -- from L2:
+// the rows were streamed about one plane (or one line) earlier.  In shared memory each slot of
+// a box is then GS * 32 consecutive rows, so a run's three mirrored values sit at one address
+// (computed once per run from its stored start column) plus constant offsets.  Consumers read
+// every matrix value from shared memory; only the x gathers go through L1.
+//
+// A warp whose 32 rows all have the full 27-entry pattern (interior rows: ~88 % of the tiles
+// at 300^3) takes a branch-free path with no per-slot predicates; same operations, same order.
 template <int NW, int NST> struct SymmCfg {
     static constexpr int THREADS = 32 * (NW + 1);
     static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
@@ -886,6 +892,41 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
         "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
+}
+
+constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots present
+
+// One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
+// ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
+// row sum; xd = x of the row itself (slot 13).
+template <bool FULL, int GS>
+__device__ __forceinline__ double symm_fold(const double *__restrict__ x, const int (&sg)[9],
+                                            unsigned msk, const double *vs, const double *mir,
+                                            const int (&madj)[5], int r0, double &xd) {
+    auto on = [&](int t) { return FULL || ((msk >> t) & 1u); };
+    double xv[27];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
+    double lv[13];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {                     // runs 0..3: 3 slots; run 4: slot 12
+        const double *mj = mir + madj[j] + (sg[j] - r0);
+        const int ne = j < 4 ? 3 : 1;
+#pragma unroll
+        for (int e = 0; e < ne; ++e) {
+            const int t = 3 * j + e, q = j < 4 ? 2 - e : 0;
+            lv[t] = FULL ? mj[q * GS * 32 + e] : (on(t) ? mj[q * GS * 32 + e] : 0.0);
+        }
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < 13; ++t)
+        if (on(t)) sum = __dadd_rn(sum, __dmul_rn(lv[t], xv[t]));
+#pragma unroll
+    for (int t = 13; t < 27; ++t)
+        if (on(t)) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
+    xd = xv[13];
+    return sum;
 }
 
 template <bool DOT, int NW, int NST>
@@ -942,15 +983,21 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 const int64_t r0 = s0 * 32;
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
-                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, 11 - 3 * g,
-                             symm_box_slice(r0, g, N0, P), &full_bar[st]);
-                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, 1, symm_box_slice(r0, 4, N0, P),
+                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
+                             11 - 3 * g, &full_bar[st]);
+                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
                          &full_bar[st]);
             }
         }
     } else {
         Expansion ex;
         ex.init();
+        // box g of a tile starts at row r0 + K_g, K_g = 32 floor((off_g - 1) / 32): column c of
+        // slot q sits at element madj[g] + q GS 32 + (c - r0) of the stage's mirror area
+        int madj[5];
+#pragma unroll
+        for (int g = 0; g < 5; ++g)
+            madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
         int64_t i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
             const int st = (int)(i % NST);
@@ -966,34 +1013,18 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 const double *mir = reinterpret_cast<const double *>(buf + C::MIR0);
                 // storage row s*32+lane; SYM-ext: only owned nodes are computed rows
                 const int64_t row = sym_row(m, a.g, s * 32 + lane, msk);
-                const int64_t r0 = tile * NW * 32;
+                const int r0 = (int)(tile * NW * 32);
                 int sg[9];
 #pragma unroll
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
-                double xv[27];
-#pragma unroll
-                for (int t = 0; t < 27; ++t)
-                    xv[t] = ((msk >> t) & 1u) ? __ldg(a.x + sg[t / 3] + (t % 3)) : 0.0;
-                double sum = 0.0;
-#pragma unroll
-                for (int t = 0; t < 13; ++t) {
-                    const int g = t < 12 ? t / 3 : 4;
-                    const int q = t < 12 ? 2 - t % 3 : 0;              // slot 13-t - first slot
-                    const int nq = t < 12 ? 3 : 1;
-                    if ((msk >> t) & 1u) {
-                        const int c = sg[t / 3] + (t % 3);
-                        const int ga = symm_box_slice(r0, g, N0, P);
-                        const double lv = mir[g * (C::MIR3_B / 8) + ((c >> 5) - ga) * nq * 32 +
-                                              q * 32 + (c & 31)];
-                        sum = __dadd_rn(sum, __dmul_rn(lv, xv[t]));
-                    }
-                }
-#pragma unroll
-                for (int t = 13; t < 27; ++t)
-                    if ((msk >> t) & 1u) sum = __dadd_rn(sum, __dmul_rn(vs[32 * (t - 13)], xv[t]));
+                double sum, xd;
+                if (__all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL))
+                    sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
+                else
+                    sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
                 if (row >= 0) {
                     a.y[row] = sum;
-                    if (DOT) ex.add(__dmul_rn(xv[13], sum), sacc);
+                    if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
                 }
             }
             __syncwarp();
@@ -2314,8 +2345,8 @@ static cudaError_t launch_tma(const SpmvArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// 3-D tensor maps of the SYM value array [nslices][14][32] doubles: boxes of {32, 3, gs} and
-// {32, 1, gs}.  cuTensorMapEncodeTiled comes from the driver through the runtime (no -lcuda).
+// 3-D tensor maps of the SYM value array [nslices][14][32] doubles, viewed slot-major: boxes of
+// {32, gs, 3} and {32, gs, 1}.  cuTensorMapEncodeTiled comes from the driver through the runtime (no -lcuda).
 static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
@@ -2327,9 +2358,11 @@ static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) 
             return false;
         enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    const cuuint64_t dims[3] = {32, 14, (cuuint64_t)m.nslices};
-    const cuuint64_t strides[2] = {32 * 8, 14 * 32 * 8};
-    const cuuint32_t box3[3] = {32, 3, (cuuint32_t)gs}, box1[3] = {32, 1, (cuuint32_t)gs};
+    // slot-major view [14][nslices][32] of the [nslices][14][32] array (dim 1 = slice, stride
+    // 14 * 256 B; dim 2 = slot, stride 256 B): a box lands as [slot][slice][lane]
+    const cuuint64_t dims[3] = {32, (cuuint64_t)m.nslices, 14};
+    const cuuint64_t strides[2] = {14 * 32 * 8, 32 * 8};
+    const cuuint32_t box3[3] = {32, (cuuint32_t)gs, 3}, box1[3] = {32, (cuuint32_t)gs, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     void *base = const_cast<double *>(m.val);
     return enc(m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box3, es,
@@ -2372,6 +2405,11 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
     if (cfg == 1) {
         const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
+        static bool warned = false;
+        if (!warned) {
+            warned = true;
+            fprintf(stderr, "minife: tensor maps unavailable, SYM SpMV uses the L1-gather kernel\n");
+        }
     }
     using C = SyCfg<16, 2>;
     static unsigned long long attr_set = 0;
