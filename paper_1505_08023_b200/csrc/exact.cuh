@@ -182,6 +182,39 @@ __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int 
     }
 }
 
+// Two-level expansion for long per-thread sums: what the first expansion cannot hold (a term
+// far below its running total -- late in CG, the Dirichlet rows' tiny products) goes to a
+// second expansion instead of the shared-memory atomics, which only see what neither holds.
+// Exact like Expansion; costs nothing while the first level absorbs every term.
+// ExpansionL<3>: a third level for a third magnitude class.
+template <int L> struct ExpansionL {
+    Expansion lv[L];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int l = 0; l < L; ++l) lv[l].init();
+    }
+    __device__ __forceinline__ void add(double x, unsigned long long *spill) {
+#pragma unroll
+        for (int j = 0; j < NEXP; ++j) two_sum(lv[0].c[j], x, lv[0].c[j], x);
+        if (x != 0.0) {
+#pragma unroll
+            for (int l = 1; l < L - 1; ++l) {
+#pragma unroll
+                for (int j = 0; j < NEXP; ++j) two_sum(lv[l].c[j], x, lv[l].c[j], x);
+            }
+            lv[L - 1].add(x, spill);
+        }
+    }
+};
+using Expansion2 = ExpansionL<2>;
+
+template <int L>
+__device__ __forceinline__ void expansion_flush_digits(const ExpansionL<L> &ex, int *dig,
+                                                       unsigned long long *acc) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) expansion_flush_digits(ex.lv[l], dig, acc);
+}
+
 // CTA accumulator = 64-bit words (slow path, flag) + 32-bit digit counters (warp flushes):
 // zero both (all threads), and add their sum into a global accumulator (all threads).
 __device__ __forceinline__ void acc_zero_shared(unsigned long long *s, int *dig) {

@@ -867,16 +867,31 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
 //
 // A warp whose 32 rows all have the full 27-entry pattern (interior rows: ~88 % of the tiles
 // at 300^3) takes a branch-free path with no per-slot predicates; same operations, same order.
-template <int NW, int NST> struct SymmCfg {
+//
+// XS (experiment): x staged too, one window x[w_j, w_j + 32 NW + 4) per run j, w_j = r0 +
+// ((off_j - 1) rounded down to even), by one bulk copy each, for tiles whose windows lie inside
+// [0, ncols) and 16-byte aligned x.
+template <int NW, int NST, bool XS = false> struct SymmCfg {
     static constexpr int THREADS = 32 * (NW + 1);
     static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
     static constexpr int GS = NW + 2;                          // slices per mirror box
     static constexpr int MIR3_B = GS * 3 * 32 * 8;             // one 3-slot box
     static constexpr int MIR1_B = GS * 32 * 8;                 // the slot-12 box
     static constexpr int MIR0 = (VAL_B + SEG_B + MSK_B + 127) / 128 * 128;
-    static constexpr int STAGE_B = (MIR0 + 4 * MIR3_B + MIR1_B + 127) / 128 * 128;
+    static constexpr int X0 = (MIR0 + 4 * MIR3_B + MIR1_B + 127) / 128 * 128;
+    static constexpr int XW = 32 * NW + 4;
+    static constexpr int STAGE_B = XS ? (X0 + 9 * XW * 8 + 127) / 128 * 128 : X0;
     static constexpr int SMEM = NST * STAGE_B;
 };
+
+// offset of run j's window start from r0 (even; r0 is a multiple of 32)
+__device__ __forceinline__ int64_t symm_xwin_off(int j, int64_t N0, int64_t P) {
+    return ((j % 3 - 1) * N0 + (j / 3 - 1) * P - 1) & ~(int64_t)1;
+}
+__device__ __forceinline__ bool symm_x_staged(int64_t r0, int nw, int64_t N0, int64_t P,
+                                              int64_t ncols) {
+    return r0 - P - N0 - 2 >= 0 && r0 + P + N0 + 32 * nw + 4 <= ncols;
+}
 
 // first slice of mirror box g (0..4) of the tile whose first row is r0 (may be negative)
 __device__ __forceinline__ int symm_box_slice(int64_t r0, int g, int64_t N0, int64_t P) {
@@ -895,18 +910,32 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
 }
 
 constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots present
+#ifndef SYMM_EXP_LEVELS
+#define SYMM_EXP_LEVELS 2     // pAp expansion levels (exact.cuh); 3 spills registers (slower)
+#endif
 
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
 // row sum; xd = x of the row itself (slot 13).
-template <bool FULL, int GS>
+template <bool FULL, int GS, bool XSRC = false>
 __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const int (&sg)[9],
                                             unsigned msk, const double *vs, const double *mir,
-                                            const int (&madj)[5], int r0, double &xd) {
+                                            const int (&madj)[5], int r0, double &xd,
+                                            const double *xw = nullptr,
+                                            const int *xadj = nullptr) {
     auto on = [&](int t) { return FULL || ((msk >> t) & 1u); };
     double xv[27];
+    if (XSRC) {
 #pragma unroll
-    for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
+        for (int j = 0; j < 9; ++j) {
+            const double *xj = xw + xadj[j] + (sg[j] - r0);
+#pragma unroll
+            for (int e = 0; e < 3; ++e) xv[3 * j + e] = on(3 * j + e) ? xj[e] : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
+    }
     double lv[13];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {                     // runs 0..3: 3 slots; run 4: slot 12
@@ -929,11 +958,11 @@ __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const 
     return sum;
 }
 
-template <bool DOT, int NW, int NST>
-__global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
+template <bool DOT, int NW, int NST, bool XS = false>
+__global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
     k_spmv_symm(SpmvArgs a, const __grid_constant__ CUtensorMap tm3,
                 const __grid_constant__ CUtensorMap tm1) {
-    using C = SymmCfg<NW, NST>;
+    using C = SymmCfg<NW, NST, XS>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST];
     __shared__ unsigned long long sacc[ACC_WORDS];
@@ -976,11 +1005,22 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 const int nsl = rem < NW ? (int)rem : NW;
                 unsigned char *buf = smem + (size_t)st * C::STAGE_B;
                 const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
-                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B);
+                const int64_t r0 = s0 * 32;
+                const bool xs = XS && symm_x_staged(r0, NW, N0, P, a.g.ncols);
+                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B +
+                                                  (xs ? 9 * C::XW * 8 : 0));
                 bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &full_bar[st], pol_keep);
                 bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
                 bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
-                const int64_t r0 = s0 * 32;
+                if (xs) {
+                    uint64_t pol_x;
+                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;"
+                                 : "=l"(pol_x));
+#pragma unroll
+                    for (int j = 0; j < 9; ++j)
+                        bulk_g2s(buf + C::X0 + j * C::XW * 8, a.x + r0 + symm_xwin_off(j, N0, P),
+                                 C::XW * 8, &full_bar[st], pol_x);
+                }
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
                     tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
@@ -990,14 +1030,16 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             }
         }
     } else {
-        Expansion ex;
+        ExpansionL<SYMM_EXP_LEVELS> ex;
         ex.init();
         // box g of a tile starts at row r0 + K_g, K_g = 32 floor((off_g - 1) / 32): column c of
         // slot q sits at element madj[g] + q GS 32 + (c - r0) of the stage's mirror area
-        int madj[5];
+        int madj[5], xadj[9];
 #pragma unroll
         for (int g = 0; g < 5; ++g)
             madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
+#pragma unroll
+        for (int j = 0; j < 9; ++j) xadj[j] = j * C::XW - (int)symm_xwin_off(j, N0, P);
         int64_t i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
             const int st = (int)(i % NST);
@@ -1018,10 +1060,20 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
                 double sum, xd;
-                if (__all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL))
+                const bool full = __all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL);
+                const double *xw = reinterpret_cast<const double *>(buf + C::X0);
+                if (XS && symm_x_staged(r0, NW, N0, P, a.g.ncols)) {
+                    if (full)
+                        sum = symm_fold<true, C::GS, true>(a.x, sg, msk, vs, mir, madj, r0, xd,
+                                                           xw, xadj);
+                    else
+                        sum = symm_fold<false, C::GS, true>(a.x, sg, msk, vs, mir, madj, r0, xd,
+                                                            xw, xadj);
+                } else if (full) {
                     sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
-                else
+                } else {
                     sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
+                }
                 if (row >= 0) {
                     a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
@@ -1096,8 +1148,9 @@ __global__ void k_init_finalize(UpdArgs a, double tol) {
 // a3 + a4: finalise pAp -> alpha; x += alpha p; r -= alpha Ap; rr' = dot(r, r)
 // ----------------------------------------------------------------------------------------
 
+template <class EX>
 __device__ __forceinline__ void xr_step(double &x, double &r, double p, double ap, double alpha,
-                                        Expansion &ex, unsigned long long *sacc) {
+                                        EX &ex, unsigned long long *sacc) {
     x = __dadd_rn(x, __dmul_rn(alpha, p));
     r = __dsub_rn(r, __dmul_rn(alpha, ap));
     ex.add(__dmul_rn(r, r), sacc);
@@ -1168,7 +1221,8 @@ __device__ __forceinline__ int p_prologue(const UpdArgs &a, double rr_new, int k
 }
 
 // XL: x is updated by K7 (see launch_update_xr); K6 touches r only: 24 instead of 48 B/row.
-__device__ __forceinline__ void r_step(double &r, double ap, double alpha, Expansion &ex,
+template <class EX>
+__device__ __forceinline__ void r_step(double &r, double ap, double alpha, EX &ex,
                                        unsigned long long *sacc) {
     r = __dsub_rn(r, __dmul_rn(alpha, ap));
     ex.add(__dmul_rn(r, r), sacc);
@@ -1193,7 +1247,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     __syncthreads();
     if (s_stop) return;
     const double alpha = s_alpha;
-    Expansion ex;
+    Expansion2 ex;
     ex.init();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -2375,18 +2429,20 @@ static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) 
                CUDA_SUCCESS;
 }
 
-template <bool DOT, int NW, int NST>
+template <bool DOT, int NW, int NST, bool XS = false>
 static cudaError_t launch_symm(const SpmvArgs &a, cudaStream_t s) {
-    using C = SymmCfg<NW, NST>;
+    using C = SymmCfg<NW, NST, XS>;
+    static_assert(C::SMEM + 1536 <= 232448, "SYMM tile exceeds shared memory");
+    if (XS && (reinterpret_cast<uintptr_t>(a.x) & 15)) return cudaErrorNotSupported;
     CUtensorMap m3, m1;
     if (!sym_maps(a.m, C::GS, &m3, &m1)) return cudaErrorNotSupported;
     static unsigned long long attr_set = 0;
-    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST>, C::SMEM, attr_set);
+    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST, XS>, C::SMEM, attr_set);
     if (e != cudaSuccess) return e;
     query_occupancy();
     const int64_t ntiles = (a.m.nslices + NW - 1) / NW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
-    k_spmv_symm<DOT, NW, NST><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
+    k_spmv_symm<DOT, NW, NST, XS><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
     return cudaGetLastError();
 }
 
@@ -2402,7 +2458,19 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
         const char *e = getenv("MINIFE_SYM_CFG");
         cfg = e ? atoi(e) : 1;
     }
-    if (cfg == 1) {
+    if (cfg >= 2) {                                   // A/B of tile widths and x staging
+        cudaError_t e = cudaErrorNotSupported;
+        switch (cfg) {
+        case 2: e = launch_symm<DOT, 11, 2>(a, s); break;
+        case 3: e = launch_symm<DOT, 12, 2>(a, s); break;
+        case 4: e = launch_symm<DOT, 10, 2, true>(a, s); break;
+        case 5: e = launch_symm<DOT, 9, 2, true>(a, s); break;
+        case 6: e = launch_symm<DOT, 8, 2, true>(a, s); break;
+        default: break;
+        }
+        if (e != cudaErrorNotSupported) return e;
+    }
+    if (cfg >= 1) {
         const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
         static bool warned = false;
