@@ -972,6 +972,14 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
         vef = e ? atoi(e) : -1;
     }
     a.val_evict_first = vef >= 0 ? vef : (40.0 * (double)p.ncols < 64e6 ? 1 : 0);
+    // plane-ahead x prefetch into L2 when x itself does not stay L2-resident (B200, 300^3:
+    // 1.0806 -> 1.0757 ms per iteration; 100^3: no gain).  MINIFE_X_PREFETCH=0/1 forces it.
+    static int xpf = -2;
+    if (xpf == -2) {
+        const char *e = getenv("MINIFE_X_PREFETCH");
+        xpf = e ? atoi(e) : -1;
+    }
+    a.x_prefetch = xpf >= 0 ? xpf : (8.0 * (double)p.ncols > 64e6 ? 1 : 0);
     return a;
 }
 

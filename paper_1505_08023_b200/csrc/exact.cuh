@@ -137,86 +137,95 @@ struct Expansion {
 // and 32-bit shared atomics are native (the 64-bit ones are CAS loops).
 constexpr int ACC_DIG16 = 2 * ACC_DIGITS;
 
-__device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int *dig,
-                                                       unsigned long long *acc) {
+// One value per lane into the 16-bit digit counters, warp-aggregated (all lanes, converged)
+__device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned long long *acc) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    const unsigned long long frac = bits & 0xfffffffffffffull;
+    const bool nz = (e != 0 || frac != 0) && e != 0x7ff;
+    const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
+    const int pos = e ? e - 1 : 0;
+    const int d16 = pos >> 4, s16 = pos & 15;
+    const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
+    if (e == 0x7ff) acc_add(acc, v);                          // flag word
+    if (dmax1 == 0u) return;                                  // warp-uniform
+    const int lo = (int)dmax1 - 1 - 8;
+    const bool inwin = nz && d16 >= lo;
+    if (nz && !inwin) acc_add(acc, v);                        // far below: slow path
+    const unsigned long long mlo = m << s16;
+    const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
+    int ch[5];
+    ch[0] = (int)(mlo & 0xffff);
+    ch[1] = (int)((mlo >> 16) & 0xffff);
+    ch[2] = (int)((mlo >> 32) & 0xffff);
+    ch[3] = (int)(mlo >> 48);
+    ch[4] = (int)mhi;
+    if (bits >> 63) {
 #pragma unroll
-    for (int j = 0; j < NEXP; ++j) {
-        const double v = ex.c[j];
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-        const int e = (int)((bits >> 52) & 0x7ff);
-        const unsigned long long frac = bits & 0xfffffffffffffull;
-        const bool nz = (e != 0 || frac != 0) && e != 0x7ff;
-        const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
-        const int pos = e ? e - 1 : 0;
-        const int d16 = pos >> 4, s16 = pos & 15;
-        const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
-        if (e == 0x7ff) acc_add(acc, v);                      // flag word
-        if (dmax1 == 0u) continue;                            // warp-uniform
-        const int lo = (int)dmax1 - 1 - 8;
-        const bool inwin = nz && d16 >= lo;
-        if (nz && !inwin) acc_add(acc, v);                    // far below: slow path
-        const unsigned long long mlo = m << s16;
-        const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
-        int ch[5];
-        ch[0] = (int)(mlo & 0xffff);
-        ch[1] = (int)((mlo >> 16) & 0xffff);
-        ch[2] = (int)((mlo >> 32) & 0xffff);
-        ch[3] = (int)(mlo >> 48);
-        ch[4] = (int)mhi;
-        if (bits >> 63) {
+        for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
+    }
 #pragma unroll
-            for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
-        }
+    for (int t = 0; t < 13; ++t) {
+        const int D = lo + t;
+        const int q = D - d16;
+        int contrib = 0;
 #pragma unroll
-        for (int t = 0; t < 13; ++t) {
-            const int D = lo + t;
-            const int q = D - d16;
-            int contrib = 0;
-#pragma unroll
-            for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
-            const int sum = __reduce_add_sync(FULL, contrib);
-            if (lane == 0 && sum != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], sum);
-        }
+        for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
+        const int sum = __reduce_add_sync(FULL, contrib);
+        if (lane == 0 && sum != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], sum);
     }
 }
 
-// Two-level expansion for long per-thread sums: what the first expansion cannot hold (a term
-// far below its running total -- late in CG, the Dirichlet rows' tiny products) goes to a
-// second expansion instead of the shared-memory atomics, which only see what neither holds.
-// Exact like Expansion; costs nothing while the first level absorbs every term.
-// ExpansionL<3>: a third level for a third magnitude class.
-template <int L> struct ExpansionL {
-    Expansion lv[L];
+__device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int *dig,
+                                                       unsigned long long *acc) {
+#pragma unroll
+    for (int j = 0; j < NEXP; ++j) flush_value_digits(ex.c[j], dig, acc);
+}
+
+// Tiered expansion for long per-thread sums: what the first expansion (N1 terms) cannot hold
+// -- a term far below its running total, e.g. late in CG the Dirichlet rows' tiny products --
+// goes to a second one (N2 terms), then a third (N3, optional), and only what none holds
+// reaches the shared-memory atomics (64-bit CAS loops).  Exact like Expansion; costs nothing
+// while the first tier absorbs every term.
+template <int N1, int N2, int N3 = 0> struct ExpansionT {
+    double a[N1], b[N2], c[N3 > 0 ? N3 : 1];
     __device__ __forceinline__ void init() {
 #pragma unroll
-        for (int l = 0; l < L; ++l) lv[l].init();
+        for (int j = 0; j < N1; ++j) a[j] = 0.0;
+#pragma unroll
+        for (int j = 0; j < N2; ++j) b[j] = 0.0;
+#pragma unroll
+        for (int j = 0; j < N3; ++j) c[j] = 0.0;
     }
     __device__ __forceinline__ void add(double x, unsigned long long *spill) {
 #pragma unroll
-        for (int j = 0; j < NEXP; ++j) two_sum(lv[0].c[j], x, lv[0].c[j], x);
+        for (int j = 0; j < N1; ++j) two_sum(a[j], x, a[j], x);
         if (x != 0.0) {
 #pragma unroll
-            for (int l = 1; l < L - 1; ++l) {
+            for (int j = 0; j < N2; ++j) two_sum(b[j], x, b[j], x);
+            if (N3 > 0 && x != 0.0) {
 #pragma unroll
-                for (int j = 0; j < NEXP; ++j) two_sum(lv[l].c[j], x, lv[l].c[j], x);
+                for (int j = 0; j < N3; ++j) two_sum(c[j], x, c[j], x);
             }
-            lv[L - 1].add(x, spill);
+            if (x != 0.0) acc_add(spill, x);  // also routes NaN to the flag word
         }
     }
 };
-using Expansion2 = ExpansionL<2>;
+using Expansion2 = ExpansionT<NEXP, NEXP>;
 
-template <int L>
-__device__ __forceinline__ void expansion_flush_digits(const ExpansionL<L> &ex, int *dig,
+template <int N1, int N2, int N3>
+__device__ __forceinline__ void expansion_flush_digits(const ExpansionT<N1, N2, N3> &ex, int *dig,
                                                        unsigned long long *acc) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) expansion_flush_digits(ex.lv[l], dig, acc);
+    for (int j = 0; j < N1; ++j) flush_value_digits(ex.a[j], dig, acc);
+#pragma unroll
+    for (int j = 0; j < N2; ++j) flush_value_digits(ex.b[j], dig, acc);
+#pragma unroll
+    for (int j = 0; j < N3; ++j) flush_value_digits(ex.c[j], dig, acc);
 }
 
-// CTA accumulator = 64-bit words (slow path, flag) + 32-bit digit counters (warp flushes):
-// zero both (all threads), and add their sum into a global accumulator (all threads).
 __device__ __forceinline__ void acc_zero_shared(unsigned long long *s, int *dig) {
     for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) s[i] = 0ull;
     for (int i = threadIdx.x; i < ACC_DIG16; i += blockDim.x) dig[i] = 0;

@@ -910,9 +910,9 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
 }
 
 constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots present
-#ifndef SYMM_EXP_LEVELS
-#define SYMM_EXP_LEVELS 2     // pAp expansion levels (exact.cuh); 3 spills registers (slower)
-#endif
+// pAp expansion tiers (exact.cuh): 4 + 4 terms (4 + 2 + 2 measures the same; a third 4-term
+// tier spills registers at the 128-register cap of the 448-thread CTA)
+using SymmExpansion = ExpansionT<4, 4>;
 
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
@@ -1021,6 +1021,17 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
                         bulk_g2s(buf + C::X0 + j * C::XW * 8, a.x + r0 + symm_xwin_off(j, N0, P),
                                  C::XW * 8, &full_bar[st], pol_x);
                 }
+                if (a.x_prefetch) {
+                    // the tile's plane-ahead x (its dz = +1 runs) is read here for the first
+                    // time: start it into L2 now, so the consumers' gathers hit L2, not HBM
+                    int64_t lo = r0 + P - N0 - 1, hi = r0 + 32 * nsl + P + N0 + 1;
+                    lo = ((lo < 0 ? 0 : lo) + 1) & ~(int64_t)1;
+                    hi = (hi > a.g.ncols ? a.g.ncols : hi) & ~(int64_t)1;
+                    if (hi > lo && !(reinterpret_cast<uintptr_t>(a.x) & 15))
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + lo),
+                                     "r"((uint32_t)((hi - lo) * 8))
+                                     : "memory");
+                }
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
                     tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
@@ -1030,7 +1041,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
             }
         }
     } else {
-        ExpansionL<SYMM_EXP_LEVELS> ex;
+        SymmExpansion ex;
         ex.init();
         // box g of a tile starts at row r0 + K_g, K_g = 32 floor((off_g - 1) / 32): column c of
         // slot q sits at element madj[g] + q GS 32 + (c - r0) of the stage's mirror area

@@ -84,6 +84,7 @@ struct SpmvArgs {
     Geom g;
     int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
     int val_evict_first;                // SYMM: stream the values evict-first in L2
+    int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
     unsigned long long *acc;            // pAp accumulator (DOT only)
