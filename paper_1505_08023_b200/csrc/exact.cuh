@@ -205,6 +205,7 @@ template <int N1, int N2, int N3 = 0> struct ExpansionT {
         if (x != 0.0) {
 #pragma unroll
             for (int j = 0; j < N2; ++j) two_sum(b[j], x, b[j], x);
+
             if (N3 > 0 && x != 0.0) {
 #pragma unroll
                 for (int j = 0; j < N3; ++j) two_sum(c[j], x, c[j], x);

@@ -910,8 +910,11 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
 }
 
 constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots present
-// pAp expansion tiers (exact.cuh): 4 + 4 terms (4 + 2 + 2 measures the same; a third 4-term
-// tier spills registers at the 128-register cap of the 448-thread CTA)
+// pAp expansion (exact.cuh): two 4-term tiers.  Measured alternatives (profiles/r01/session3):
+// 4 + 2 + 2 the same; 2 parked spill slots drained into a 2-term tier once per tile 2.5 %
+// faster while nothing spills but far slower late in CG (the tier overflows into the atomics);
+// a 4-term drained tier or a third 4-term tier spills registers (128 per thread: 4 warps on
+// an SM sub-partition share its 16 K registers).
 using SymmExpansion = ExpansionT<4, 4>;
 
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
@@ -1668,6 +1671,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
     for (int e = tid; e < ACC_WORDS; e += CL_THREADS) S.sacc[e] = 0ull;
     // C6 step 1: x = 0, r = b, p = b (every CTA holds all of p), rr_0
     for (int64_t i = tid; i < rows; i += CL_THREADS) S.pfull[i] = a.b[i];
+    __syncthreads();                               // counters zeroed before any thread adds
     double xv[CL_RPT], rv[CL_RPT], apv[CL_RPT];
     Expansion ex;
     ex.init();
