@@ -1242,7 +1242,7 @@ __device__ __forceinline__ void r_step(double &r, double ap, double alpha, EX &e
     ex.add(__dmul_rn(r, r), sacc);
 }
 
-template <bool IDENT, bool XL>
+template <bool IDENT, bool XL, class EX = Expansion>
 __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) {
     __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
     __shared__ int sdig[ACC_DIG16];
@@ -1261,7 +1261,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     __syncthreads();
     if (s_stop) return;
     const double alpha = s_alpha;
-    Expansion2 ex;
+    EX ex;
     ex.init();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -2679,8 +2679,31 @@ static bool x_late() {
     return v == 1;
 }
 
+// rr expansion of K6: plain 4-term (default) or two 4-term tiers (exact.cuh; fewer divergent
+// spills late in CG, but 80 registers and fewer resident CTAs).  MINIFE_K6_EXP=2 selects the
+// tiered one (A/B).
+static int k6_exp() {
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("MINIFE_K6_EXP");
+        m = e ? atoi(e) : 1;
+    }
+    return m;
+}
+
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
     const bool xl = x_late() || a.alpha_hist;     // x-every-2 scheme: K6 updates r only
+    if (a.g.ident && xl && k6_exp() == 2) {
+        static int bps = 0;
+        if (!bps) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_update_xr<true, true, Expansion2>,
+                                                          UPD_THREADS, 0);
+            if (bps <= 0) bps = 1;
+        }
+        const int g = std::max(1, std::min(grid, g_sms * bps));
+        k_update_xr<true, true, Expansion2><<<g, UPD_THREADS, 0, s>>>(a, k);
+        return cudaGetLastError();
+    }
     if (a.g.ident) {
         if (xl) k_update_xr<true, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
         else k_update_xr<true, false><<<grid, UPD_THREADS, 0, s>>>(a, k);
