@@ -908,6 +908,15 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_box3_hint(void *dst, const CUtensorMap *tm, int c0, int c1,
+                                              int c2, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+        "l"(pol)
+        : "memory");
+}
 
 constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots present
 // pAp expansion (exact.cuh): two 4-term tiers.  Measured alternatives (profiles/r01/session3):
@@ -997,6 +1006,8 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
             uint64_t pol_keep;
             if (a.val_evict_first)
                 asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_keep));
+            else if (a.l2_flags & 2)
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
             else
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
             int64_t i = 0;
@@ -1035,12 +1046,22 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
                                      "r"((uint32_t)((hi - lo) * 8))
                                      : "memory");
                 }
+                if (a.l2_flags & 1) {
+                    // a mirrored value is dead after this read: drop it from L2 first
 #pragma unroll
-                for (int g = 0; g < 4; ++g)
-                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
-                             11 - 3 * g, &full_bar[st]);
-                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
-                         &full_bar[st]);
+                    for (int g = 0; g < 4; ++g)
+                        tma_box3_hint(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0,
+                                      symm_box_slice(r0, g, N0, P), 11 - 3 * g, &full_bar[st], pol);
+                    tma_box3_hint(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0,
+                                  symm_box_slice(r0, 4, N0, P), 1, &full_bar[st], pol);
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0,
+                                 symm_box_slice(r0, g, N0, P), 11 - 3 * g, &full_bar[st]);
+                    tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P),
+                             1, &full_bar[st]);
+                }
             }
         }
     } else {
@@ -1089,7 +1110,15 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
                     sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
                 }
                 if (row >= 0) {
-                    a.y[row] = sum;
+                    if (a.l2_flags & 4) {
+                        uint64_t ypol;
+                        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;"
+                                     : "=l"(ypol));
+                        asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;"
+                                     ::"l"(a.y + row), "d"(sum), "l"(ypol) : "memory");
+                    }
+                    else
+                        a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
                 }
             }
