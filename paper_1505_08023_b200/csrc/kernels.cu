@@ -144,23 +144,33 @@ __global__ void k_rowlen_widths(Geom g, uint8_t *row_len, uint8_t *width, int64_
 // a0.3 + a0.4 + a0.5: element operator, gather-assembly, Dirichlet elimination
 // ----------------------------------------------------------------------------------------
 
-// C1: K(d) for the 8 difference patterns d = dx | dy<<1 | dz<<2 of an (hx,hy,hz) brick.
-__device__ void element_operator(int nx, int ny, int nz, double K[8]) {
+// C1: K(d) for one of the 8 difference patterns d = dx | dy<<1 | dz<<2 of an (hx,hy,hz) brick.
+__device__ double element_operator_d(int nx, int ny, int nz, int d) {
     const double h[3] = {__ddiv_rn(1.0, (double)nx), __ddiv_rn(1.0, (double)ny),
                          __ddiv_rn(1.0, (double)nz)};
-    for (int d = 0; d < 8; ++d) {
-        double T[3];
-        for (int k = 0; k < 3; ++k) {
-            const bool dk = (d >> k) & 1;
-            const double g = __ddiv_rn(1.0, h[k]);
-            const double S = dk ? -g : g;
-            const int i = (k == 0) ? 1 : 0, j = (k == 2) ? 1 : 2;
-            const double Mi = ((d >> i) & 1) ? __ddiv_rn(h[i], 6.0) : __ddiv_rn(h[i], 3.0);
-            const double Mj = ((d >> j) & 1) ? __ddiv_rn(h[j], 6.0) : __ddiv_rn(h[j], 3.0);
-            T[k] = __dmul_rn(__dmul_rn(S, Mi), Mj);
-        }
-        K[d] = __dadd_rn(__dadd_rn(T[0], T[1]), T[2]);
+    double T[3];
+    for (int k = 0; k < 3; ++k) {
+        const bool dk = (d >> k) & 1;
+        const double g = __ddiv_rn(1.0, h[k]);
+        const double S = dk ? -g : g;
+        const int i = (k == 0) ? 1 : 0, j = (k == 2) ? 1 : 2;
+        const double Mi = ((d >> i) & 1) ? __ddiv_rn(h[i], 6.0) : __ddiv_rn(h[i], 3.0);
+        const double Mj = ((d >> j) & 1) ? __ddiv_rn(h[j], 6.0) : __ddiv_rn(h[j], 3.0);
+        T[k] = __dmul_rn(__dmul_rn(S, Mi), Mj);
     }
+    return __dadd_rn(__dadd_rn(T[0], T[1]), T[2]);
+}
+
+// C1 + C2 table of a CTA: sKc[d][c] = fold from +0.0 of c copies of K(d), c = 0..8; one
+// pattern per thread (threads 0..7)
+__device__ __forceinline__ void assembly_table(const Geom &g, double (*sKc)[9]) {
+    if (threadIdx.x < 8) {
+        const double K = element_operator_d(g.nx, g.ny, g.nz, threadIdx.x);
+        double v = 0.0;
+        sKc[threadIdx.x][0] = v;
+        for (int q = 1; q <= 8; ++q) sKc[threadIdx.x][q] = v = __dadd_rn(v, K);
+    }
+    __syncthreads();
 }
 
 // One thread per local row (all 32 lanes of the last slice run: padding lanes write the
@@ -171,20 +181,13 @@ __device__ void element_operator(int nx, int ny, int nz, double K[8]) {
 // global order b = fl(b - fl(A v)), then A = +0.0.  The pattern (incl. zeros) is kept.
 __global__ void k_assemble(AsmArgs a) {
     const Geom &g = a.g;
-    // C1 once per CTA (24 divisions), shared by its rows
-    // C1 once per CTA, and C2's folds of c copies of K(d) (c = 0..8) as a table
-    __shared__ double sK[8], sKc[8][9];
-    if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
-    __syncthreads();
-    if (threadIdx.x < 8) {
-        double v = 0.0;
-        sKc[threadIdx.x][0] = v;
-        for (int q = 1; q <= 8; ++q) sKc[threadIdx.x][q] = v = __dadd_rn(v, sK[threadIdx.x]);
-    }
-    __syncthreads();
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // C1 and C2's folds of c copies of K(d) (c = 0..8) as a table, once per CTA; the grid is
+    // a few CTAs per SM looping over the rows, so the divisions are not paid per 256 rows
+    __shared__ double sKc[8][9];
+    assembly_table(g, sKc);
     const int64_t nslices = (g.rows + 31) >> 5;
-    if ((row >> 5) >= nslices) return;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (row >> 5) < nslices;
+         row += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(row & 31);
     // CRS: row slice; SEG/SYM: storage position of the row's slice (interior-first order)
     const int64_t s = (a.fmt != FMT_CRS && a.slice_pos) ? (int64_t)a.slice_pos[row >> 5]
@@ -203,7 +206,7 @@ __global__ void k_assemble(AsmArgs a) {
             for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
             a.mask[s * 32 + lane] = 0u;            // mask is padded to 32 * slices
         }
-        return;
+        continue;
     }
     // value slot t of this row: SEG stores all 27 stencil slots, SYM the upper slots t >= 13
     // (both SELL-32, k-major)
@@ -275,6 +278,7 @@ __global__ void k_assemble(AsmArgs a) {
     }
     if (row_bc) b = (ix == g.nx) ? 1.0 : 0.0;
     a.b[row] = b;
+    }
 }
 
 // a0.2-a0.5 for FMT_SYM on a part with a halo: one thread per EXTENDED-box node (storage
@@ -284,26 +288,19 @@ __global__ void k_assemble(AsmArgs a) {
 // mask bit 31 marks owned nodes; b is written for owned rows only.
 __global__ void k_assemble_symx(AsmArgs a) {
     const Geom &g = a.g;
-    // C1 once per CTA, and C2's folds of c copies of K(d) (c = 0..8) as a table
-    __shared__ double sK[8], sKc[8][9];
-    if (threadIdx.x == 0) element_operator(g.nx, g.ny, g.nz, sK);
-    __syncthreads();
-    if (threadIdx.x < 8) {
-        double v = 0.0;
-        sKc[threadIdx.x][0] = v;
-        for (int q = 1; q <= 8; ++q) sKc[threadIdx.x][q] = v = __dadd_rn(v, sK[threadIdx.x]);
-    }
-    __syncthreads();
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // C1 and C2's fold table once per CTA; grid-stride over the extended box (as k_assemble)
+    __shared__ double sKc[8][9];
+    assembly_table(g, sKc);
     const int64_t nslices = (g.ncols + 31) >> 5;
-    if ((c >> 5) >= nslices) return;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (c >> 5) < nslices;
+         c += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(c & 31);
     const int64_t s = c >> 5;
     if (c >= g.ncols) {                            // padding lanes of the last slice
         for (int t = 0; t < 14; ++t) a.val[(14 * s + t) * 32 + lane] = 0.0;
         for (int j = 0; j < 9; ++j) a.seg[(9 * s + j) * 32 + lane] = 0;
         a.mask[c] = 0u;
-        return;
+        continue;
     }
     const unsigned u = (unsigned)c;
     const unsigned line = u / (unsigned)g.ext_n[0];
@@ -352,6 +349,7 @@ __global__ void k_assemble_symx(AsmArgs a) {
     }
     a.mask[c] = mask;
     if (row >= 0) a.b[row] = row_bc ? ((ix == g.nx) ? 1.0 : 0.0) : b;
+    }
 }
 
 // ----------------------------------------------------------------------------------------
@@ -2419,14 +2417,15 @@ cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width
     return cudaGetLastError();
 }
 
+// grid-stride: at most 8 CTAs of 256 threads per SM (each builds the C1/C2 table once)
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
-    if (a.fmt == FMT_SYM && !a.g.ident) {
-        const int64_t threads = ((a.g.ncols + 31) >> 5) * 32;
-        k_assemble_symx<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
-        return cudaGetLastError();
-    }
-    const int64_t threads = ((a.g.rows + 31) >> 5) * 32;
-    k_assemble<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+    query_occupancy();
+    const bool symx = a.fmt == FMT_SYM && !a.g.ident;
+    const int64_t threads = (((symx ? a.g.ncols : a.g.rows) + 31) >> 5) * 32;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((threads + 255) / 256,
+                                                                (int64_t)g_sms * 8));
+    if (symx) k_assemble_symx<<<(unsigned)grid, 256, 0, s>>>(a);
+    else k_assemble<<<(unsigned)grid, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
