@@ -922,7 +922,11 @@ constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots pres
 // faster while nothing spills but far slower late in CG (the tier overflows into the atomics);
 // a 4-term drained tier or a third 4-term tier spills registers (128 per thread: 4 warps on
 // an SM sub-partition share its 16 K registers).
-using SymmExpansion = ExpansionT<4, 4>;
+#ifndef SYMM_EXP_A
+#define SYMM_EXP_A 4
+#define SYMM_EXP_B 4
+#endif
+using SymmExpansion = ExpansionT<SYMM_EXP_A, SYMM_EXP_B>;
 
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
