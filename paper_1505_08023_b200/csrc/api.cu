@@ -980,12 +980,6 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
         xpf = e ? atoi(e) : -1;
     }
     a.x_prefetch = xpf >= 0 ? xpf : (8.0 * (double)p.ncols > 64e6 ? 1 : 0);
-    static int l2f = -2;
-    if (l2f == -2) {
-        const char *e = getenv("MINIFE_SYM_L2");
-        l2f = e ? atoi(e) : 0;
-    }
-    a.l2_flags = l2f;
     return a;
 }
 

@@ -865,31 +865,16 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
 //
 // A warp whose 32 rows all have the full 27-entry pattern (interior rows: ~88 % of the tiles
 // at 300^3) takes a branch-free path with no per-slot predicates; same operations, same order.
-//
-// XS (experiment): x staged too, one window x[w_j, w_j + 32 NW + 4) per run j, w_j = r0 +
-// ((off_j - 1) rounded down to even), by one bulk copy each, for tiles whose windows lie inside
-// [0, ncols) and 16-byte aligned x.
-template <int NW, int NST, bool XS = false> struct SymmCfg {
+template <int NW, int NST> struct SymmCfg {
     static constexpr int THREADS = 32 * (NW + 1);
     static constexpr int VAL_B = NW * 14 * 32 * 8, SEG_B = NW * 9 * 32 * 4, MSK_B = NW * 32 * 4;
     static constexpr int GS = NW + 2;                          // slices per mirror box
     static constexpr int MIR3_B = GS * 3 * 32 * 8;             // one 3-slot box
     static constexpr int MIR1_B = GS * 32 * 8;                 // the slot-12 box
     static constexpr int MIR0 = (VAL_B + SEG_B + MSK_B + 127) / 128 * 128;
-    static constexpr int X0 = (MIR0 + 4 * MIR3_B + MIR1_B + 127) / 128 * 128;
-    static constexpr int XW = 32 * NW + 4;
-    static constexpr int STAGE_B = XS ? (X0 + 9 * XW * 8 + 127) / 128 * 128 : X0;
+    static constexpr int STAGE_B = (MIR0 + 4 * MIR3_B + MIR1_B + 127) / 128 * 128;
     static constexpr int SMEM = NST * STAGE_B;
 };
-
-// offset of run j's window start from r0 (even; r0 is a multiple of 32)
-__device__ __forceinline__ int64_t symm_xwin_off(int j, int64_t N0, int64_t P) {
-    return ((j % 3 - 1) * N0 + (j / 3 - 1) * P - 1) & ~(int64_t)1;
-}
-__device__ __forceinline__ bool symm_x_staged(int64_t r0, int nw, int64_t N0, int64_t P,
-                                              int64_t ncols) {
-    return r0 - P - N0 - 2 >= 0 && r0 + P + N0 + 32 * nw + 4 <= ncols;
-}
 
 // first slice of mirror box g (0..4) of the tile whose first row is r0 (may be negative)
 __device__ __forceinline__ int symm_box_slice(int64_t r0, int g, int64_t N0, int64_t P) {
@@ -904,15 +889,6 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *tm, int c
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_box3_hint(void *dst, const CUtensorMap *tm, int c0, int c1,
-                                              int c2, uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
-        "l"(pol)
         : "memory");
 }
 
@@ -931,25 +907,14 @@ using SymmExpansion = ExpansionT<SYMM_EXP_A, SYMM_EXP_B>;
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
 // row sum; xd = x of the row itself (slot 13).
-template <bool FULL, int GS, bool XSRC = false>
+template <bool FULL, int GS>
 __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const int (&sg)[9],
                                             unsigned msk, const double *vs, const double *mir,
-                                            const int (&madj)[5], int r0, double &xd,
-                                            const double *xw = nullptr,
-                                            const int *xadj = nullptr) {
+                                            const int (&madj)[5], int r0, double &xd) {
     auto on = [&](int t) { return FULL || ((msk >> t) & 1u); };
     double xv[27];
-    if (XSRC) {
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-            const double *xj = xw + xadj[j] + (sg[j] - r0);
-#pragma unroll
-            for (int e = 0; e < 3; ++e) xv[3 * j + e] = on(3 * j + e) ? xj[e] : 0.0;
-        }
-    } else {
-#pragma unroll
-        for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
-    }
+    for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
     double lv[13];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {                     // runs 0..3: 3 slots; run 4: slot 12
@@ -972,11 +937,11 @@ __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const 
     return sum;
 }
 
-template <bool DOT, int NW, int NST, bool XS = false>
-__global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
+template <bool DOT, int NW, int NST>
+__global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     k_spmv_symm(SpmvArgs a, const __grid_constant__ CUtensorMap tm3,
                 const __grid_constant__ CUtensorMap tm1) {
-    using C = SymmCfg<NW, NST, XS>;
+    using C = SymmCfg<NW, NST>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST];
     __shared__ unsigned long long sacc[ACC_WORDS];
@@ -1008,8 +973,6 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
             uint64_t pol_keep;
             if (a.val_evict_first)
                 asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_keep));
-            else if (a.l2_flags & 2)
-                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
             else
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
             int64_t i = 0;
@@ -1022,21 +985,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
                 unsigned char *buf = smem + (size_t)st * C::STAGE_B;
                 const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
                 const int64_t r0 = s0 * 32;
-                const bool xs = XS && symm_x_staged(r0, NW, N0, P, a.g.ncols);
-                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B +
-                                                  (xs ? 9 * C::XW * 8 : 0));
+                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B);
                 bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &full_bar[st], pol_keep);
                 bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
                 bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
-                if (xs) {
-                    uint64_t pol_x;
-                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;"
-                                 : "=l"(pol_x));
-#pragma unroll
-                    for (int j = 0; j < 9; ++j)
-                        bulk_g2s(buf + C::X0 + j * C::XW * 8, a.x + r0 + symm_xwin_off(j, N0, P),
-                                 C::XW * 8, &full_bar[st], pol_x);
-                }
                 if (a.x_prefetch) {
                     // the tile's plane-ahead x (its dz = +1 runs) is read here for the first
                     // time: start it into L2 now, so the consumers' gathers hit L2, not HBM
@@ -1048,22 +1000,12 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
                                      "r"((uint32_t)((hi - lo) * 8))
                                      : "memory");
                 }
-                if (a.l2_flags & 1) {
-                    // a mirrored value is dead after this read: drop it from L2 first
 #pragma unroll
-                    for (int g = 0; g < 4; ++g)
-                        tma_box3_hint(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0,
-                                      symm_box_slice(r0, g, N0, P), 11 - 3 * g, &full_bar[st], pol);
-                    tma_box3_hint(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0,
-                                  symm_box_slice(r0, 4, N0, P), 1, &full_bar[st], pol);
-                } else {
-#pragma unroll
-                    for (int g = 0; g < 4; ++g)
-                        tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0,
-                                 symm_box_slice(r0, g, N0, P), 11 - 3 * g, &full_bar[st]);
-                    tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P),
-                             1, &full_bar[st]);
-                }
+                for (int g = 0; g < 4; ++g)
+                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
+                             11 - 3 * g, &full_bar[st]);
+                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
+                         &full_bar[st]);
             }
         }
     } else {
@@ -1071,12 +1013,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
         ex.init();
         // box g of a tile starts at row r0 + K_g, K_g = 32 floor((off_g - 1) / 32): column c of
         // slot q sits at element madj[g] + q GS 32 + (c - r0) of the stage's mirror area
-        int madj[5], xadj[9];
+        int madj[5];
 #pragma unroll
         for (int g = 0; g < 5; ++g)
             madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
-#pragma unroll
-        for (int j = 0; j < 9; ++j) xadj[j] = j * C::XW - (int)symm_xwin_off(j, N0, P);
         int64_t i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
             const int st = (int)(i % NST);
@@ -1097,30 +1037,12 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST, XS>::THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
                 double sum, xd;
-                const bool full = __all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL);
-                const double *xw = reinterpret_cast<const double *>(buf + C::X0);
-                if (XS && symm_x_staged(r0, NW, N0, P, a.g.ncols)) {
-                    if (full)
-                        sum = symm_fold<true, C::GS, true>(a.x, sg, msk, vs, mir, madj, r0, xd,
-                                                           xw, xadj);
-                    else
-                        sum = symm_fold<false, C::GS, true>(a.x, sg, msk, vs, mir, madj, r0, xd,
-                                                            xw, xadj);
-                } else if (full) {
+                if (__all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL))
                     sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
-                } else {
+                else
                     sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
-                }
                 if (row >= 0) {
-                    if (a.l2_flags & 4) {
-                        uint64_t ypol;
-                        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;"
-                                     : "=l"(ypol));
-                        asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;"
-                                     ::"l"(a.y + row), "d"(sum), "l"(ypol) : "memory");
-                    }
-                    else
-                        a.y[row] = sum;
+                    a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
                 }
             }
@@ -2476,20 +2398,19 @@ static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) 
                CUDA_SUCCESS;
 }
 
-template <bool DOT, int NW, int NST, bool XS = false>
+template <bool DOT, int NW, int NST>
 static cudaError_t launch_symm(const SpmvArgs &a, cudaStream_t s) {
-    using C = SymmCfg<NW, NST, XS>;
+    using C = SymmCfg<NW, NST>;
     static_assert(C::SMEM + 1536 <= 232448, "SYMM tile exceeds shared memory");
-    if (XS && (reinterpret_cast<uintptr_t>(a.x) & 15)) return cudaErrorNotSupported;
     CUtensorMap m3, m1;
     if (!sym_maps(a.m, C::GS, &m3, &m1)) return cudaErrorNotSupported;
     static unsigned long long attr_set = 0;
-    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST, XS>, C::SMEM, attr_set);
+    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST>, C::SMEM, attr_set);
     if (e != cudaSuccess) return e;
     query_occupancy();
     const int64_t ntiles = (a.m.nslices + NW - 1) / NW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
-    k_spmv_symm<DOT, NW, NST, XS><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
+    k_spmv_symm<DOT, NW, NST><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
     return cudaGetLastError();
 }
 
@@ -2505,19 +2426,7 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
         const char *e = getenv("MINIFE_SYM_CFG");
         cfg = e ? atoi(e) : 1;
     }
-    if (cfg >= 2) {                                   // A/B of tile widths and x staging
-        cudaError_t e = cudaErrorNotSupported;
-        switch (cfg) {
-        case 2: e = launch_symm<DOT, 11, 2>(a, s); break;
-        case 3: e = launch_symm<DOT, 12, 2>(a, s); break;
-        case 4: e = launch_symm<DOT, 10, 2, true>(a, s); break;
-        case 5: e = launch_symm<DOT, 9, 2, true>(a, s); break;
-        case 6: e = launch_symm<DOT, 8, 2, true>(a, s); break;
-        default: break;
-        }
-        if (e != cudaErrorNotSupported) return e;
-    }
-    if (cfg >= 1) {
+    if (cfg == 1) {
         const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
         static bool warned = false;
@@ -2711,31 +2620,8 @@ static bool x_late() {
     return v == 1;
 }
 
-// rr expansion of K6: plain 4-term (default) or two 4-term tiers (exact.cuh; fewer divergent
-// spills late in CG, but 80 registers and fewer resident CTAs).  MINIFE_K6_EXP=2 selects the
-// tiered one (A/B).
-static int k6_exp() {
-    static int m = -1;
-    if (m < 0) {
-        const char *e = getenv("MINIFE_K6_EXP");
-        m = e ? atoi(e) : 1;
-    }
-    return m;
-}
-
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
     const bool xl = x_late() || a.alpha_hist;     // x-every-2 scheme: K6 updates r only
-    if (a.g.ident && xl && k6_exp() == 2) {
-        static int bps = 0;
-        if (!bps) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_update_xr<true, true, Expansion2>,
-                                                          UPD_THREADS, 0);
-            if (bps <= 0) bps = 1;
-        }
-        const int g = std::max(1, std::min(grid, g_sms * bps));
-        k_update_xr<true, true, Expansion2><<<g, UPD_THREADS, 0, s>>>(a, k);
-        return cudaGetLastError();
-    }
     if (a.g.ident) {
         if (xl) k_update_xr<true, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
         else k_update_xr<true, false><<<grid, UPD_THREADS, 0, s>>>(a, k);

@@ -85,8 +85,6 @@ struct SpmvArgs {
     int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
     int val_evict_first;                // SYMM: stream the values evict-first in L2
     int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
-    int l2_flags;                       // SYMM L2 policies (A/B): 1 mirror boxes evict-first,
-                                        // 2 value stream evict-last, 4 y stores evict-first
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
     unsigned long long *acc;            // pAp accumulator (DOT only)
