@@ -185,6 +185,20 @@ def test_x_every_second_iteration_bit_identical(n, fmt):
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
+def test_cluster_solver_after_spmv_leftovers():
+    """The one-cluster solver right after SpMV launches that fill every SM's shared memory
+    with other data: 20 solves, each bitwise the oracle (subprocess: MINIFE_SMALL is read once
+    per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MINIFE_SMALL="2")
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "_cluster_after_spmv.py")], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 def test_timing_window_inside_the_solve():
     """minife_set_timing_window: events around the SpMVs of a range of iterations are part of
     the solve graph; the results stay bitwise the oracle's; the window needs a solve that ran
