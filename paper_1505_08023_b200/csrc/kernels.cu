@@ -1806,11 +1806,38 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             if (!stop) a.p[j] = __dadd_rn(a.r[j], __dmul_rn(beta, pj));
         }
     } else {
-        for (int64_t i = tid; i < rows; i += stride) {
-            const int64_t c = row_to_col(a.g, i);
-            const double pc = a.p[c];
-            if (XL) a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc));
-            if (!stop) a.p[c] = __dadd_rn(a.r[i], __dmul_rn(beta, pc));
+        // a part with a halo: p lives in extended-box order.  One warp per owned x-line
+        // (own_n0 consecutive rows <-> own_n0 consecutive columns): one division per line
+        // instead of two per row, coalesced, four elements per lane in flight
+        const int64_t n0 = a.g.own_n[0], n1 = a.g.own_n[1];
+        const int64_t nlines = n1 * a.g.own_n[2];
+        const int64_t E0 = a.g.ext_n[0], E1 = a.g.ext_n[1];
+        const int lane = threadIdx.x & 31;
+        const int64_t wid = tid >> 5, nw = stride >> 5;
+        for (int64_t line = wid; line < nlines; line += nw) {
+            const int64_t lz = line / n1, ly = line - lz * n1;
+            const int64_t i0 = line * n0;
+            const int64_t c0 = a.g.off[0] + E0 * ((ly + a.g.off[1]) + E1 * (lz + a.g.off[2]));
+            for (int64_t lx = lane; lx < n0; lx += 4 * 32) {
+                double pc[4], xi[4], ri[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t e = lx + 32 * u;
+                    if (e < n0) {
+                        pc[u] = a.p[c0 + e];
+                        if (XL) xi[u] = a.x[i0 + e];
+                        ri[u] = a.r[i0 + e];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t e = lx + 32 * u;
+                    if (e < n0) {
+                        if (XL) a.x[i0 + e] = __dadd_rn(xi[u], __dmul_rn(alpha, pc[u]));
+                        if (!stop) a.p[c0 + e] = __dadd_rn(ri[u], __dmul_rn(beta, pc[u]));
+                    }
+                }
+            }
         }
     }
 }
