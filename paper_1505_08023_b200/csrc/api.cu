@@ -1223,13 +1223,18 @@ static bool x2_mode(const minife_ctx *c) {
     }
     // only where the vectors stream from HBM anyway (B200: 300^3 -1.0 % per iteration; at
     // 100^3, whose vectors sit in L2, the second p buffer costs +0.7 %)
-    return env && c->parts.size() == 1 && c->world == 1 && !fused_mode(c) &&
+    // partitioned (SYM with a halo, halo overlapped with K7 over the wire or device copies):
+    // the exchange fills the halo of the buffer p_(k+1) goes to
+    const bool single = c->parts.size() == 1 && c->world == 1;
+    const bool parts_ok = overlap_sym(c) && !push_mode(c);
+    return env && (single || parts_ok) && !fused_mode(c) &&
            (env == 2 || 40.0 * (double)c->parts[0].ncols >= 64e6);   // 2: any size (tests)
 }
 
 static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
-    if ((fused_mode(c) || x2_mode(c)) && !c->parts[0].d_p2) {
-        Part &p = c->parts[0];
+    if (!(fused_mode(c) || x2_mode(c))) return MINIFE_OK;
+    for (auto &p : c->parts) {
+        if (p.d_p2) continue;
         DevGuard g(p.dev);
         TRY(alloc_colvec(c, p, &p.d_p2));
     }
@@ -1261,18 +1266,61 @@ static int small_mode(const minife_ctx *c) {
 static double *x2_pbuf(const Part &p, int k) { return (k & 1) ? p.d_p : p.d_p2; }
 
 static int enqueue_iteration_x2(minife_ctx *c, int k) {
-    Part &p = c->parts[0];
-    DevGuard g(p.dev);
-    cudaStream_t s = launch_stream(c, p);
+    const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
+    const bool halo = c->parts.size() > 1 || c->world > 1;
     TRY(tw_mark(c, k, false));
-    CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(p, k), p.d_Ap, true), true, p.grid_spmv, s));
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(p, k), p.d_Ap, true), true, p.grid_spmv,
+                                launch_stream(c, p)));
+    }
     TRY(tw_mark(c, k, true));
-    UpdArgs u6 = upd_args(c, p, 0);
-    u6.alpha_hist = p.d_alpha;
-    CUDA_TRY(c, launch_update_xr(u6, k, p.grid_upd, s));
-    UpdArgs u7 = upd_args(c, p, 1);
-    u7.alpha_hist = p.d_alpha;
-    CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(p, k), x2_pbuf(p, k + 1), p.grid_upd, s));
+    TRY(enqueue_allreduce(c, 0));
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        UpdArgs u6 = upd_args(c, p, 0);
+        u6.alpha_hist = p.d_alpha;
+        CUDA_TRY(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
+    }
+    TRY(enqueue_allreduce(c, 1));
+    if (halo) {
+        // as enqueue_k7_with_halo: the send slots' p_(k+1) ahead of K7, exchanged on the
+        // transport stream into the halo of the buffer p_(k+1) goes to, while K7 runs
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs a = upd_args(c, p, 1);
+            a.p = x2_pbuf(p, k);
+            CUDA_TRY(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
+                                           (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
+        }
+        for (auto &p : c->parts) {
+            if (virt && &p != &c->parts[0]) break;
+            DevGuard g(p.dev);
+            CUDA_TRY(c, cudaEventRecord(p.ev_fork, launch_stream(c, p)));
+            CUDA_TRY(c, cudaStreamWaitEvent(p.cstream, p.ev_fork, 0));
+        }
+        if (k & 1) TRY(enqueue_halo(c, [](Part &p) { return p.d_p2; }, true, true));
+        else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }, true, true));
+        for (auto &p : c->parts) {
+            if (virt && &p != &c->parts[0]) break;
+            DevGuard g(p.dev);
+            CUDA_TRY(c, cudaEventRecord(p.ev_join, p.cstream));
+        }
+    }
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        UpdArgs u7 = upd_args(c, p, 1);
+        u7.alpha_hist = p.d_alpha;
+        CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(p, k), x2_pbuf(p, k + 1), p.grid_upd,
+                                     launch_stream(c, p)));
+    }
+    if (halo) {
+        for (auto &p : c->parts) {
+            if (virt && &p != &c->parts[0]) break;
+            DevGuard g(p.dev);
+            CUDA_TRY(c, cudaStreamWaitEvent(launch_stream(c, p), p.ev_join, 0));
+        }
+    }
     return MINIFE_OK;
 }
 
@@ -1280,12 +1328,15 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
     if (!t) c->tw_armed = false;
     if (!t && x2_mode(c) && !small_mode(c)) {
         TRY(enqueue_init(c, tol));
+        if (c->parts.size() > 1 || c->world > 1)      // halo of p_1 = b (buffer of odd k)
+            TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
         for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration_x2(c, k));
-        Part &p = c->parts[0];
-        DevGuard g(p.dev);
-        UpdArgs u = upd_args(c, p, 0);
-        u.alpha_hist = p.d_alpha;
-        CUDA_TRY(c, launch_x2_finish(u, p.d_p, p.d_p2, launch_stream(c, p)));
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs u = upd_args(c, p, 0);
+            u.alpha_hist = p.d_alpha;
+            CUDA_TRY(c, launch_x2_finish(u, p.d_p, p.d_p2, launch_stream(c, p)));
+        }
         return MINIFE_OK;
     }
     const int sm = t ? 0 : small_mode(c);

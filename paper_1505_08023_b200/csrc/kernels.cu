@@ -1846,6 +1846,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
 // iteration k is fl(x + fl(alpha_k p_k)) exactly as in K7; it is only deferred by one
 // iteration on odd k, so p_(k+1) goes to the other buffer and p_(k-1) survives until the
 // next (even) K7, which applies both updates in order with one pass over x.
+template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, const double *pk,
                                                            double *po) {
     __shared__ unsigned long long s_in[ACC_WORDS];
@@ -1879,6 +1880,43 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
         if (upx) x = __dadd_rn(x, __dmul_rn(ak, p));           // alpha_k p_k
         if (!stop) po_ = __dadd_rn(r, __dmul_rn(beta, p));     // p_(k+1)
     };
+    if (!IDENT) {
+        // a part with a halo: p buffers in extended-box order, one warp per owned x-line (as
+        // k_update_p); the halo columns of po are written by the exchange meanwhile
+        const int64_t n0 = a.g.own_n[0], n1 = a.g.own_n[1];
+        const int64_t nlines = n1 * a.g.own_n[2];
+        const int64_t E0 = a.g.ext_n[0], E1 = a.g.ext_n[1];
+        const int lane = threadIdx.x & 31;
+        for (int64_t line = tid >> 5; line < nlines; line += stride >> 5) {
+            const int64_t lz = line / n1, ly = line - lz * n1;
+            const int64_t i0 = line * n0;
+            const int64_t c0 = a.g.off[0] + E0 * ((ly + a.g.off[1]) + E1 * (lz + a.g.off[2]));
+            for (int64_t lx = lane; lx < n0; lx += 4 * 32) {
+                double pv[4], ov[4], xv[4], rv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t e = lx + 32 * u;
+                    ov[u] = xv[u] = rv[u] = 0.0;
+                    if (e < n0) {
+                        pv[u] = pk[c0 + e];
+                        if (even) ov[u] = po[c0 + e];
+                        if (upx) xv[u] = a.x[i0 + e];
+                        if (!stop) rv[u] = a.r[i0 + e];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t e = lx + 32 * u;
+                    if (e < n0) {
+                        step(xv[u], ov[u], rv[u], pv[u]);
+                        if (upx) a.x[i0 + e] = xv[u];
+                        if (!stop) po[c0 + e] = ov[u];
+                    }
+                }
+            }
+        }
+        return;
+    }
     for (int64_t i = tid; i < n2; i += stride) {
         const double2 pv = pk2[i];
         double2 ov = make_double2(0.0, 0.0), xv = make_double2(0.0, 0.0), rv = make_double2(0.0, 0.0);
@@ -1900,6 +1938,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
 }
 
 // After the loop: the x update of the last iteration with an alpha, if still pending.
+template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_x2_finish(UpdArgs a, const double *p_odd,
                                                            const double *p_even) {
     const int j = a.st->x_done + 1;
@@ -1908,7 +1947,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_x2_finish(UpdArgs a, const doub
     const double *p = (j & 1) ? p_odd : p_even;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride)
-        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, p[i]));
+        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, p[IDENT ? i : row_to_col(a.g, i)]));
 }
 
 // Halo values of p_(k+1) computed ahead of K7 (SYM with a halo): the packed
@@ -2614,13 +2653,15 @@ cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *
     const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
     const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
     (void)grid;
-    k_update_p2<<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    if (a.g.ident) k_update_p2<true><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    else k_update_p2<false><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
     return cudaGetLastError();
 }
 
 cudaError_t launch_x2_finish(const UpdArgs &a, const double *p_odd, const double *p_even,
                              cudaStream_t s) {
-    k_x2_finish<<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
+    if (a.g.ident) k_x2_finish<true><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
+    else k_x2_finish<false><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
     return cudaGetLastError();
 }
 
