@@ -1406,8 +1406,9 @@ static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, doub
         res->seconds = seconds;
         const double rows = (double)c->mesh.rows(), nnz = (double)c->mesh.nnz();
         res->flops = (double)st.iters * (2.0 * nnz + 10.0 * rows);
-        // vector bytes per row: 80 (three-kernel scheme, x updated with p) or 72 (fused)
-        const double vec = fused_mode(c) ? 72.0 : 80.0;
+        // vector bytes per row: 80 (three-kernel scheme, x updated with p), 76 (x every
+        // second iteration: K7 moves 24 and 48 B/row alternately) or 72 (fused)
+        const double vec = fused_mode(c) ? 72.0 : (x2_mode(c) && !small_mode(c) ? 76.0 : 80.0);
         double bytes = 0.0;
         for (auto &q : c->parts) bytes += spmv_alg_bytes(c, q) + vec * (double)q.rows;
         res->bytes = (double)st.iters * bytes;
