@@ -989,8 +989,15 @@ static int tw_mark(minife_ctx *c, int k, bool end) {
     Part &p = c->parts[0];
     DevGuard g(p.dev);
     // External: a real event-record node when the stream is being captured into the graph
-    CUDA_TRY(c, cudaEventRecordWithFlags(c->tw_ev[2 * (k - c->tw_k0) + (end ? 1 : 0)],
-                                         launch_stream(c, p), cudaEventRecordExternal));
+    // (a plain record when the solve is enqueued directly, MULTI ctxs or MINIFE_GRAPH=0)
+    cudaStream_t s = launch_stream(c, p);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(c, cudaStreamIsCapturing(s, &cs));
+    cudaEvent_t ev = c->tw_ev[2 * (k - c->tw_k0) + (end ? 1 : 0)];
+    if (cs == cudaStreamCaptureStatusActive)
+        CUDA_TRY(c, cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+    else
+        CUDA_TRY(c, cudaEventRecord(ev, s));
     if (end && k == c->tw_k0 + c->tw_n - 1) c->tw_armed = true;
     return MINIFE_OK;
 }
@@ -1431,14 +1438,21 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
     DevGuard g(p0.dev);
-    if (c->mode == MINIFE_MODE_MULTI) {
+    // MINIFE_GRAPH=0: enqueue every solve directly instead of replaying a captured graph
+    // (an escape hatch for environments where capturing the NCCL calls of RANK ctxs fails)
+    static int graphs = -1;
+    if (graphs < 0) {
+        const char *e = getenv("MINIFE_GRAPH");
+        graphs = e ? atoi(e) : 1;
+    }
+    if (c->mode == MINIFE_MODE_MULTI || !graphs) {
         // one host thread drives every device: launch the sequence directly
-        CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev0, launch_stream(c, p0)));
         TRY(enqueue_solve(c, max_iters, tol, nullptr));
-        CUDA_TRY(c, cudaEventRecord(c->ev1, p0.stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev1, launch_stream(c, p0)));
         for (auto &p : c->parts) {
             DevGuard gg(p.dev);
-            CUDA_TRY(c, cudaStreamSynchronize(p.stream));
+            CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
         }
     } else {
         if (!c->gexec || c->g_iters != max_iters || c->g_tol != tol) {
