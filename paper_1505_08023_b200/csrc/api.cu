@@ -158,6 +158,7 @@ struct minife_ctx {
     int tw_k0 = 0, tw_n = 0;
     std::vector<cudaEvent_t> tw_ev;              // [2 * tw_n]: start, end of each SpMV
     bool tw_armed = false;                       // the enqueued solve records the window
+    bool eager = false;                          // capture failed once (world > 1): no graphs
     // last solve
     int last_iters = 0;
     bool solved = false;
@@ -1445,7 +1446,39 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         const char *e = getenv("MINIFE_GRAPH");
         graphs = e ? atoi(e) : 1;
     }
-    if (c->mode == MINIFE_MODE_MULTI || !graphs) {
+    bool eager = c->mode == MINIFE_MODE_MULTI || !graphs || c->eager;
+    if (!eager && (!c->gexec || c->g_iters != max_iters || c->g_tol != tol)) {
+        drop_graph(c);
+        // capture on the ctx's own stream (a torch stream may be the legacy default one)
+        cudaStream_t cap = p0.stream;
+        cudaStream_t saved = c->user_stream;
+        c->user_stream = nullptr;
+        CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        int st = enqueue_solve(c, max_iters, tol, nullptr);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cap, &graph);
+        c->user_stream = saved;
+        if (st == MINIFE_OK && e == cudaSuccess) {
+            e = cudaGraphInstantiate(&c->gexec, graph, 0);
+            if (e != cudaSuccess) c->gexec = nullptr;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (st != MINIFE_OK || e != cudaSuccess) {
+            // a multi-rank job whose capture failed (every rank takes the same path) runs
+            // this and later solves directly; anything else is an error
+            if (c->world > 1 && c->mode == MINIFE_MODE_RANK) {
+                cudaGetLastError();
+                c->eager = eager = true;
+            } else {
+                if (st != MINIFE_OK) return st;
+                CUDA_TRY(c, e);
+            }
+        } else {
+            c->g_iters = max_iters;
+            c->g_tol = tol;
+        }
+    }
+    if (eager) {
         // one host thread drives every device: launch the sequence directly
         CUDA_TRY(c, cudaEventRecord(c->ev0, launch_stream(c, p0)));
         TRY(enqueue_solve(c, max_iters, tol, nullptr));
@@ -1455,28 +1488,6 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
             CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
         }
     } else {
-        if (!c->gexec || c->g_iters != max_iters || c->g_tol != tol) {
-            drop_graph(c);
-            // capture on the ctx's own stream (a torch stream may be the legacy default one)
-            cudaStream_t cap = p0.stream;
-            cudaStream_t saved = c->user_stream;
-            c->user_stream = nullptr;
-            CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-            int st = enqueue_solve(c, max_iters, tol, nullptr);
-            cudaGraph_t graph = nullptr;
-            cudaError_t e = cudaStreamEndCapture(cap, &graph);
-            c->user_stream = saved;
-            if (st != MINIFE_OK) {
-                if (graph) cudaGraphDestroy(graph);
-                return st;
-            }
-            CUDA_TRY(c, e);
-            e = cudaGraphInstantiate(&c->gexec, graph, 0);
-            cudaGraphDestroy(graph);
-            CUDA_TRY(c, e);
-            c->g_iters = max_iters;
-            c->g_tol = tol;
-        }
         cudaStream_t s = launch_stream(c, p0);
         CUDA_TRY(c, cudaEventRecord(c->ev0, s));
         CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
