@@ -1041,13 +1041,17 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                     sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
                 else
                     sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
+                // every value of the stage is in registers: release it before the epilogue
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[st]);
                 if (row >= 0) {
                     a.y[row] = sum;
                     if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
                 }
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[st]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[st]);
         }
         if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
