@@ -1041,7 +1041,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                     sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
                 else
                     sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
-                // every value of the stage is in registers: release it before the epilogue
+                // every value of the stage has been consumed by the fold: release it before
+                // the epilogue (the empty asm pins the fold's result ahead of the arrive, so
+                // no shared-memory read of the stage can still be in flight)
+                asm volatile("" ::"d"(sum) : "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[st]);
                 if (row >= 0) {
