@@ -64,8 +64,9 @@ extern "C" {
 #define MINIFE_SCHEME_3K 0     /* per iteration: SpMV + pAp | r update + rr | x and p update   */
                                /* (x += alpha p with the p read for the p update).  Default. */
                                /* 12 nnz-class bytes + 80 B per row.  Parts whose vectors     */
-                               /* exceed L2 apply the x update every second iteration (two   */
-                               /* updates in order in one pass; same arithmetic, 76 B/row).  */
+                               /* exceed L2 apply the x update every 8th iteration (8 updates */
+                               /* in order in one pass over a ring of 8 p buffers; same       */
+                               /* arithmetic, 73 B/row).                                      */
 #define MINIFE_SCHEME_FUSED 1  /* SURVEY §8(f) NEXT #2, one part + MINIFE_FMT_SEG only (other */
                                /* ctxs run 3K): the p update is formed at gather time inside  */
                                /* the SpMV and x is updated one iteration late there; a second */

@@ -89,6 +89,7 @@ struct Part {
     // vectors: b, x, r, Ap in row (owned) order; p in column (extended-box) order
     double *d_b = nullptr, *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
     double *d_p2 = nullptr;                       // fused scheme: second p buffer (lazy)
+    double *d_pr[XDEF_MAX] = {};                  // deferred x: ring buffers 2.. (lazy)
     double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
     // exact accumulators, parity double-buffered: [pAp_0, rr_0, pAp_1, rr_1] x ACC_WORDS
     unsigned long long *d_acc = nullptr;
@@ -121,6 +122,7 @@ struct Part {
         return d_acc + (2 * (par & 1) + 1) * ACC_WORDS;
     }
     double *p_buf(int k) const { return (k & 1) ? d_p2 : d_p; }   // fused: p_k lives in k % 2
+    double *ring(int i) const { return i == 0 ? d_p : (i == 1 ? d_p2 : d_pr[i]); }
 };
 
 struct DevGuard {
@@ -254,6 +256,8 @@ static void free_part(Part &p) {
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
                     p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha};
     for (void *b : bufs)
+        if (b) cudaFree(b);
+    for (double *b : p.d_pr)
         if (b) cudaFree(b);
     if (p.comm) nccl()->CommDestroy(p.comm);
     if (p.ev_push) cudaEventDestroy(p.ev_push);
@@ -1223,28 +1227,37 @@ static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
 // alpha_(k-1) p_(k-1) and alpha_k p_k in one pass over x.  x then costs 16 B per row every
 // second iteration (36 instead of 40 B/row per K7 on average); same operations, same order:
 // bit-identical.  MINIFE_X2=0 disables.
-static bool x2_mode(const minife_ctx *c) {
+// Deferred x: x += alpha_k p_k is applied X iterations at a time, p_k living
+// in a ring of X buffers.  Returns X, or 0 when off.  MINIFE_X2=0 disables it; MINIFE_X2=n
+// (2..8) forces X = n at any size (tests); unset: X = XDEF_DEFAULT where the vectors stream
+// from HBM anyway (B200, 300^3 per iteration: X = 2 -1.0 % against no deferral, X = 4 a
+// further -0.5 %, X = 8 -1.1 %; K7 moves 24 B/row plus (16 + 8 (X-1)) / X for x; at 100^3,
+// whose vectors sit in L2, a second p buffer costs +0.7 %).
+constexpr int XDEF_DEFAULT = 8;
+static int xdef_of(const minife_ctx *c) {
     static int env = -1;
     if (env < 0) {
         const char *e = getenv("MINIFE_X2");
         env = e ? atoi(e) : 1;
     }
-    // only where the vectors stream from HBM anyway (B200: 300^3 -1.0 % per iteration; at
-    // 100^3, whose vectors sit in L2, the second p buffer costs +0.7 %)
     // partitioned (SYM with a halo, halo overlapped with K7 over the wire or device copies):
     // the exchange fills the halo of the buffer p_(k+1) goes to
     const bool single = c->parts.size() == 1 && c->world == 1;
     const bool parts_ok = overlap_sym(c) && !push_mode(c);
-    return env && (single || parts_ok) && !fused_mode(c) &&
-           (env == 2 || 40.0 * (double)c->parts[0].ncols >= 64e6);   // 2: any size (tests)
+    if (!env || !(single || parts_ok) || fused_mode(c)) return 0;
+    if (env >= 2) return std::min(env, XDEF_MAX);
+    return 40.0 * (double)c->parts[0].ncols >= 64e6 ? XDEF_DEFAULT : 0;
 }
+static bool x2_mode(const minife_ctx *c) { return xdef_of(c) > 0; }
 
 static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
     if (!(fused_mode(c) || x2_mode(c))) return MINIFE_OK;
+    const int X = std::max(2, xdef_of(c));
     for (auto &p : c->parts) {
-        if (p.d_p2) continue;
         DevGuard g(p.dev);
-        TRY(alloc_colvec(c, p, &p.d_p2));
+        if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
+        for (int i = 2; i < X; ++i)
+            if (!p.d_pr[i]) TRY(alloc_colvec(c, p, &p.d_pr[i]));
     }
     return MINIFE_OK;
 }
@@ -1271,7 +1284,14 @@ static int small_mode(const minife_ctx *c) {
 }
 
 // p_k of the x-every-2 scheme: p_1 (written by the init kernels) in d_p, then alternating
-static double *x2_pbuf(const Part &p, int k) { return (k & 1) ? p.d_p : p.d_p2; }
+static double *x2_pbuf(const minife_ctx *c, const Part &p, int k) {
+    return p.ring((k - 1) % xdef_of(c));
+}
+static void set_ring(const minife_ctx *c, const Part &p, UpdArgs &u) {
+    const int X = xdef_of(c);
+    for (int i = 0; i < XDEF_MAX; ++i) u.ring[i] = i < X ? p.ring(i) : nullptr;
+    u.xdef = X;
+}
 
 static int enqueue_iteration_x2(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
@@ -1279,7 +1299,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
     TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(p, k), p.d_Ap, true), true, p.grid_spmv,
+        CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true), true, p.grid_spmv,
                                 launch_stream(c, p)));
     }
     TRY(tw_mark(c, k, true));
@@ -1297,7 +1317,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
             UpdArgs a = upd_args(c, p, 1);
-            a.p = x2_pbuf(p, k);
+            a.p = x2_pbuf(c, p, k);
             CUDA_TRY(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
                                            (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
         }
@@ -1307,8 +1327,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
             CUDA_TRY(c, cudaEventRecord(p.ev_fork, launch_stream(c, p)));
             CUDA_TRY(c, cudaStreamWaitEvent(p.cstream, p.ev_fork, 0));
         }
-        if (k & 1) TRY(enqueue_halo(c, [](Part &p) { return p.d_p2; }, true, true));
-        else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }, true, true));
+        TRY(enqueue_halo(c, [c, k](Part &p) { return x2_pbuf(c, p, k + 1); }, true, true));
         for (auto &p : c->parts) {
             if (virt && &p != &c->parts[0]) break;
             DevGuard g(p.dev);
@@ -1319,7 +1338,8 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
         DevGuard g(p.dev);
         UpdArgs u7 = upd_args(c, p, 1);
         u7.alpha_hist = p.d_alpha;
-        CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(p, k), x2_pbuf(p, k + 1), p.grid_upd,
+        set_ring(c, p, u7);
+        CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1), p.grid_upd,
                                      launch_stream(c, p)));
     }
     if (halo) {
@@ -1343,7 +1363,8 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
             DevGuard g(p.dev);
             UpdArgs u = upd_args(c, p, 0);
             u.alpha_hist = p.d_alpha;
-            CUDA_TRY(c, launch_x2_finish(u, p.d_p, p.d_p2, launch_stream(c, p)));
+            set_ring(c, p, u);
+            CUDA_TRY(c, launch_x2_finish(u, launch_stream(c, p)));
         }
         return MINIFE_OK;
     }
@@ -1416,7 +1437,8 @@ static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, doub
         res->flops = (double)st.iters * (2.0 * nnz + 10.0 * rows);
         // vector bytes per row: 80 (three-kernel scheme, x updated with p), 76 (x every
         // second iteration: K7 moves 24 and 48 B/row alternately) or 72 (fused)
-        const double vec = fused_mode(c) ? 72.0 : (x2_mode(c) && !small_mode(c) ? 76.0 : 80.0);
+        const int X = xdef_of(c);
+        const double vec = fused_mode(c) ? 72.0 : (X && !small_mode(c) ? 72.0 + 8.0 / X : 80.0);
         double bytes = 0.0;
         for (auto &q : c->parts) bytes += spmv_alg_bytes(c, q) + vec * (double)q.rows;
         res->bytes = (double)st.iters * bytes;

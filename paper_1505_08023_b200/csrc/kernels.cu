@@ -1849,11 +1849,14 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     }
 }
 
-// K7 of the x-every-second-iteration scheme (one part, launch_update_p2).  The x update of
-// iteration k is fl(x + fl(alpha_k p_k)) exactly as in K7; it is only deferred by one
-// iteration on odd k, so p_(k+1) goes to the other buffer and p_(k-1) survives until the
-// next (even) K7, which applies both updates in order with one pass over x.
-template <bool IDENT>
+// K7 of the deferred-x scheme (launch_update_p2): the x update of iteration k is
+// fl(x + fl(alpha_k p_k)) exactly as in K7, only deferred: p_(k+1) goes to the next buffer of
+// a ring of X, and every X-th K7 (or one that stops) applies the pending updates
+// j = X floor((k-1)/X) + 1 .. k in order with one pass over x.  The ring buffer p_(k+1) goes
+// to holds p_(k-X+1), read (as the first pending update) before it is overwritten.  FLUSH
+// (k a multiple of X, decided on the host) is a separate instantiation so the plain p update
+// keeps its registers; a stop in a non-flush K7 leaves the pending updates to k_x2_finish.
+template <bool IDENT, bool FLUSH>
 __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, const double *pk,
                                                            double *po) {
     __shared__ unsigned long long s_in[ACC_WORDS];
@@ -1869,24 +1872,31 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
         s_beta = beta;
     }
     __syncthreads();
-    const bool stop = s_stop, even = !(k & 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (even || stop)) a.st->x_done = k;
+    const int X = a.xdef;
+    const bool stop = s_stop, flush = FLUSH;
+    const int j0 = X * ((k - 1) / X) + 1;              // first pending update
+    if (blockIdx.x == 0 && threadIdx.x == 0 && flush) a.st->x_done = k;
     if (!stop && blockIdx.x == 0 && a.acc_zero)
         for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
-    const double beta = s_beta, ak = a.alpha_hist[k], ak1 = even ? a.alpha_hist[k - 1] : 0.0;
-    const bool upx = even || stop;
+    const double beta = s_beta;
+    // the pending updates: alpha_j and p_j (p_k = pk)
+    double al[XDEF_MAX];
+    const double *pj[XDEF_MAX];
+#pragma unroll
+    for (int q = 0; q < XDEF_MAX; ++q) {
+        const int j = j0 + q;
+        al[q] = (flush && j <= k) ? a.alpha_hist[j] : 0.0;
+        pj[q] = (flush && j <= k) ? a.ring[(j - 1) % X] : nullptr;
+    }
+    const int np = flush ? k - j0 + 1 : 0;
+    auto xflush = [&](double x, int64_t c) {
+#pragma unroll
+        for (int q = 0; q < XDEF_MAX; ++q)
+            if (q < np) x = __dadd_rn(x, __dmul_rn(al[q], pj[q][c]));
+        return x;
+    };
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t rows = a.g.rows, n2 = rows >> 1;
-    double2 *x2 = reinterpret_cast<double2 *>(a.x);
-    const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
-    const double2 *pk2 = reinterpret_cast<const double2 *>(pk);
-    double2 *po2 = reinterpret_cast<double2 *>(po);
-    auto step = [&](double &x, double &po_, double r, double p) {
-        if (even) x = __dadd_rn(x, __dmul_rn(ak1, po_));       // alpha_(k-1) p_(k-1)
-        if (upx) x = __dadd_rn(x, __dmul_rn(ak, p));           // alpha_k p_k
-        if (!stop) po_ = __dadd_rn(r, __dmul_rn(beta, p));     // p_(k+1)
-    };
     if (!IDENT) {
         // a part with a halo: p buffers in extended-box order, one warp per owned x-line (as
         // k_update_p); the halo columns of po are written by the exchange meanwhile
@@ -1898,63 +1908,61 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
             const int64_t lz = line / n1, ly = line - lz * n1;
             const int64_t i0 = line * n0;
             const int64_t c0 = a.g.off[0] + E0 * ((ly + a.g.off[1]) + E1 * (lz + a.g.off[2]));
-            for (int64_t lx = lane; lx < n0; lx += 4 * 32) {
-                double pv[4], ov[4], xv[4], rv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t e = lx + 32 * u;
-                    ov[u] = xv[u] = rv[u] = 0.0;
-                    if (e < n0) {
-                        pv[u] = pk[c0 + e];
-                        if (even) ov[u] = po[c0 + e];
-                        if (upx) xv[u] = a.x[i0 + e];
-                        if (!stop) rv[u] = a.r[i0 + e];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t e = lx + 32 * u;
-                    if (e < n0) {
-                        step(xv[u], ov[u], rv[u], pv[u]);
-                        if (upx) a.x[i0 + e] = xv[u];
-                        if (!stop) po[c0 + e] = ov[u];
-                    }
-                }
+            for (int64_t e = lane; e < n0; e += 32) {
+                const double pv = pk[c0 + e];
+                if (flush) a.x[i0 + e] = xflush(a.x[i0 + e], c0 + e);
+                if (!stop) po[c0 + e] = __dadd_rn(a.r[i0 + e], __dmul_rn(beta, pv));
             }
         }
         return;
     }
+    const int64_t rows = a.g.rows, n2 = rows >> 1;
+    double2 *x2 = reinterpret_cast<double2 *>(a.x);
+    const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
+    const double2 *pk2 = reinterpret_cast<const double2 *>(pk);
+    double2 *po2 = reinterpret_cast<double2 *>(po);
     for (int64_t i = tid; i < n2; i += stride) {
         const double2 pv = pk2[i];
-        double2 ov = make_double2(0.0, 0.0), xv = make_double2(0.0, 0.0), rv = make_double2(0.0, 0.0);
-        if (even) ov = po2[i];                              // p_(k-1), still pending
-        if (upx) xv = x2[i];
-        if (!stop) rv = r2[i];
-        step(xv.x, ov.x, rv.x, pv.x);
-        step(xv.y, ov.y, rv.y, pv.y);
-        if (upx) x2[i] = xv;
-        if (!stop) po2[i] = ov;
+        if (flush) {
+            double2 xv = x2[i];
+#pragma unroll
+            for (int q = 0; q < XDEF_MAX; ++q)
+                if (q < np) {
+                    const double2 v = reinterpret_cast<const double2 *>(pj[q])[i];
+                    xv.x = __dadd_rn(xv.x, __dmul_rn(al[q], v.x));
+                    xv.y = __dadd_rn(xv.y, __dmul_rn(al[q], v.y));
+                }
+            x2[i] = xv;
+        }
+        if (!stop) {
+            const double2 rv = r2[i];
+            po2[i] = make_double2(__dadd_rn(rv.x, __dmul_rn(beta, pv.x)),
+                                  __dadd_rn(rv.y, __dmul_rn(beta, pv.y)));
+        }
     }
     if ((rows & 1) && tid == 0) {
         const int64_t j = rows - 1;
-        double xj = upx ? a.x[j] : 0.0, oj = even ? po[j] : 0.0;
-        step(xj, oj, stop ? 0.0 : a.r[j], pk[j]);
-        if (upx) a.x[j] = xj;
-        if (!stop) po[j] = oj;
+        const double pv = pk[j];
+        if (flush) a.x[j] = xflush(a.x[j], j);
+        if (!stop) po[j] = __dadd_rn(a.r[j], __dmul_rn(beta, pv));
     }
 }
 
-// After the loop: the x update of the last iteration with an alpha, if still pending.
+// After the loop: the x updates still pending (a stop in K6, or an iteration count that is
+// not a multiple of X), j = x_done + 1 .. alpha_iter, in order.
 template <bool IDENT>
-__global__ void __launch_bounds__(UPD_THREADS) k_x2_finish(UpdArgs a, const double *p_odd,
-                                                           const double *p_even) {
-    const int j = a.st->x_done + 1;
-    if (j > a.st->alpha_iter) return;
-    const double alpha = a.alpha_hist[j];
-    const double *p = (j & 1) ? p_odd : p_even;
+__global__ void __launch_bounds__(UPD_THREADS) k_x2_finish(UpdArgs a) {
+    const int j0 = a.st->x_done + 1, j1 = a.st->alpha_iter;
+    if (j0 > j1) return;
+    const int X = a.xdef;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride)
-        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, p[IDENT ? i : row_to_col(a.g, i)]));
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.g.rows; i += stride) {
+        const int64_t c = IDENT ? i : row_to_col(a.g, i);
+        double x = a.x[i];
+        for (int j = j0; j <= j1; ++j)
+            x = __dadd_rn(x, __dmul_rn(a.alpha_hist[j], a.ring[(j - 1) % X][c]));
+        a.x[i] = x;
+    }
 }
 
 // Halo values of p_(k+1) computed ahead of K7 (SYM with a halo): the packed
@@ -2660,15 +2668,20 @@ cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *
     const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
     const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
     (void)grid;
-    if (a.g.ident) k_update_p2<true><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
-    else k_update_p2<false><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    const bool flush = k % a.xdef == 0;
+    if (a.g.ident) {
+        if (flush) k_update_p2<true, true><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+        else k_update_p2<true, false><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    } else {
+        if (flush) k_update_p2<false, true><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+        else k_update_p2<false, false><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
+    }
     return cudaGetLastError();
 }
 
-cudaError_t launch_x2_finish(const UpdArgs &a, const double *p_odd, const double *p_even,
-                             cudaStream_t s) {
-    if (a.g.ident) k_x2_finish<true><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
-    else k_x2_finish<false><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a, p_odd, p_even);
+cudaError_t launch_x2_finish(const UpdArgs &a, cudaStream_t s) {
+    if (a.g.ident) k_x2_finish<true><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a);
+    else k_x2_finish<false><<<stream_grid(a.g.rows), UPD_THREADS, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -113,7 +113,12 @@ struct UpdArgs {
     double *hist, *rr;                  // [max_iters+1]
     CgState *st;
     double *alpha_hist;                 // [max_iters+1]: alpha_k recorded by K6 (may be null)
+    // deferred x (launch_update_p2 / launch_x2_finish): ring of xdef p buffers, p_k in
+    // ring[(k-1) % xdef]
+    const double *ring[8];
+    int xdef;
 };
+constexpr int XDEF_MAX = 8;
 
 // Setup (a0.2-a0.5)
 cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width,
@@ -131,8 +136,7 @@ cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s);
 // on a stop).  x2_finish applies an x update still pending after the loop.
 cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *po, int grid,
                              cudaStream_t s);
-cudaError_t launch_x2_finish(const UpdArgs &a, const double *p_odd, const double *p_even,
-                             cudaStream_t s);
+cudaError_t launch_x2_finish(const UpdArgs &a, cudaStream_t s);
 // fused scheme: K6' (alpha_k; r -= alpha Ap; exact rr) and the finish kernel (rr_K, pending x)
 cudaError_t launch_update_r(const UpdArgs &a, int k, unsigned long long *acc_pAp_next_zero,
                             int grid, cudaStream_t s);

@@ -169,15 +169,16 @@ def test_single_launch_solvers_bit_identical(n, fmt, small):
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("xdef", ["2", "5", "8"])
 @pytest.mark.parametrize("n,fmt", [((23, 17, 9), "sym"), ((33, 32, 31), "seg"), ((7, 1, 3), "sym")])
-def test_x_every_second_iteration_bit_identical(n, fmt):
-    """the x-every-2 scheme (forced at any size with MINIFE_X2=2, the multi-kernel
-    path with MINIFE_SMALL=0): 200 iterations, a tolerance stop and an odd count (7) leave
-    nothing pending -- bitwise the oracle."""
+def test_x_every_second_iteration_bit_identical(n, fmt, xdef):
+    """the deferred x update, every X iterations from a ring of X p buffers (forced
+    at any size with MINIFE_X2=X, the multi-kernel path with MINIFE_SMALL=0): 200 iterations,
+    a tolerance stop and an odd count (7) leave nothing pending -- bitwise the oracle."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, MINIFE_X2="2", MINIFE_SMALL="0")
+    env = dict(os.environ, MINIFE_X2=xdef, MINIFE_SMALL="0")
     here = os.path.dirname(os.path.abspath(__file__))
     out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
                           *map(str, n), fmt], env=env, capture_output=True, text=True,
