@@ -1908,10 +1908,25 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
             const int64_t lz = line / n1, ly = line - lz * n1;
             const int64_t i0 = line * n0;
             const int64_t c0 = a.g.off[0] + E0 * ((ly + a.g.off[1]) + E1 * (lz + a.g.off[2]));
-            for (int64_t e = lane; e < n0; e += 32) {
-                const double pv = pk[c0 + e];
-                if (flush) a.x[i0 + e] = xflush(a.x[i0 + e], c0 + e);
-                if (!stop) po[c0 + e] = __dadd_rn(a.r[i0 + e], __dmul_rn(beta, pv));
+            for (int64_t lx = lane; lx < n0; lx += 4 * 32) {
+                double pv[4], rv[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {          // four elements per lane in flight
+                    const int64_t e = lx + 32 * u;
+                    if (e < n0) {
+                        pv[u] = pk[c0 + e];
+                        rv[u] = stop ? 0.0 : a.r[i0 + e];
+                        if (flush) xv[u] = a.x[i0 + e];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t e = lx + 32 * u;
+                    if (e < n0) {
+                        if (flush) a.x[i0 + e] = xflush(xv[u], c0 + e);
+                        if (!stop) po[c0 + e] = __dadd_rn(rv[u], __dmul_rn(beta, pv[u]));
+                    }
+                }
             }
         }
         return;
@@ -2665,10 +2680,21 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
 cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *po, int grid,
                              cudaStream_t s) {
     query_occupancy();
-    const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
-    const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * g_updp_bps));
     (void)grid;
+    // grid: the resident CTAs of the instantiation launched (grid-stride loops; a partial
+    // second wave would leave SMs idle at the end)
+    static int bps[4] = {0, 0, 0, 0};
+    if (!bps[0]) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[0], k_update_p2<true, false>, UPD_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[1], k_update_p2<true, true>, UPD_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[2], k_update_p2<false, false>, UPD_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[3], k_update_p2<false, true>, UPD_THREADS, 0);
+        for (int &b : bps) b = std::max(1, std::min(b, g_updp_bps));
+    }
     const bool flush = k % a.xdef == 0;
+    const int v = (a.g.ident ? 0 : 2) + (flush ? 1 : 0);
+    const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;
+    const int g7 = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)g_sms * bps[v]));
     if (a.g.ident) {
         if (flush) k_update_p2<true, true><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
         else k_update_p2<true, false><<<g7, UPD_THREADS, 0, s>>>(a, k, pk, po);
