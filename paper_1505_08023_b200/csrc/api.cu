@@ -282,6 +282,11 @@ static Geom geom_of(const minife_ctx *c, const Part &p) {
     g.rows = p.rows;
     g.ncols = p.ncols;
     g.ident = p.ncols == p.rows;
+    for (int k = 0; k < 2; ++k) {                 // ext_n >= 2 (a box has >= 2 nodes per axis)
+        const unsigned __int128 two64 = (unsigned __int128)1 << 64;
+        const uint64_t d = (uint64_t)std::max(2, g.ext_n[k]);
+        g.ext_mag[k] = (uint64_t)((two64 + d - 1) / d);
+    }
     return g;
 }
 

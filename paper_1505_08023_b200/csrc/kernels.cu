@@ -97,9 +97,9 @@ __device__ __forceinline__ void row_coords(const Geom &g, int64_t l, int &lx, in
 // extended-box column c -> owned row, or -1 for a halo node
 __device__ __forceinline__ int64_t col_to_row(const Geom &g, int64_t c) {
     const unsigned u = (unsigned)c;
-    const unsigned line = u / (unsigned)g.ext_n[0];
+    const unsigned line = (unsigned)__umul64hi((unsigned long long)u, g.ext_mag[0]);
     const int ex = (int)(u - line * (unsigned)g.ext_n[0]);
-    const unsigned plane = line / (unsigned)g.ext_n[1];
+    const unsigned plane = (unsigned)__umul64hi((unsigned long long)line, g.ext_mag[1]);
     const int ey = (int)(line - plane * (unsigned)g.ext_n[1]), ez = (int)plane;
     const int lx = ex - g.off[0], ly = ey - g.off[1], lz = ez - g.off[2];
     if (lx < 0 || lx >= g.own_n[0] || ly < 0 || ly >= g.own_n[1] || lz < 0 || lz >= g.own_n[2])

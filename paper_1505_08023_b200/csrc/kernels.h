@@ -40,6 +40,9 @@ struct Geom {
     int off[3];                         // own_lo - ext_lo
     int64_t rows, ncols;
     int ident;                          // extended box == owned box (one part)
+    // u / ext_n[a] for u < 2^31 as __umul64hi(u, ext_mag[a]), ext_mag[a] = ceil(2^64 / ext_n[a])
+    // (exact: the error u / 2^64 stays below 1 / ext_n[a])
+    uint64_t ext_mag[2];
 };
 
 struct Matrix {
