@@ -907,14 +907,16 @@ using SymmExpansion = ExpansionT<SYMM_EXP_A, SYMM_EXP_B>;
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
 // row sum; xd = x of the row itself (slot 13).
-template <bool FULL, int GS>
+template <bool FULL, int GS, class WAIT>
 __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const int (&sg)[9],
                                             unsigned msk, const double *vs, const double *mir,
-                                            const int (&madj)[5], int r0, double &xd) {
+                                            const int (&madj)[5], int r0, double &xd,
+                                            WAIT &&wait_values) {
     auto on = [&](int t) { return FULL || ((msk >> t) & 1u); };
     double xv[27];
 #pragma unroll
     for (int t = 0; t < 27; ++t) xv[t] = on(t) ? __ldg(x + sg[t / 3] + (t % 3)) : 0.0;
+    wait_values();                                    // the x gathers are in flight meanwhile
     double lv[13];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {                     // runs 0..3: 3 slots; run 4: slot 12
@@ -943,7 +945,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 const __grid_constant__ CUtensorMap tm1) {
     using C = SymmCfg<NW, NST>;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST];
+    // per stage two "full" barriers: full_bar for the run starts and masks (small, issued
+    // first: the consumers start their x gathers as soon as these land) and val_bar for the
+    // values and mirror boxes (waited for after the gathers are in flight)
+    __shared__ __align__(8) uint64_t full_bar[NST], val_bar[NST], empty_bar[NST];
     __shared__ unsigned long long sacc[ACC_WORDS];
     __shared__ int sdig[ACC_DIG16];
     if (DOT && a.st && a.st->done) return;
@@ -951,6 +956,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full_bar[s], 1);
+            mbar_init(&val_bar[s], 1);
             mbar_init(&empty_bar[s], NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -985,10 +991,11 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 unsigned char *buf = smem + (size_t)st * C::STAGE_B;
                 const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
                 const int64_t r0 = s0 * 32;
-                mbar_expect_tx(&full_bar[st], bv + bs + bm + 4 * C::MIR3_B + C::MIR1_B);
-                bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &full_bar[st], pol_keep);
+                mbar_expect_tx(&full_bar[st], bs + bm);
                 bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
                 bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
+                mbar_expect_tx(&val_bar[st], bv + 4 * C::MIR3_B + C::MIR1_B);
+                bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &val_bar[st], pol_keep);
                 if (a.x_prefetch) {
                     // the tile's plane-ahead x (its dz = +1 runs) is read here for the first
                     // time: start it into L2 now, so the consumers' gathers hit L2, not HBM
@@ -1003,9 +1010,9 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
                     tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
-                             11 - 3 * g, &full_bar[st]);
+                             11 - 3 * g, &val_bar[st]);
                 tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
-                         &full_bar[st]);
+                         &val_bar[st]);
             }
         }
     } else {
@@ -1037,10 +1044,15 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 9; ++j) sg[j] = ss[32 * j];
                 double sum, xd;
+                auto wait_values = [&]() {
+                    mbar_wait(&val_bar[st], (uint32_t)((i / NST) & 1));
+                };
                 if (__all_sync(0xffffffffu, (msk & SYM_FULL) == SYM_FULL))
-                    sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
+                    sum = symm_fold<true, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd,
+                                                 wait_values);
                 else
-                    sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd);
+                    sum = symm_fold<false, C::GS>(a.x, sg, msk, vs, mir, madj, r0, xd,
+                                                  wait_values);
                 // every value of the stage has been consumed by the fold: release it before
                 // the epilogue (the empty asm pins the fold's result ahead of the arrive, so
                 // no shared-memory read of the stage can still be in flight)
