@@ -186,6 +186,22 @@ def test_x_every_second_iteration_bit_identical(n, fmt, xdef):
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("n", [(23, 17, 9), (33, 32, 31)])
+def test_sym_fallback_kernel_bit_identical(n):
+    """The L1-gather SYM SpMV (`k_spmv_sym`, used where tensor maps are unavailable;
+    MINIFE_SYM_CFG=0 selects it) through the three-kernel path: bitwise the oracle
+    (subprocess: the selection is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MINIFE_SYM_CFG="0", MINIFE_SMALL="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
+                          *map(str, n), "sym"], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 def test_cluster_solver_after_spmv_leftovers():
     """The one-cluster solver right after SpMV launches that fill every SM's shared memory
     with other data: 20 solves, each bitwise the oracle (subprocess: MINIFE_SMALL is read once
