@@ -118,6 +118,9 @@ typedef struct minife_info {
     int32_t format;           /* MINIFE_FMT_*                                             */
     int32_t reserved;
     int64_t local_nns;        /* non-zero segments (x-runs) of the rows held here */
+    int64_t kernel_launches;  /* kernels of this library launched by this ctx since creation
+                                 (graph replays counted per kernel node; NCCL's own kernels
+                                 and memset/copy nodes not included)                        */
 } minife_info;
 
 typedef struct minife_cg_result {
@@ -169,9 +172,29 @@ int minife_create_rank(int nx, int ny, int nz, int rank, int world, int device,
 void minife_destroy(minife_ctx *ctx);
 
 /* Run all subsequent device work of a SINGLE/RANK ctx on `stream` (a cudaStream_t, may be a
- * torch stream).  NULL restores the ctx's own stream.  Invalidates captured graphs.
+ * torch stream).  NULL restores the ctx's own stream.  Captured solve graphs stay valid: they
+ * are captured on the ctx's own stream and launched on the selected one.
  * Errors: MINIFE_EINVAL (ctx NULL), MINIFE_ESTATE (mode VIRTUAL/MULTI). */
 int minife_set_stream(minife_ctx *ctx, void *stream);
+
+/* Per-ctx execution options (the library reads no environment variables for them).  Every
+ * option selects between code paths that compute the SAME results bit for bit (C0-C6); they
+ * exist for tests and A/B measurements.  -1 = automatic (the default where listed).
+ *   "x_defer"         deferred x update over a ring of X p buffers: -1 auto (X = 8 where
+ *                     the vectors exceed L2), 0 or 1 off, 2..8 force X
+ *   "small_solver"    single-launch solvers for small one-part problems: -1 auto, 0 none
+ *                     (multi-kernel graph), 1 one CTA (<= 2048 rows), 2 one 16-CTA cluster
+ *                     (<= 8192 rows; only where such a cluster can be scheduled)
+ *   "graph"           1 (default) replay one captured CUDA graph per solve, 0 enqueue directly
+ *   "val_evict_first" SYM SpMV value stream L2 policy: -1 auto, 0 normal, 1 evict-first
+ *   "x_prefetch"      SYM SpMV plane-ahead L2 prefetch of x: -1 auto, 0 off, 1 on
+ *   "sym_kernel"      SYM SpMV: 1 (default) tensor-map mirror kernel, 0 L1-gather kernel
+ *   "spmv_impl"       SEG/CRS SpMV: -1 auto, 1 TMA pipeline, 0 register streaming
+ *   "x_late"          1 (default) K7 applies x += alpha p with the p it reads, 0 K6 does
+ *   "cluster_dd"      cluster solver digit exchange: 1 (default) DSMEM pushes, 0 pulls
+ * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,
+ * value out of range). */
+int minife_set_option(minife_ctx *ctx, const char *name, int64_t value);
 
 const char *minife_strerror(int status);
 const char *minife_last_error(const minife_ctx *ctx);

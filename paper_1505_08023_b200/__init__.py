@@ -66,7 +66,8 @@ class minife_info(ctypes.Structure):
                 ("max_part_rows", ctypes.c_int64), ("max_part_nnz", ctypes.c_int64),
                 ("max_part_externals", ctypes.c_int64), ("sell_entries", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("format", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("local_nns", ctypes.c_int64)]
+                ("reserved", ctypes.c_int32), ("local_nns", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64)]
 
 
 class minife_cg_result(ctypes.Structure):
@@ -104,6 +105,7 @@ SIGNATURES = {
     "minife_set_format": (_I, [_P, _I]),
     "minife_set_scheme": (_I, [_P, _I]),
     "minife_set_transport": (_I, [_P, _I]),
+    "minife_set_option": (_I, [_P, ctypes.c_char_p, _I64]),
     "minife_assemble": (_I, [_P]),
     "minife_cg_solve": (_I, [_P, _I, _D, ctypes.POINTER(minife_cg_result)]),
     "minife_cg_profile": (_I, [_P, _I, ctypes.POINTER(minife_kernel_times)]),
@@ -222,7 +224,8 @@ class Minife:
     """RAII wrapper: Minife(nx, ny, nz, ngpu=1 | virtual=p | rank=(r, w, dev, uid))."""
 
     def __init__(self, nx: int, ny: int, nz: int, ngpu: int = 1, virtual: int | None = None,
-                 rank: tuple | None = None, fmt: int | None = None):
+                 rank: tuple | None = None, fmt: int | None = None,
+                 options: dict | None = None):
         h = ctypes.c_void_p()
         if rank is not None:
             r, w, dev, uid = rank
@@ -237,6 +240,8 @@ class Minife:
         self.h = h
         if fmt is not None:
             self._check(minife_set_format(self.h, fmt), "minife_set_format")
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
         self.info = self.get_info()
 
     # -- lifecycle -------------------------------------------------------------------------
@@ -293,6 +298,10 @@ class Minife:
     def set_transport(self, transport: int):
         """VIRTUAL ctxs: TRANSPORT_DIRECT (default) or TRANSPORT_WIRE (the NCCL-mode protocol)."""
         self._check(minife_set_transport(self.h, transport), "minife_set_transport")
+
+    def set_option(self, name: str, value: int):
+        """Per-ctx execution option (minife.h: x_defer, small_solver, graph, ...)."""
+        self._check(minife_set_option(self.h, name.encode(), int(value)), "minife_set_option")
 
     def set_scheme(self, scheme: int):
         """SCHEME_3K (default) or SCHEME_FUSED (one part + FMT_SEG); bit-identical results."""

@@ -161,6 +161,22 @@ struct minife_ctx {
     std::vector<cudaEvent_t> tw_ev;              // [2 * tw_n]: start, end of each SpMV
     bool tw_armed = false;                       // the enqueued solve records the window
     bool eager = false;                          // capture failed once (world > 1): no graphs
+    // options (minife_set_option): -1 = automatic choice
+    struct {
+        int x_defer = -1;          // deferred x update: 0 off, 2..8 forced ring size X
+        int small_solver = -1;     // single-launch solvers: 0 none, 1 one CTA, 2 one cluster
+        int graph = 1;             // 0: enqueue every solve directly (no CUDA graph)
+        int val_evict_first = -1;  // SYM SpMV value stream evict-first in L2
+        int x_prefetch = -1;       // SYM SpMV plane-ahead L2 prefetch of x
+        int sym_kernel = 1;        // SYM SpMV: 1 tensor-map mirrors, 0 L1-gather kernel
+        int spmv_impl = -1;        // SEG/CRS SpMV: 1 TMA pipeline, 0 register streaming
+        int x_late = 1;            // x += alpha p applied by K7 (1) or K6 (0)
+        int cluster_dd = 1;        // cluster solver: DSMEM digit pushes
+    } opt;
+    // kernel launch accounting: enq_kernels counts launch_* calls as they are enqueued (into a
+    // capture or directly); g_kernels = kernels in the captured solve graph; kernel_launches =
+    // kernels launched by this ctx so far (graph replays included)
+    int64_t enq_kernels = 0, g_kernels = 0, kernel_launches = 0;
     // last solve
     int last_iters = 0;
     bool solved = false;
@@ -193,6 +209,13 @@ static void set_err(minife_ctx *c, const char *fmt, ...) {
                     __LINE__);                                                                \
             return MINIFE_ENCCL;                                                              \
         }                                                                                     \
+    } while (0)
+
+// one kernel of ours per launch_* wrapper (kernels.cu): counted for minife_info.kernel_launches
+#define LAUNCH(ctx, call)                                                                     \
+    do {                                                                                      \
+        CUDA_TRY(ctx, call);                                                                  \
+        ++(ctx)->enq_kernels;                                                                 \
     } while (0)
 
 #define TRY(call)                                                                             \
@@ -232,7 +255,9 @@ static void dfree(Part &p, T *&ptr, size_t n) {
 static int alloc_colvec(minife_ctx *c, Part &p, double **ptr) {
     const size_t n = (size_t)(p.ncols + 32);
     TRY(dalloc(c, p, ptr, n));
-    CUDA_TRY(c, cudaMemset(*ptr, 0, n * sizeof(double)));
+    // stream-ordered before every later kernel on the part's queue (the legacy-stream
+    // cudaMemset is not ordered with the non-blocking ctx streams)
+    CUDA_TRY(c, cudaMemsetAsync(*ptr, 0, n * sizeof(double), launch_stream(c, p)));
     return MINIFE_OK;
 }
 
@@ -404,6 +429,7 @@ static int setup_push(minife_ctx *c) {
             CUDA_TRY(c, cudaMemcpy(p.d_push_ptr, ptr.data(), sizeof(double *) * ptr.size(),
                                    cudaMemcpyHostToDevice));
         CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_push, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaDeviceSynchronize());     // legacy-stream copies above, see create_common
     }
     c->push_ready = true;
     return MINIFE_OK;
@@ -472,6 +498,12 @@ static int create_common(minife_ctx *c, int nx, int ny, int nz, int nparts,
     // default format: SYM (B200, 300^3: SYM SpMV 0.88 ms vs SEG 1.07 ms; with a halo the
     // halo nodes are stored as ghost rows, profiles/r01/session2)
     c->fmt = MINIFE_FMT_SYM;
+    // the setup copies/memsets above ran on the legacy stream: complete them before any
+    // kernel on the (non-blocking) ctx streams can touch those buffers
+    for (auto &p : c->parts) {
+        DevGuard gp(p.dev);
+        CUDA_TRY(c, cudaDeviceSynchronize());
+    }
     DevGuard g(c->parts[0].dev);
     CUDA_TRY(c, cudaEventCreate(&c->ev0));
     CUDA_TRY(c, cudaEventCreate(&c->ev1));
@@ -599,6 +631,39 @@ extern "C" int minife_set_stream(minife_ctx *c, void *stream) {
     if (c->mode != MINIFE_MODE_SINGLE && c->mode != MINIFE_MODE_RANK) return MINIFE_ESTATE;
     c->user_stream = (cudaStream_t)stream;
     return MINIFE_OK;
+}
+
+extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value) {
+    if (!c || !name) return MINIFE_EINVAL;
+    struct {
+        const char *name;
+        int *field;
+        int lo, hi;
+    } table[] = {
+        {"x_defer", &c->opt.x_defer, -1, XDEF_MAX},
+        {"small_solver", &c->opt.small_solver, -1, 2},
+        {"graph", &c->opt.graph, 0, 1},
+        {"val_evict_first", &c->opt.val_evict_first, -1, 1},
+        {"x_prefetch", &c->opt.x_prefetch, -1, 1},
+        {"sym_kernel", &c->opt.sym_kernel, 0, 1},
+        {"spmv_impl", &c->opt.spmv_impl, -1, 1},
+        {"x_late", &c->opt.x_late, 0, 1},
+        {"cluster_dd", &c->opt.cluster_dd, 0, 1},
+    };
+    for (auto &t : table) {
+        if (strcmp(t.name, name) != 0) continue;
+        if (value < t.lo || value > t.hi) {
+            set_err(c, "option %s: value %lld outside [%d, %d]", name, (long long)value, t.lo, t.hi);
+            return MINIFE_EINVAL;
+        }
+        if (*t.field != (int)value) {
+            *t.field = (int)value;
+            drop_graph(c);
+        }
+        return MINIFE_OK;
+    }
+    set_err(c, "unknown option %s", name);
+    return MINIFE_EINVAL;
 }
 
 extern "C" int minife_set_transport(minife_ctx *c, int transport) {
@@ -755,7 +820,7 @@ extern "C" int minife_assemble(minife_ctx *c) {
         a.fmt = c->fmt;
         if (c->fmt == MINIFE_FMT_CRS) {
             // slice widths on the device, offsets by a host prefix sum (8 B per 32 rows)
-            CUDA_TRY(c, launch_rowlen_widths(geo, p.d_row_len, p.d_width, p.nslices, s));
+            LAUNCH(c, launch_rowlen_widths(geo, p.d_row_len, p.d_width, p.nslices, s));
             std::vector<uint8_t> w(p.nslices);
             CUDA_TRY(c, cudaMemcpyAsync(w.data(), p.d_width, p.nslices, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -797,7 +862,7 @@ extern "C" int minife_assemble(minife_ctx *c) {
         a.val = p.d_val;
         a.b = p.d_b;
         a.slice_pos = c->fmt == MINIFE_FMT_SEG ? p.d_slice_pos : nullptr;
-        CUDA_TRY(c, launch_assemble(a, s));
+        LAUNCH(c, launch_assemble(a, s));
         p.grid_spmv = spmv_grid(p.nslices, c->fmt);
     }
     for (auto &p : c->parts) {
@@ -825,7 +890,7 @@ static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now) {
         a.rr = p.d_rr;
         a.st = p.d_st;
         a.acc_in = p.acc_rr();
-        CUDA_TRY(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr,
+        LAUNCH(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr,
                                 p.d_push_dst, p.d_push_ptr, (int64_t)p.plan.send_idx.size(),
                                 launch_stream(c, p)));
         if (c->mode == MINIFE_MODE_MULTI) CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
@@ -856,7 +921,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepac
                 auto it = std::lower_bound(src.plan.nbr.begin(), src.plan.nbr.end(),
                                            dst.plan.rank);
                 const size_t j = (size_t)(it - src.plan.nbr.begin());
-                CUDA_TRY(c, launch_move(vec(src), src.d_send_col + src.plan.send_off[j], vec(dst),
+                LAUNCH(c, launch_move(vec(src), src.d_send_col + src.plan.send_off[j], vec(dst),
                                         dst.d_recv_pos + dst.plan.recv_off[k],
                                         src.plan.send_cnt[j], s));
             }
@@ -867,7 +932,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepac
     for (auto &p : c->parts) {
         if (prepacked) break;
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
+        LAUNCH(c, launch_move(vec(p), p.d_send_col, p.d_sendbuf, nullptr,
                                 (int64_t)p.plan.send_idx.size(), sp(p)));
     }
     if (c->mode == MINIFE_MODE_VIRTUAL) {
@@ -892,7 +957,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepac
             }
         }
         for (auto &p : c->parts)
-            CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, s));
+            LAUNCH(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, s));
         return MINIFE_OK;
     }
     NCCL_TRY(c, nccl()->GroupStart());
@@ -910,7 +975,7 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepac
     NCCL_TRY(c, nccl()->GroupEnd());
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, sp(p)));
+        LAUNCH(c, launch_move(p.d_recvbuf, nullptr, vec(p), p.d_recv_pos, p.plan.n_ext, sp(p)));
     }
     return MINIFE_OK;
 }
@@ -921,7 +986,7 @@ static int enqueue_allreduce(minife_ctx *c, int which) {
     if (c->mode == MINIFE_MODE_VIRTUAL) {
         std::vector<unsigned long long *> accs;
         for (auto &p : c->parts) accs.push_back(which ? p.acc_rr() : p.acc_pAp());
-        CUDA_TRY(c, launch_vsum(accs.data(), (int)accs.size(), c->parts[0].stream));
+        LAUNCH(c, launch_vsum(accs.data(), (int)accs.size(), c->parts[0].stream));
         return MINIFE_OK;
     }
     NCCL_TRY(c, nccl()->GroupStart());
@@ -949,6 +1014,8 @@ static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
     a.hist = p.d_hist;
     a.rr = p.d_rr;
     a.st = p.d_st;
+    a.x_late = c->opt.x_late;
+    a.cl_dd = c->opt.cluster_dd;
     if (which_in == 0) {          // K6: in = pAp, out = rr
         a.acc_in = p.acc_pAp();
         a.acc_out = p.acc_rr();
@@ -975,21 +1042,15 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     // SYM value stream evict-first in L2 when the CG vectors (5 x 8 B per row) fit beside it
     // in the 126 MB L2 and so stay resident across the iteration's kernels (B200, 100^3:
     // 62.9 -> 60.9 us per iteration); at 300^3 the mirrored reads need the normal policy
-    // (evict-first there: 1.207 -> 1.301 ms).  MINIFE_VAL_EF=0/1 forces it.
-    static int vef = -2;
-    if (vef == -2) {
-        const char *e = getenv("MINIFE_VAL_EF");
-        vef = e ? atoi(e) : -1;
-    }
+    // (evict-first there: 1.207 -> 1.301 ms).  Option "val_evict_first" = 0/1 forces it.
+    const int vef = c->opt.val_evict_first;
     a.val_evict_first = vef >= 0 ? vef : (40.0 * (double)p.ncols < 64e6 ? 1 : 0);
     // plane-ahead x prefetch into L2 when x itself does not stay L2-resident (B200, 300^3:
-    // 1.0806 -> 1.0757 ms per iteration; 100^3: no gain).  MINIFE_X_PREFETCH=0/1 forces it.
-    static int xpf = -2;
-    if (xpf == -2) {
-        const char *e = getenv("MINIFE_X_PREFETCH");
-        xpf = e ? atoi(e) : -1;
-    }
+    // 1.0806 -> 1.0757 ms per iteration; 100^3: no gain).  Option "x_prefetch" = 0/1 forces it.
+    const int xpf = c->opt.x_prefetch;
     a.x_prefetch = xpf >= 0 ? xpf : (8.0 * (double)p.ncols > 64e6 ? 1 : 0);
+    a.sym_kernel = c->opt.sym_kernel;
+    a.impl = c->opt.spmv_impl;
     return a;
 }
 
@@ -1031,14 +1092,14 @@ static int enqueue_k7_with_halo(minife_ctx *c, int k) {
         TRY(enqueue_push(c, k, 1, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+            LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
         }
         return push_wait(c);
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 1);
-        CUDA_TRY(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
+        LAUNCH(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
                                        (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
     }
     for (auto &p : c->parts) {
@@ -1055,7 +1116,7 @@ static int enqueue_k7_with_halo(minife_ctx *c, int k) {
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+        LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
     }
     for (auto &p : c->parts) {
         if (virt && &p != &c->parts[0]) break;
@@ -1085,7 +1146,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
         CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 4 * ACC_WORDS * sizeof(unsigned long long), s));
         UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
-        CUDA_TRY(c, launch_init_vectors(a, p.grid_upd, s));
+        LAUNCH(c, launch_init_vectors(a, p.grid_upd, s));
     }
     TRY(enqueue_allreduce(c, 1));
     for (auto &p : c->parts) {
@@ -1093,7 +1154,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
         UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
         a.acc_zero = p.acc_pAp();
-        CUDA_TRY(c, launch_init_finalize(a, tol, launch_stream(c, p)));
+        LAUNCH(c, launch_init_finalize(a, tol, launch_stream(c, p)));
     }
     return MINIFE_OK;
 }
@@ -1120,7 +1181,7 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c, int k) {
         DevGuard g(p.dev);
         SpmvArgs a = spmv_args(c, p, p.d_p, p.d_Ap, true);
         a.s_end = p.n_int;
-        CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
+        if (a.s_end > a.s_begin) LAUNCH(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1129,7 +1190,7 @@ static int enqueue_halo_spmv_overlapped(minife_ctx *c, int k) {
             CUDA_TRY(c, cudaStreamWaitEvent(launch_stream(c, p), q.ev_join, 0));
         SpmvArgs a = spmv_args(c, p, p.d_p, p.d_Ap, true);
         a.s_begin = p.n_int;
-        CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
+        if (a.s_end > a.s_begin) LAUNCH(c, launch_spmv(a, true, p.grid_spmv, launch_stream(c, p)));
     }
     TRY(tw_mark(c, k, true));
     return MINIFE_OK;
@@ -1143,7 +1204,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+            LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
                                     launch_stream(c, p)));
         }
         TRY(tw_mark(c, k, true));
@@ -1154,7 +1215,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         if (!t) TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+            LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
                                     launch_stream(c, p)));
         }
         if (!t) TRY(tw_mark(c, k, true));
@@ -1164,7 +1225,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_update_xr(upd_args(c, p, 0), k, p.grid_upd, launch_stream(c, p)));
+        LAUNCH(c, launch_update_xr(upd_args(c, p, 0), k, p.grid_upd, launch_stream(c, p)));
     }
     if (t) t->mark(1);
     TRY(enqueue_allreduce(c, 1));
@@ -1174,7 +1235,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
     } else {
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            CUDA_TRY(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+            LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
         }
     }
     if (t) t->mark(2);
@@ -1214,14 +1275,14 @@ static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
     a.rr = p.d_rr;
     a.stw = p.d_st;
     if (!t) TRY(tw_mark(c, k, false));
-    CUDA_TRY(c, launch_spmv(a, true, p.grid_spmv, s));
+    LAUNCH(c, launch_spmv(a, true, p.grid_spmv, s));
     if (!t) TRY(tw_mark(c, k, true));
     if (t) t->mark(0);
     // K6'(k): alpha_k, r -= alpha_k Ap_k, exact rr_k
     UpdArgs u = upd_args(c, p, 0);
     u.acc_in = p.acc_pAp(k);
     u.acc_out = p.acc_rr(k);
-    CUDA_TRY(c, launch_update_r(u, k, p.acc_pAp(k + 1), p.grid_upd, s));
+    LAUNCH(c, launch_update_r(u, k, p.acc_pAp(k + 1), p.grid_upd, s));
     if (t) t->mark(1);
     return MINIFE_OK;
 }
@@ -1231,25 +1292,21 @@ static int enqueue_iteration_fused(minife_ctx *c, int k, PhaseTimer *t) {
 // alone and writes p_(k+1) into the other p buffer; the next (even) K7 applies
 // alpha_(k-1) p_(k-1) and alpha_k p_k in one pass over x.  x then costs 16 B per row every
 // second iteration (36 instead of 40 B/row per K7 on average); same operations, same order:
-// bit-identical.  MINIFE_X2=0 disables.
+// bit-identical.
 // Deferred x: x += alpha_k p_k is applied X iterations at a time, p_k living
-// in a ring of X buffers.  Returns X, or 0 when off.  MINIFE_X2=0 disables it; MINIFE_X2=n
-// (2..8) forces X = n at any size (tests); unset: X = XDEF_DEFAULT where the vectors stream
+// in a ring of X buffers.  Returns X, or 0 when off.  Option "x_defer" = 0 disables it, n
+// (2..8) forces X = n at any size (tests); -1 (default): X = XDEF_DEFAULT where the vectors stream
 // from HBM anyway (B200, 300^3 per iteration: X = 2 -1.0 % against no deferral, X = 4 a
 // further -0.5 %, X = 8 -1.1 %; K7 moves 24 B/row plus (16 + 8 (X-1)) / X for x; at 100^3,
 // whose vectors sit in L2, a second p buffer costs +0.7 %).
 constexpr int XDEF_DEFAULT = 8;
 static int xdef_of(const minife_ctx *c) {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("MINIFE_X2");
-        env = e ? atoi(e) : 1;
-    }
+    const int env = c->opt.x_defer;
     // partitioned (SYM with a halo, halo overlapped with K7 over the wire or device copies):
     // the exchange fills the halo of the buffer p_(k+1) goes to
     const bool single = c->parts.size() == 1 && c->world == 1;
     const bool parts_ok = overlap_sym(c) && !push_mode(c);
-    if (!env || !(single || parts_ok) || fused_mode(c)) return 0;
+    if (!env || env == 1 || !(single || parts_ok) || fused_mode(c)) return 0;
     if (env >= 2) return std::min(env, XDEF_MAX);
     return 40.0 * (double)c->parts[0].ncols >= 64e6 ? XDEF_DEFAULT : 0;
 }
@@ -1269,20 +1326,21 @@ static int ensure_fused_buffers(minife_ctx *c) {   // never called while a strea
 
 // Single-launch solvers for small single-part problems (SEG/SYM): 0 = none, 1 = one CTA
 // (k_cg_small, <= SMALL_MAX_ROWS rows), 2 = one thread-block cluster (k_cg_cluster, <=
-// CL_MAX_ROWS rows).  MINIFE_SMALL=0/1/2 forces a choice (where it fits).  Profile mode always
-// times the multi-kernel sequence.
+// CL_MAX_ROWS rows).  Option "small_solver" = 0/1/2 forces a choice (where it fits).  Profile
+// mode always times the multi-kernel sequence.
+static bool cluster_available(const Part &p) {
+    DevGuard g(p.dev);
+    return cluster_solver_available();
+}
 static int small_mode(const minife_ctx *c) {
-    static int env = -2;
-    if (env == -2) {
-        const char *e = getenv("MINIFE_SMALL");
-        env = e ? atoi(e) : -1;
-    }
+    const int env = c->opt.small_solver;
     const Part &p = c->parts[0];
     if (env == 0 || c->parts.size() != 1 || c->world != 1 || p.ncols != p.rows ||
         (c->fmt != MINIFE_FMT_SEG && c->fmt != MINIFE_FMT_SYM))
         return 0;
     const bool fits1 = p.rows <= SMALL_MAX_ROWS;
-    const bool fits2 = p.rows <= CL_MAX_ROWS && (p.nslices + CL_CTAS - 1) / CL_CTAS <= CL_MAX_SL;
+    const bool fits2 = p.rows <= CL_MAX_ROWS &&
+                       (p.nslices + CL_CTAS - 1) / CL_CTAS <= CL_MAX_SL && cluster_available(p);
     if (env == 1) return fits1 ? 1 : 0;
     if (env == 2) return fits2 ? 2 : 0;
     return fits2 ? 2 : (fits1 ? 1 : 0);
@@ -1304,7 +1362,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
     TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true), true, p.grid_spmv,
+        LAUNCH(c, launch_spmv(spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true), true, p.grid_spmv,
                                 launch_stream(c, p)));
     }
     TRY(tw_mark(c, k, true));
@@ -1313,7 +1371,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
         DevGuard g(p.dev);
         UpdArgs u6 = upd_args(c, p, 0);
         u6.alpha_hist = p.d_alpha;
-        CUDA_TRY(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
+        LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
     }
     TRY(enqueue_allreduce(c, 1));
     if (halo) {
@@ -1323,7 +1381,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
             DevGuard g(p.dev);
             UpdArgs a = upd_args(c, p, 1);
             a.p = x2_pbuf(c, p, k);
-            CUDA_TRY(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
+            LAUNCH(c, launch_pack_next_p(a, k, p.d_send_row, p.d_send_col, p.d_sendbuf,
                                            (int64_t)p.plan.send_idx.size(), launch_stream(c, p)));
         }
         for (auto &p : c->parts) {
@@ -1344,7 +1402,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
         UpdArgs u7 = upd_args(c, p, 1);
         u7.alpha_hist = p.d_alpha;
         set_ring(c, p, u7);
-        CUDA_TRY(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1), p.grid_upd,
+        LAUNCH(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1), p.grid_upd,
                                      launch_stream(c, p)));
     }
     if (halo) {
@@ -1369,7 +1427,7 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
             UpdArgs u = upd_args(c, p, 0);
             u.alpha_hist = p.d_alpha;
             set_ring(c, p, u);
-            CUDA_TRY(c, launch_x2_finish(u, launch_stream(c, p)));
+            LAUNCH(c, launch_x2_finish(u, launch_stream(c, p)));
         }
         return MINIFE_OK;
     }
@@ -1378,10 +1436,10 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
         Part &p = c->parts[0];
         DevGuard g(p.dev);
         if (sm == 1)
-            CUDA_TRY(c, launch_cg_small(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
+            LAUNCH(c, launch_cg_small(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
                                         launch_stream(c, p)));
         else
-            CUDA_TRY(c, launch_cg_cluster(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
+            LAUNCH(c, launch_cg_cluster(matrix_of(c, p), upd_args(c, p, 0), max_iters, tol,
                                           launch_stream(c, p)));
         return MINIFE_OK;
     }
@@ -1399,7 +1457,7 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
         DevGuard g(p.dev);
         UpdArgs u = upd_args(c, p, 0);
         u.acc_in = p.acc_rr(max_iters);
-        CUDA_TRY(c, launch_cg_finish(u, max_iters, p.p_buf(0), p.p_buf(1), p.grid_upd,
+        LAUNCH(c, launch_cg_finish(u, max_iters, p.p_buf(0), p.p_buf(1), p.grid_upd,
                                      launch_stream(c, p)));
         if (t) t->mark(2);
     }
@@ -1466,14 +1524,9 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
     DevGuard g(p0.dev);
-    // MINIFE_GRAPH=0: enqueue every solve directly instead of replaying a captured graph
+    // option "graph" = 0: enqueue every solve directly instead of replaying a captured graph
     // (an escape hatch for environments where capturing the NCCL calls of RANK ctxs fails)
-    static int graphs = -1;
-    if (graphs < 0) {
-        const char *e = getenv("MINIFE_GRAPH");
-        graphs = e ? atoi(e) : 1;
-    }
-    bool eager = c->mode == MINIFE_MODE_MULTI || !graphs || c->eager;
+    bool eager = c->mode == MINIFE_MODE_MULTI || !c->opt.graph || c->eager;
     if (!eager && (!c->gexec || c->g_iters != max_iters || c->g_tol != tol)) {
         drop_graph(c);
         // capture on the ctx's own stream (a torch stream may be the legacy default one)
@@ -1481,7 +1534,10 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         cudaStream_t saved = c->user_stream;
         c->user_stream = nullptr;
         CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        const int64_t k0 = c->enq_kernels;
         int st = enqueue_solve(c, max_iters, tol, nullptr);
+        const int64_t captured = c->enq_kernels - k0;
+        c->enq_kernels = k0;
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(cap, &graph);
         c->user_stream = saved;
@@ -1503,6 +1559,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         } else {
             c->g_iters = max_iters;
             c->g_tol = tol;
+            c->g_kernels = captured;
         }
     }
     if (eager) {
@@ -1518,6 +1575,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         cudaStream_t s = launch_stream(c, p0);
         CUDA_TRY(c, cudaEventRecord(c->ev0, s));
         CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
+        c->kernel_launches += c->g_kernels;
         CUDA_TRY(c, cudaEventRecord(c->ev1, s));
     }
     CUDA_TRY(c, cudaEventSynchronize(c->ev1));
@@ -1668,19 +1726,24 @@ extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
             gather_owned(p.plan, x, tmp.data());
             src = tmp.data();
         }
+        // stream-ordered with the SpMV below (a pageable cudaMemcpy may return before its DMA
+        // lands, and the legacy stream is not ordered with the non-blocking ctx streams)
+        cudaStream_t s = launch_stream(c, p);
         if (p.ncols == p.rows) {
-            CUDA_TRY(c, cudaMemcpy(p.d_xin, src, sizeof(double) * p.rows, cudaMemcpyHostToDevice));
+            CUDA_TRY(c, cudaMemcpyAsync(p.d_xin, src, sizeof(double) * p.rows,
+                                        cudaMemcpyHostToDevice, s));
         } else {
             colv.assign(p.ncols, 0.0);
             rows_to_cols(p.plan, src, colv.data());
-            CUDA_TRY(c, cudaMemcpy(p.d_xin, colv.data(), sizeof(double) * p.ncols,
-                                   cudaMemcpyHostToDevice));
+            CUDA_TRY(c, cudaMemcpyAsync(p.d_xin, colv.data(), sizeof(double) * p.ncols,
+                                        cudaMemcpyHostToDevice, s));
         }
+        CUDA_TRY(c, cudaStreamSynchronize(s));     // tmp/colv are reused by the next part
     }
     TRY(enqueue_halo(c, [](Part &p) { return p.d_xin; }));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        CUDA_TRY(c, launch_spmv(spmv_args(c, p, p.d_xin, p.d_yout, false), false, p.grid_spmv,
+        LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_xin, p.d_yout, false), false, p.grid_spmv,
                                 launch_stream(c, p)));
     }
     for (auto &p : c->parts) {
@@ -1704,7 +1767,7 @@ extern "C" int minife_spmv_device(minife_ctx *c, const double *d_x, double *d_y,
     Part &p = c->parts[0];
     DevGuard g(p.dev);
     cudaStream_t s = stream ? (cudaStream_t)stream : stream_of(c, p);
-    CUDA_TRY(c, launch_spmv(spmv_args(c, p, d_x, d_y, false), false, p.grid_spmv, s));
+    LAUNCH(c, launch_spmv(spmv_args(c, p, d_x, d_y, false), false, p.grid_spmv, s));
     return MINIFE_OK;
 }
 
@@ -1748,6 +1811,7 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
     o->rows = c->mesh.rows();
     o->nnz = c->mesh.nnz();
     o->format = c->fmt;
+    o->kernel_launches = c->kernel_launches + c->enq_kernels;
     for (auto &p : c->parts) {
         o->local_rows += p.rows;
         o->local_nnz += p.nnz;
@@ -1790,7 +1854,8 @@ static int extract_part_rows(minife_ctx *c, Part &p, const std::vector<int64_t> 
     int st = MINIFE_OK;
     for (int64_t b = 0; b < k && st == MINIFE_OK; b += chunk) {
         const int64_t n = std::min(chunk, k - b);
-        cudaError_t e = cudaMemcpy(d_rows, loc.data() + b, 8 * n, cudaMemcpyHostToDevice);
+        cudaError_t e = cudaMemcpyAsync(d_rows, loc.data() + b, 8 * n, cudaMemcpyHostToDevice,
+                                        p.stream);
         if (e == cudaSuccess)
             e = launch_extract_rows(matrix_of(c, p), geom_of(c, p), d_rows, n, d_oc, d_ov, d_ol,
                                     p.stream);

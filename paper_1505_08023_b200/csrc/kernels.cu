@@ -2439,9 +2439,6 @@ static void query_occupancy() {
     for (int f = 0; f < 2; ++f)
         if (g_spmv_bps[f] <= 0) g_spmv_bps[f] = 1;
     if (g_upd_bps <= 0) g_upd_bps = 1;
-    // A/B: CTAs per SM of the update kernels (grid = SMs x this), capped by the occupancy
-    if (const char *e = getenv("MINIFE_K6_BPS")) g_upd_bps = std::max(1, std::min(g_upd_bps, atoi(e)));
-    if (const char *e = getenv("MINIFE_K7_BPS")) g_updp_bps = std::max(1, std::min(g_updp_bps, atoi(e)));
 }
 
 int spmv_grid(int64_t nslices, int fmt) {
@@ -2542,13 +2539,8 @@ template <bool DOT>
 static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
     // default: mirrored values staged by tensor-map TMA (13 consumer warps, 2 stages; B200,
     // 300^3: 1.196 ms per CG iteration vs 1.243 with L1 mirror gathers, profiles/r01/session2);
-    // MINIFE_SYM_CFG=0 (or no tensor-map support) selects the L1-gather kernel
-    static int cfg = -1;
-    if (cfg < 0) {
-        const char *e = getenv("MINIFE_SYM_CFG");
-        cfg = e ? atoi(e) : 1;
-    }
-    if (cfg == 1) {
+    // the ctx option "sym_kernel" = 0 (or no tensor-map support) selects the L1-gather kernel
+    if (a.sym_kernel != 0) {
         const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
         static bool warned = false;
@@ -2586,13 +2578,9 @@ cudaError_t launch_cg_finish(const UpdArgs &a, int K, const double *p_even, cons
 
 // Kernel choice per format (measured on B200, 300^3, profiles/r01): SEG -> TMA pipeline
 // (1.105 ms vs 1.442 ms register-streaming); CRS -> register streaming (1.48 ms vs 1.77 ms
-// for its 2-stage TMA variant).  MINIFE_SPMV_IMPL=tma|reg overrides for experiments.
-static int spmv_impl(int fmt) {
-    static int forced = -2;
-    if (forced == -2) {
-        const char *e = getenv("MINIFE_SPMV_IMPL");
-        forced = !e ? -1 : (e[0] == 't' ? 1 : (e[0] == 'r' ? 0 : -1));
-    }
+// for its 2-stage TMA variant).  The ctx option "spmv_impl" (1 TMA, 0 register streaming)
+// overrides the choice for experiments.
+static int spmv_impl(int fmt, int forced) {
     if (fmt == FMT_SYM) return 1;                       // TMA kernel only
     if (forced >= 0) return forced;
     return fmt == FMT_SEG ? 1 : 0;
@@ -2607,7 +2595,7 @@ cudaError_t launch_spmv(const SpmvArgs &a, bool with_dot, int grid, cudaStream_t
     if (a.m.fmt == FMT_SYM) {
         return with_dot ? launch_sym<true>(a, s) : launch_sym<false>(a, s);
     }
-    if (spmv_impl(a.m.fmt) == 1) {
+    if (spmv_impl(a.m.fmt, a.impl) == 1) {
         if (a.m.fmt == FMT_SEG)
             return with_dot ? launch_tma<true, FMT_SEG, true>(a, s)
                             : launch_tma<false, FMT_SEG, true>(a, s);
@@ -2640,16 +2628,46 @@ cudaError_t launch_cg_small(const Matrix &m, const UpdArgs &a, int K, double tol
     return cudaGetLastError();
 }
 
+// Can a CL_CTAS-CTA cluster of k_cg_cluster be scheduled on the current device (MIG, MPS or
+// SM-limited partitions may not fit a non-portable 16-CTA cluster)?  Queried once per device.
+bool cluster_solver_available() {
+    static signed char known[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    signed char &k = known[dev & 63];
+    if (k) return k > 0;
+    const int smem = (int)sizeof(ClusterSmem);
+    int n = 0;
+    cudaError_t e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_cg_cluster<FMT_SYM, true>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(CL_CTAS, 1, 1);
+        cfg.blockDim = dim3(CL_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL_CTAS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaOccupancyMaxActiveClusters(&n, k_cg_cluster<FMT_SYM, true>, &cfg);
+    }
+    if (e != cudaSuccess) cudaGetLastError();
+    k = (e == cudaSuccess && n > 0) ? 1 : -1;
+    return k > 0;
+}
+
 cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double tol,
                               cudaStream_t s) {
     if (m.rows > CL_MAX_ROWS || (m.nslices + CL_CTAS - 1) / CL_CTAS > CL_MAX_SL ||
         !a.g.ident || (m.fmt != FMT_SEG && m.fmt != FMT_SYM) || m.slice_row)
         return cudaErrorInvalidValue;
-    static int dd = -1;
-    if (dd < 0) {
-        const char *e = getenv("MINIFE_CL_DD");
-        dd = (e && e[0] == '0') ? 0 : 1;
-    }
+    const int dd = a.cl_dd;
     auto kern = m.fmt == FMT_SEG ? (dd ? k_cg_cluster<FMT_SEG, true> : k_cg_cluster<FMT_SEG, false>)
                                  : (dd ? k_cg_cluster<FMT_SYM, true> : k_cg_cluster<FMT_SYM, false>);
     const int smem = (int)sizeof(ClusterSmem);
@@ -2748,20 +2766,13 @@ cudaError_t launch_init_finalize(const UpdArgs &a, double tol, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// x/r and p updates.  XL (default; MINIFE_X_LATE=0 restores the textbook split): K6 updates
-// r only and K7 applies x += alpha_k p_k while it reads p_k for p_(k+1) = r + beta p_k, so p
-// is read once per iteration (64 instead of 72 B per row).  Same values, same operations.
-static bool x_late() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MINIFE_X_LATE");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
+// x/r and p updates.  XL (default; the ctx option "x_late" = 0 restores the textbook split):
+// K6 updates r only and K7 applies x += alpha_k p_k while it reads p_k for
+// p_(k+1) = r + beta p_k, so p is read once per iteration (64 instead of 72 B per row).  Same
+// values, same operations.
 
 cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    const bool xl = x_late() || a.alpha_hist;     // x-every-2 scheme: K6 updates r only
+    const bool xl = a.x_late || a.alpha_hist;     // x-every-2 scheme: K6 updates r only
     if (a.g.ident) {
         if (xl) k_update_xr<true, true><<<grid, UPD_THREADS, 0, s>>>(a, k);
         else k_update_xr<true, false><<<grid, UPD_THREADS, 0, s>>>(a, k);
@@ -2773,7 +2784,7 @@ cudaError_t launch_update_xr(const UpdArgs &a, int k, int grid, cudaStream_t s) 
 }
 
 cudaError_t launch_update_p(const UpdArgs &a, int k, int grid, cudaStream_t s) {
-    const bool xl = x_late();
+    const bool xl = a.x_late;
     if (a.g.ident) {
         // K7 has its own (higher) occupancy than K6, whose grid is passed in
         const int64_t need = (a.g.rows / 2 + UPD_THREADS - 1) / UPD_THREADS;

@@ -88,6 +88,8 @@ struct SpmvArgs {
     int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
     int val_evict_first;                // SYMM: stream the values evict-first in L2
     int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
+    int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
+    int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
     unsigned long long *acc;            // pAp accumulator (DOT only)
@@ -120,6 +122,8 @@ struct UpdArgs {
     // ring[(k-1) % xdef]
     const double *ring[8];
     int xdef;
+    int x_late;                         // K7 applies x += alpha p (1, default) or K6 does (0)
+    int cl_dd;                          // cluster solver: DSMEM digit pushes (1, default)
 };
 constexpr int XDEF_MAX = 8;
 
@@ -158,6 +162,7 @@ constexpr int CL_CTAS = 16, CL_THREADS = 256, CL_WARPS = CL_THREADS / 32, CL_MAX
               CL_RPT = CL_MAX_SL / CL_WARPS, CL_MAX_ROWS = CL_CTAS * CL_MAX_SL * 32;
 cudaError_t launch_cg_cluster(const Matrix &m, const UpdArgs &a, int K, double tol,
                               cudaStream_t s);
+bool cluster_solver_available();     // a CL_CTAS-CTA cluster fits this device (once per device)
 
 // SYM with a halo: sendbuf[i] = r[send_row[i]] + beta_k p[send_col[i]] (p_(k+1) at the send
 // list, ahead of K7), beta_k from the rr accumulator a.acc_in and a.rr[k-1].

@@ -1,4 +1,4 @@
-"""Subprocess helper for test_gpu_parity: the single-launch cluster solver (MINIFE_SMALL=2) run
+"""Subprocess helper for test_gpu_parity: the single-launch cluster solver (option small_solver = 2) run
 right after large SpMV launches that leave their data in every SM's shared memory, repeatedly,
 each solve compared with the oracle bit for bit (the solver must not read shared memory it has
 not written: a fresh-process race of this kind was fixed, profiles/r01/session3 §5).  Prints
@@ -23,7 +23,7 @@ rows = big.io_rows
 x = torch.rand(rows + 64, dtype=torch.float64, device="cuda") * 1e300   # loud garbage
 y = torch.empty_like(x)
 stream = torch.cuda.current_stream().cuda_stream
-with M.Minife(*n, fmt=M.FMT_SYM) as g:
+with M.Minife(*n, fmt=M.FMT_SYM, options={"small_solver": 2}) as g:
     g.assemble()
     for rep in range(20):
         for _ in range(3):

@@ -149,67 +149,74 @@ def test_overlapped_halo_split_bit_identical(n, p, transport, fmt):
         check_cg(g, n, 200, 0.0)
 
 
-@pytest.mark.parametrize("small", ["0", "1", "2"])
-@pytest.mark.parametrize("n,fmt", [((10, 10, 10), "sym"), ((10, 10, 10), "seg"),
-                                   ((23, 17, 9), "sym"), ((7, 1, 3), "seg")])
+def _solver_variant(n, fmt, options):
+    """One mesh through the library with the given ctx options; bitwise the oracle for a
+    200-iteration solve, a tolerance stop and an odd iteration count."""
+    s = oracle_system(n)
+    with M.Minife(*n, fmt=fmt, options=options) as g:
+        g.assemble()
+        for iters, tol in ((200, 0.0), (200, 1e-8), (7, 0.0)):
+            r = g.cg_solve(iters, tol)
+            o = oracle_cg(n, iters, tol)
+            assert (r.status, r.iterations, r.converged) == (o.status, o.iters, o.converged)
+            assert _same(g.history(), o.hist)
+            assert _same(g.solution(), o.x)
+
+
+@pytest.mark.parametrize("small", [0, 1, 2])
+@pytest.mark.parametrize("n,fmt", [((10, 10, 10), M.FMT_SYM), ((10, 10, 10), M.FMT_SEG),
+                                   ((23, 17, 9), M.FMT_SYM), ((7, 1, 3), M.FMT_SEG)])
 def test_single_launch_solvers_bit_identical(n, fmt, small):
-    """MINIFE_SMALL=1 one-CTA solver, 2 one-cluster solver (DSMEM),
-    0 the three-kernel graph -- each bitwise the oracle (subprocess: the selection is read
-    once per process)."""
-    import os
-    import subprocess
-    import sys
-    if small == "1" and (n[0] + 1) * (n[1] + 1) * (n[2] + 1) > 2048:
+    """option small_solver = 1 one-CTA solver, 2 one-cluster solver
+    (DSMEM), 0 the three-kernel graph -- each bitwise the oracle."""
+    if small == 1 and (n[0] + 1) * (n[1] + 1) * (n[2] + 1) > 2048:
         pytest.skip("one-CTA solver holds <= 2048 rows")
-    env = dict(os.environ, MINIFE_SMALL=small)
-    here = os.path.dirname(os.path.abspath(__file__))
-    out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
-                          *map(str, n), fmt], env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    _solver_variant(n, fmt, {"small_solver": small})
 
 
-@pytest.mark.parametrize("xdef", ["2", "5", "8"])
-@pytest.mark.parametrize("n,fmt", [((23, 17, 9), "sym"), ((33, 32, 31), "seg"), ((7, 1, 3), "sym")])
+@pytest.mark.parametrize("xdef", [2, 5, 8])
+@pytest.mark.parametrize("n,fmt", [((23, 17, 9), M.FMT_SYM), ((33, 32, 31), M.FMT_SEG),
+                                   ((7, 1, 3), M.FMT_SYM)])
 def test_x_every_second_iteration_bit_identical(n, fmt, xdef):
     """the deferred x update, every X iterations from a ring of X p buffers (forced
-    at any size with MINIFE_X2=X, the multi-kernel path with MINIFE_SMALL=0): 200 iterations,
-    a tolerance stop and an odd count (7) leave nothing pending -- bitwise the oracle."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, MINIFE_X2=xdef, MINIFE_SMALL="0")
-    here = os.path.dirname(os.path.abspath(__file__))
-    out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
-                          *map(str, n), fmt], env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    at any size with option x_defer = X, the multi-kernel path with small_solver = 0): 200
+    iterations, a tolerance stop and an odd count (7) leave nothing pending -- bitwise the
+    oracle."""
+    _solver_variant(n, fmt, {"x_defer": xdef, "small_solver": 0})
 
 
 @pytest.mark.parametrize("n", [(23, 17, 9), (33, 32, 31)])
 def test_sym_fallback_kernel_bit_identical(n):
-    """The L1-gather SYM SpMV (`k_spmv_sym`, used where tensor maps are unavailable;
-    MINIFE_SYM_CFG=0 selects it) through the three-kernel path: bitwise the oracle
-    (subprocess: the selection is read once per process)."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, MINIFE_SYM_CFG="0", MINIFE_SMALL="0")
-    here = os.path.dirname(os.path.abspath(__file__))
-    out = subprocess.run([sys.executable, os.path.join(here, "_solver_variant.py"),
-                          *map(str, n), "sym"], env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    """The L1-gather SYM SpMV (`k_spmv_sym`, used where tensor maps are unavailable; option
+    sym_kernel = 0 selects it) through the three-kernel path: bitwise the oracle."""
+    _solver_variant(n, M.FMT_SYM, {"sym_kernel": 0, "small_solver": 0})
+
+
+@pytest.mark.parametrize("opts", [{"x_late": 0}, {"cluster_dd": 0, "small_solver": 2},
+                                  {"graph": 0}, {"spmv_impl": 0}, {"val_evict_first": 1},
+                                  {"x_prefetch": 1, "small_solver": 0}])
+def test_other_options_bit_identical(opts):
+    fmt = M.FMT_SEG if "spmv_impl" in opts else M.FMT_SYM
+    _solver_variant((10, 10, 10), fmt, opts)
+    _solver_variant((23, 17, 9), fmt, opts)
+
+
+def test_option_errors():
+    with M.Minife(3, 3, 3) as g:
+        for name, v in (("no_such_option", 1), ("x_defer", 9), ("graph", 2), ("small_solver", -2)):
+            with pytest.raises(M.MinifeError) as e:
+                g.set_option(name, v)
+            assert e.value.status == M.MINIFE_EINVAL
 
 
 def test_cluster_solver_after_spmv_leftovers():
     """The one-cluster solver right after SpMV launches that fill every SM's shared memory
-    with other data: 20 solves, each bitwise the oracle (subprocess: MINIFE_SMALL is read once
-    per process)."""
+    with other data: 20 solves, each bitwise the oracle (a fresh process: the race this guards
+    against showed up in one)."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, MINIFE_SMALL="2")
+    env = dict(os.environ)
     here = os.path.dirname(os.path.abspath(__file__))
     out = subprocess.run([sys.executable, os.path.join(here, "_cluster_after_spmv.py")], env=env,
                          capture_output=True, text=True, timeout=300)
