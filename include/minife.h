@@ -37,14 +37,21 @@ extern "C" {
 #define MINIFE_ENOTSPD 6     /* CG met pAp < 0, or pAp == 0 with rr != 0 */
 #define MINIFE_EDIVERGED 7   /* CG met a non-finite pAp or rr */
 #define MINIFE_ENODEV 8      /* no CUDA device (or fewer than requested) */
+#define MINIFE_ECOMM 9       /* device-initiated comm: a peer did not signal in time (dead or
+                                hung rank, broken mapping); see option comm_timeout_ms     */
 
 /* ---- context modes ---------------------------------------------------------------------- */
 #define MINIFE_MODE_SINGLE 0   /* one process, one GPU, one part */
 #define MINIFE_MODE_VIRTUAL 1  /* one process, one GPU, p RCB parts ("virtual ranks") */
-#define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1: NCCL all-reduce;
-                                  halo by peer push over NVLink when every device pair has
-                                  peer access (else NCCL send/recv) */
-#define MINIFE_MODE_RANK 3     /* SPMD: this process is rank r of w (torchrun), NCCL comm */
+#define MINIFE_MODE_MULTI 2    /* one process driving devices 0..ngpu-1.  With peer access
+                                  between every device pair: device-initiated comm (halo
+                                  pushed over NVLink by the p-update's sender, exact
+                                  accumulators reduced in-kernel through peer stores + flags)
+                                  and one CUDA graph per device; otherwise NCCL send/recv and
+                                  all-reduce, enqueued directly */
+#define MINIFE_MODE_RANK 3     /* SPMD: this process is rank r of w (torchrun).  Device comm
+                                  over CUDA-IPC mappings exchanged at creation when every rank
+                                  can map every other; otherwise NCCL (graph-captured) */
 
 /* ---- matrix storage formats ---------------------------------------------- */
 #define MINIFE_FMT_CRS 0       /* SELL-32, one int32 column per stored entry: the paper's CRS
@@ -83,6 +90,11 @@ extern "C" {
                                       part stores every send slot straight into the receiver's
                                       halo column.  MULTI ctxs use it over NVLink when every
                                       device pair has peer access.                            */
+#define MINIFE_TRANSPORT_DEVICE 3  /* the device-initiated protocol of MULTI/RANK ctxs on one GPU:
+                                      PUSH for the halo plus in-kernel reductions -- every part
+                                      stores its exact accumulator into every part's inbox and
+                                      raises a release flag; consumers wait on acquire flags
+                                      (DESIGN.md §7).  No host-launched collective.          */
 
 typedef struct minife_ctx minife_ctx;
 
@@ -192,6 +204,11 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *   "spmv_impl"       SEG/CRS SpMV: -1 auto, 1 TMA pipeline, 0 register streaming
  *   "x_late"          1 (default) K7 applies x += alpha p with the p it reads, 0 K6 does
  *   "cluster_dd"      cluster solver digit exchange: 1 (default) DSMEM pushes, 0 pulls
+ *   "device_comm"     MULTI/RANK: -1 (default) device-initiated comm where it was set up at
+ *                     creation, 0 NCCL transport; RANK at world 1: 1 forces the device
+ *                     reduction kernels (self-exchange).  Set identically on every rank.
+ *   "comm_timeout_ms" device comm: how long a kernel waits for a peer's flag before the
+ *                     solve fails with MINIFE_ECOMM (default 60000)
  * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,
  * value out of range). */
 int minife_set_option(minife_ctx *ctx, const char *name, int64_t value);
@@ -206,9 +223,10 @@ const char *minife_last_error(const minife_ctx *ctx);
  * summation order).  Errors: MINIFE_EINVAL (ctx NULL or unknown format). */
 int minife_set_format(minife_ctx *ctx, int format);
 
-/* VIRTUAL ctxs: select the halo transport (MINIFE_TRANSPORT_*), so the wire protocol of the
- * multi-GPU modes runs, bit-exactly checkable, on one GPU.  Errors: MINIFE_EINVAL (NULL,
- * unknown transport), MINIFE_ESTATE (not a VIRTUAL ctx). */
+/* VIRTUAL ctxs: select the halo transport (MINIFE_TRANSPORT_*), so the protocols of the
+ * multi-GPU modes (NCCL wire protocol, device push, device-initiated reductions) run,
+ * bit-exactly checkable, on one GPU.  Errors: MINIFE_EINVAL (NULL, unknown transport),
+ * MINIFE_ESTATE (not a VIRTUAL ctx). */
 int minife_set_transport(minife_ctx *ctx, int transport);
 
 /* Select the CG iteration scheme of later solves (MINIFE_SCHEME_*).  Both schemes perform

@@ -40,10 +40,11 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 MINIFE_OK, MINIFE_EINVAL, MINIFE_ESTATE, MINIFE_ECUDA, MINIFE_ENCCL = 0, 1, 2, 3, 4
 MINIFE_ENOMEM, MINIFE_ENOTSPD, MINIFE_EDIVERGED, MINIFE_ENODEV = 5, 6, 7, 8
+MINIFE_ECOMM = 9
 MODE_SINGLE, MODE_VIRTUAL, MODE_MULTI, MODE_RANK = 0, 1, 2, 3
 FMT_CRS, FMT_SEG, FMT_SYM = 0, 1, 2
 SCHEME_3K, SCHEME_FUSED = 0, 1
-TRANSPORT_DIRECT, TRANSPORT_WIRE, TRANSPORT_PUSH = 0, 1, 2
+TRANSPORT_DIRECT, TRANSPORT_WIRE, TRANSPORT_PUSH, TRANSPORT_DEVICE = 0, 1, 2, 3
 
 
 class minife_part_info(ctypes.Structure):
@@ -296,7 +297,9 @@ class Minife:
         self.info = self.get_info()
 
     def set_transport(self, transport: int):
-        """VIRTUAL ctxs: TRANSPORT_DIRECT (default) or TRANSPORT_WIRE (the NCCL-mode protocol)."""
+        """VIRTUAL ctxs: TRANSPORT_DIRECT (default), TRANSPORT_WIRE (the NCCL-mode protocol),
+        TRANSPORT_PUSH (device halo push) or TRANSPORT_DEVICE (push + in-kernel reductions:
+        the device-initiated protocol of MULTI/RANK ctxs)."""
         self._check(minife_set_transport(self.h, transport), "minife_set_transport")
 
     def set_option(self, name: str, value: int):

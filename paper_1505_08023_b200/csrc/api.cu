@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,12 @@ struct NcclApi {
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
                               ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t);
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int,
+                           ncclComm_t, cudaStream_t);
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
+    ncclResult_t (*CommAbort)(ncclComm_t);
 };
 
 const NcclApi *nccl() {
@@ -71,6 +78,10 @@ const NcclApi *nccl() {
     api.Send = (decltype(api.Send))sym("ncclSend");
     api.Recv = (decltype(api.Recv))sym("ncclRecv");
     api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+    api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))sym("ncclCommGetAsyncError");
+    api.CommAbort = (decltype(api.CommAbort))sym("ncclCommAbort");
     state = ok ? 1 : -1;
     return ok ? &api : nullptr;
 }
@@ -107,6 +118,13 @@ struct Part {
     int32_t *d_push_dst = nullptr;
     double **d_push_ptr = nullptr;
     cudaEvent_t ev_push = nullptr;
+    // device-initiated comm (DevComm, kernels.h): this part's comm region, the table of every
+    // rank's region as seen from this device, the neighbor ranks; RANK: CUDA-IPC mappings of
+    // the other ranks' regions and p arrays (closed on destroy)
+    unsigned long long *d_comm = nullptr;
+    unsigned long long **d_comm_ptrs = nullptr;
+    int32_t *d_nbr_rank = nullptr;
+    std::vector<void *> ipc_opened;
     double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
     // SEG slice storage order (multi-part): interior slices [0, n_int) first, DESIGN.md §7
     int32_t *d_slice_row = nullptr, *d_slice_pos = nullptr;
@@ -172,7 +190,12 @@ struct minife_ctx {
         int spmv_impl = -1;        // SEG/CRS SpMV: 1 TMA pipeline, 0 register streaming
         int x_late = 1;            // x += alpha p applied by K7 (1) or K6 (0)
         int cluster_dd = 1;        // cluster solver: DSMEM digit pushes
+        int device_comm = -1;      // MULTI/RANK: 1 device-initiated comm, 0 NCCL, -1 auto
+        int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
     } opt;
+    bool devcomm_ready = false;                  // regions + peer tables built
+    int cur_max_iters = 0;                       // max_iters of the solve being enqueued
+    std::vector<cudaGraphExec_t> gexec_parts;    // MULTI + device comm: one graph per device
     // kernel launch accounting: enq_kernels counts launch_* calls as they are enqueued (into a
     // capture or directly); g_kernels = kernels in the captured solve graph; kernel_launches =
     // kernels launched by this ctx so far (graph replays included)
@@ -279,7 +302,9 @@ static void free_part(Part &p) {
                     p.d_r,         p.d_p,       p.d_Ap,      p.d_xin,      p.d_yout,  p.d_p2,
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
-                    p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha};
+                    p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha,
+                    p.d_comm,      p.d_comm_ptrs, p.d_nbr_rank};
+    for (void *q : p.ipc_opened) cudaIpcCloseMemHandle(q);
     for (void *b : bufs)
         if (b) cudaFree(b);
     for (double *b : p.d_pr)
@@ -393,45 +418,205 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     return MINIFE_OK;
 }
 
-// Push tables (MINIFE_TRANSPORT_PUSH): part p's slot j of its block for neighbor q lands in
-// q's halo slot recv_off_q[p] + j, i.e. q's extended column ext_pos_q[...]; the store goes
-// through q's p array (a peer pointer when q is on another device).
-static int setup_push(minife_ctx *c) {
-    for (auto &p : c->parts) {
-        const size_t ns = p.plan.send_idx.size();
-        std::vector<uint8_t> nb(ns);
-        std::vector<int32_t> dst(ns);
-        std::vector<double *> ptr(p.plan.nbr.size());
-        for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
-            Part &q = c->parts[p.plan.nbr[k]];
-            auto it = std::lower_bound(q.plan.nbr.begin(), q.plan.nbr.end(), p.plan.rank);
-            const size_t kq = (size_t)(it - q.plan.nbr.begin());
-            if (kq >= q.plan.nbr.size() || q.plan.nbr[kq] != p.plan.rank ||
-                q.plan.recv_cnt[kq] != p.plan.send_cnt[k] || k > 255) {
-                set_err(c, "push plan mismatch between parts %d and %d", p.plan.rank, q.plan.rank);
-                return MINIFE_ESTATE;
-            }
-            for (int64_t j = 0; j < p.plan.send_cnt[k]; ++j) {
-                nb[p.plan.send_off[k] + j] = (uint8_t)k;
-                dst[p.plan.send_off[k] + j] = (int32_t)q.plan.ext_pos[q.plan.recv_off[kq] + j];
-            }
-            ptr[k] = q.d_p;
+// Push tables (MINIFE_TRANSPORT_PUSH / device comm): part p's slot j of its block for
+// neighbor q lands in q's halo slot recv_off_q[p] + j, i.e. q's extended column
+// ext_pos_q[...]; the store goes through q's p array as seen from p's device (the same
+// pointer on one device, a peer pointer in MULTI ctxs, a CUDA-IPC mapping in RANK ctxs:
+// `remote_p` gives it).  q's plan is recomputed on the host when q lives in another process.
+template <class RemoteP>
+static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
+    const size_t ns = p.plan.send_idx.size();
+    std::vector<uint8_t> nb(ns);
+    std::vector<int32_t> dst(ns);
+    std::vector<double *> ptr(p.plan.nbr.size());
+    for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
+        const int qr = p.plan.nbr[k];
+        Plan qown;
+        const Plan *qp = nullptr;
+        if (c->mode == MINIFE_MODE_RANK) {
+            if (!build_plan(c->mesh, c->world, qr, qown)) return MINIFE_ESTATE;
+            qp = &qown;
+        } else {
+            qp = &c->parts[qr].plan;
         }
-        DevGuard g(p.dev);
+        const Plan &q = *qp;
+        auto it = std::lower_bound(q.nbr.begin(), q.nbr.end(), p.plan.rank);
+        const size_t kq = (size_t)(it - q.nbr.begin());
+        if (kq >= q.nbr.size() || q.nbr[kq] != p.plan.rank ||
+            q.recv_cnt[kq] != p.plan.send_cnt[k] || k > 255) {
+            set_err(c, "push plan mismatch between parts %d and %d", p.plan.rank, qr);
+            return MINIFE_ESTATE;
+        }
+        for (int64_t j = 0; j < p.plan.send_cnt[k]; ++j) {
+            nb[p.plan.send_off[k] + j] = (uint8_t)k;
+            dst[p.plan.send_off[k] + j] = (int32_t)q.ext_pos[q.recv_off[kq] + j];
+        }
+        ptr[k] = remote_p(qr);
+    }
+    DevGuard g(p.dev);
+    if (!p.d_push_nbr) {
         TRY(dalloc(c, p, &p.d_push_nbr, ns));
         TRY(dalloc(c, p, &p.d_push_dst, ns));
         TRY(dalloc(c, p, &p.d_push_ptr, ptr.size()));
-        if (ns) {
-            CUDA_TRY(c, cudaMemcpy(p.d_push_nbr, nb.data(), ns, cudaMemcpyHostToDevice));
-            CUDA_TRY(c, cudaMemcpy(p.d_push_dst, dst.data(), 4 * ns, cudaMemcpyHostToDevice));
-        }
-        if (!ptr.empty())
-            CUDA_TRY(c, cudaMemcpy(p.d_push_ptr, ptr.data(), sizeof(double *) * ptr.size(),
-                                   cudaMemcpyHostToDevice));
-        CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_push, cudaEventDisableTiming));
-        CUDA_TRY(c, cudaDeviceSynchronize());     // legacy-stream copies above, see create_common
     }
+    if (ns) {
+        CUDA_TRY(c, cudaMemcpy(p.d_push_nbr, nb.data(), ns, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaMemcpy(p.d_push_dst, dst.data(), 4 * ns, cudaMemcpyHostToDevice));
+    }
+    if (!ptr.empty())
+        CUDA_TRY(c, cudaMemcpy(p.d_push_ptr, ptr.data(), sizeof(double *) * ptr.size(),
+                               cudaMemcpyHostToDevice));
+    if (!p.ev_push) CUDA_TRY(c, cudaEventCreateWithFlags(&p.ev_push, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaDeviceSynchronize());     // legacy-stream copies above, see create_common
+    return MINIFE_OK;
+}
+
+static int setup_push(minife_ctx *c) {
+    for (auto &p : c->parts)
+        TRY(build_push_tables(c, p, [c](int qr) { return c->parts[qr].d_p; }));
     c->push_ready = true;
+    return MINIFE_OK;
+}
+
+// Device comm regions (DevComm, kernels.h) of every part of this ctx, zeroed, plus the
+// neighbor-rank lists; `region_of(p, r)` = rank r's region as seen from part p's device.
+template <class RegionOf>
+static int setup_comm_tables(minife_ctx *c, RegionOf region_of) {
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        std::vector<unsigned long long *> regs(c->world);
+        for (int r = 0; r < c->world; ++r) regs[r] = region_of(p, r);
+        if (!p.d_comm_ptrs) TRY(dalloc(c, p, &p.d_comm_ptrs, c->world));
+        CUDA_TRY(c, cudaMemcpy(p.d_comm_ptrs, regs.data(), sizeof(void *) * c->world,
+                               cudaMemcpyHostToDevice));
+        std::vector<int32_t> nbr(p.plan.nbr.begin(), p.plan.nbr.end());
+        if (!p.d_nbr_rank) TRY(dalloc(c, p, &p.d_nbr_rank, nbr.size()));
+        if (!nbr.empty())
+            CUDA_TRY(c, cudaMemcpy(p.d_nbr_rank, nbr.data(), 4 * nbr.size(),
+                                   cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaDeviceSynchronize());
+    }
+    return MINIFE_OK;
+}
+
+static int alloc_comm_regions(minife_ctx *c) {
+    const int64_t words = comm_words(c->world);
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        if (!p.d_comm) TRY(dalloc(c, p, &p.d_comm, words));
+        CUDA_TRY(c, cudaMemset(p.d_comm, 0, 8 * (size_t)words));
+        CUDA_TRY(c, cudaDeviceSynchronize());
+    }
+    return MINIFE_OK;
+}
+
+// VIRTUAL and MULTI (peer access enabled): every region is addressable from every device
+static int setup_devcomm_local(minife_ctx *c) {
+    TRY(alloc_comm_regions(c));
+    TRY(setup_comm_tables(c, [c](Part &, int r) { return c->parts[r].d_comm; }));
+    c->devcomm_ready = true;
+    return MINIFE_OK;
+}
+
+// RANK ctxs (one process per GPU, torchrun): the comm region and the p array of every rank
+// are exported as CUDA-IPC handles and exchanged once with an NCCL all-gather; each rank maps
+// every other rank's region and its neighbors' p arrays.  The ranks then agree (NCCL MIN
+// all-reduce) whether every mapping succeeded: if any rank failed (no P2P between some pair,
+// IPC unavailable), all of them keep the NCCL transport.  Collective over the ranks.
+struct IpcRecord {
+    cudaIpcMemHandle_t comm, p;
+    int32_t dev, ok;
+};
+
+static int setup_devcomm_ipc(minife_ctx *c) {
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    TRY(alloc_comm_regions(c));
+    const int W = c->world, R = c->rank;
+    IpcRecord mine{};
+    mine.dev = p.dev;
+    mine.ok = cudaIpcGetMemHandle(&mine.comm, p.d_comm) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.p, p.d_p) == cudaSuccess;
+    cudaGetLastError();
+    std::vector<IpcRecord> all(W);
+    IpcRecord *d_all = nullptr;
+    int32_t *d_ok = nullptr;
+    CUDA_TRY(c, cudaMalloc((void **)&d_all, sizeof(IpcRecord) * W));
+    CUDA_TRY(c, cudaMalloc((void **)&d_ok, sizeof(int32_t)));
+    int st = MINIFE_OK;
+    cudaError_t e = cudaMemcpyAsync(d_all + R, &mine, sizeof mine, cudaMemcpyHostToDevice, p.stream);
+    ncclResult_t nr = ncclSuccess;
+    if (e == cudaSuccess)
+        nr = nccl()->AllGather(d_all + R, d_all, sizeof(IpcRecord), ncclUint8, p.comm, p.stream);
+    if (e == cudaSuccess && nr == ncclSuccess)
+        e = cudaMemcpyAsync(all.data(), d_all, sizeof(IpcRecord) * W, cudaMemcpyDeviceToHost,
+                            p.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p.stream);
+    if (e != cudaSuccess || nr != ncclSuccess) {
+        set_err(c, "IPC handle exchange: %s / %s", cudaGetErrorString(e),
+                nccl()->GetErrorString(nr));
+        st = e != cudaSuccess ? MINIFE_ECUDA : MINIFE_ENCCL;
+    }
+    // map every other rank's region, and the neighbors' p arrays
+    std::vector<unsigned long long *> regions(W, nullptr);
+    std::vector<double *> remote_p(W, nullptr);
+    int32_t ok = st == MINIFE_OK ? 1 : 0;
+    for (int r = 0; r < W && ok; ++r) {
+        if (!all[r].ok) ok = 0;
+        if (r == R) {
+            regions[r] = p.d_comm;
+            remote_p[r] = p.d_p;
+            continue;
+        }
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, p.dev, all[r].dev) != cudaSuccess || !can) ok = 0;
+        void *q = nullptr;
+        if (ok && cudaIpcOpenMemHandle(&q, all[r].comm, cudaIpcMemLazyEnablePeerAccess) ==
+                      cudaSuccess) {
+            p.ipc_opened.push_back(q);
+            regions[r] = (unsigned long long *)q;
+        } else {
+            ok = 0;
+        }
+        if (ok && std::binary_search(p.plan.nbr.begin(), p.plan.nbr.end(), r)) {
+            if (cudaIpcOpenMemHandle(&q, all[r].p, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+                p.ipc_opened.push_back(q);
+                remote_p[r] = (double *)q;
+            } else {
+                ok = 0;
+            }
+        }
+        cudaGetLastError();
+    }
+    // every rank must take the same transport
+    if (st == MINIFE_OK) {
+        e = cudaMemcpyAsync(d_ok, &ok, sizeof ok, cudaMemcpyHostToDevice, p.stream);
+        if (e == cudaSuccess)
+            nr = nccl()->AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, p.comm, p.stream);
+        if (e == cudaSuccess && nr == ncclSuccess)
+            e = cudaMemcpyAsync(&ok, d_ok, sizeof ok, cudaMemcpyDeviceToHost, p.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p.stream);
+        if (e != cudaSuccess || nr != ncclSuccess) {
+            set_err(c, "transport agreement: %s / %s", cudaGetErrorString(e),
+                    nccl()->GetErrorString(nr));
+            st = e != cudaSuccess ? MINIFE_ECUDA : MINIFE_ENCCL;
+        }
+    }
+    cudaFree(d_all);
+    cudaFree(d_ok);
+    if (st != MINIFE_OK) return st;
+    if (!ok) {                                   // NCCL transport on every rank
+        for (void *q : p.ipc_opened) cudaIpcCloseMemHandle(q);
+        p.ipc_opened.clear();
+        cudaGetLastError();
+        return MINIFE_OK;
+    }
+    TRY(setup_comm_tables(c, [&regions](Part &, int r) { return regions[r]; }));
+    if (W > 1) {
+        TRY(build_push_tables(c, p, [&remote_p](int qr) { return remote_p[qr]; }));
+        c->push_ready = true;
+    }
+    c->devcomm_ready = true;
     return MINIFE_OK;
 }
 
@@ -450,14 +635,36 @@ static bool enable_peers(minife_ctx *c) {
     return true;
 }
 
+// Device-initiated comm in use for the next solve: VIRTUAL with MINIFE_TRANSPORT_DEVICE; MULTI
+// and RANK when the regions are mapped (peer access / CUDA IPC) unless option device_comm = 0
+// (RANK at world 1 only when forced with device_comm = 1: it exercises the same kernels).
+static bool devcomm(const minife_ctx *c) {
+    if (!c->devcomm_ready) return false;
+    if (c->mode == MINIFE_MODE_VIRTUAL) return c->world > 1 && c->transport == MINIFE_TRANSPORT_DEVICE;
+    if (c->world == 1) return c->mode == MINIFE_MODE_RANK && c->opt.device_comm == 1;
+    return c->opt.device_comm != 0;
+}
+
 static bool push_mode(const minife_ctx *c) {
+    if (devcomm(c)) return c->world > 1;
     return c->world > 1 && c->push_ready &&
            (c->mode == MINIFE_MODE_MULTI ||
             (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_PUSH));
 }
 
-// MULTI: each part's compute stream waits for its neighbors' push kernels
-static int push_wait(minife_ctx *c) {
+static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in);
+
+// Before SpMV(k): device comm -> a wait kernel per part (neighbors' halo flags); MULTI with
+// NCCL reductions -> each part's compute stream waits for its neighbors' push kernels
+static int push_wait(minife_ctx *c, int k) {
+    if (devcomm(c)) {
+        for (auto &p : c->parts) {
+            if (p.plan.nbr.empty()) continue;
+            DevGuard g(p.dev);
+            LAUNCH(c, launch_halo_wait(upd_args(c, p, 0), k, launch_stream(c, p)));
+        }
+        return MINIFE_OK;
+    }
     if (c->mode != MINIFE_MODE_MULTI) return MINIFE_OK;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -535,7 +742,12 @@ extern "C" int minife_create(int nx, int ny, int nz, int ngpu, minife_ctx **out)
             for (int q = 0; q < ngpu; ++q) c->parts[q].comm = comms[q];
         }
     }
-    if (st == MINIFE_OK && ngpu > 1 && enable_peers(c)) st = setup_push(c);
+    // peer access between every device pair: halo push over NVLink and device-initiated
+    // reductions (comm regions addressed through peer pointers); otherwise NCCL throughout
+    if (st == MINIFE_OK && ngpu > 1 && enable_peers(c)) {
+        st = setup_push(c);
+        if (st == MINIFE_OK) st = setup_devcomm_local(c);
+    }
     if (st != MINIFE_OK) {
         minife_destroy(c);
         return st;
@@ -555,6 +767,7 @@ extern "C" int minife_create_virtual(int nx, int ny, int nz, int nparts, minife_
     std::vector<int> devs(nparts, 0);
     int st = create_common(c, nx, ny, nz, nparts, devs, -1);
     if (st == MINIFE_OK && nparts > 1) st = setup_push(c);
+    if (st == MINIFE_OK && nparts > 1) st = setup_devcomm_local(c);
     if (st != MINIFE_OK) {
         minife_destroy(c);
         return st;
@@ -599,6 +812,7 @@ extern "C" int minife_create_rank(int nx, int ny, int nz, int rank, int world, i
             st = MINIFE_ENCCL;
         }
     }
+    if (st == MINIFE_OK) st = setup_devcomm_ipc(c);
     if (st != MINIFE_OK) {
         minife_destroy(c);
         return st;
@@ -610,6 +824,8 @@ extern "C" int minife_create_rank(int nx, int ny, int nz, int rank, int world, i
 static void drop_graph(minife_ctx *c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     c->gexec = nullptr;
+    for (auto ex : c->gexec_parts) cudaGraphExecDestroy(ex);
+    c->gexec_parts.clear();
     c->g_iters = -1;
 }
 
@@ -649,6 +865,8 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"spmv_impl", &c->opt.spmv_impl, -1, 1},
         {"x_late", &c->opt.x_late, 0, 1},
         {"cluster_dd", &c->opt.cluster_dd, 0, 1},
+        {"device_comm", &c->opt.device_comm, -1, 1},
+        {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
     };
     for (auto &t : table) {
         if (strcmp(t.name, name) != 0) continue;
@@ -668,7 +886,7 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
 
 extern "C" int minife_set_transport(minife_ctx *c, int transport) {
     if (!c || (transport != MINIFE_TRANSPORT_DIRECT && transport != MINIFE_TRANSPORT_WIRE &&
-               transport != MINIFE_TRANSPORT_PUSH))
+               transport != MINIFE_TRANSPORT_PUSH && transport != MINIFE_TRANSPORT_DEVICE))
         return MINIFE_EINVAL;
     if (c->mode != MINIFE_MODE_VIRTUAL) return MINIFE_ESTATE;
     if (transport != c->transport) {
@@ -712,6 +930,7 @@ extern "C" const char *minife_strerror(int s) {
     case MINIFE_ENOTSPD: return "matrix not SPD (pAp <= 0 with rr != 0)";
     case MINIFE_EDIVERGED: return "CG diverged (non-finite value)";
     case MINIFE_ENODEV: return "no (or not enough) CUDA devices";
+    case MINIFE_ECOMM: return "device-initiated comm: a peer did not signal in time";
     default: return "unknown status";
     }
 }
@@ -883,19 +1102,16 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // waits are placed by the caller after K7 (wait_now = false).
 static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now) {
     for (auto &p : c->parts) {
+        const int64_t n = (int64_t)p.plan.send_idx.size();
+        if (!n) continue;
         DevGuard g(p.dev);
-        UpdArgs a{};
-        a.p = p.d_p;
-        a.r = p.d_r;
-        a.rr = p.d_rr;
-        a.st = p.d_st;
-        a.acc_in = p.acc_rr();
-        LAUNCH(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr,
-                                p.d_push_dst, p.d_push_ptr, (int64_t)p.plan.send_idx.size(),
-                                launch_stream(c, p)));
-        if (c->mode == MINIFE_MODE_MULTI) CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
+        UpdArgs a = upd_args(c, p, 1);           // acc_in = rr_k (mode 1), p, r, rr, st, dc
+        LAUNCH(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr, p.d_push_dst,
+                              p.d_push_ptr, n, launch_stream(c, p)));
+        if (c->mode == MINIFE_MODE_MULTI && !devcomm(c))
+            CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
     }
-    if (wait_now) return push_wait(c);
+    if (wait_now) return push_wait(c, mode == 1 ? k + 1 : (k > 0 ? k : 1));
     return MINIFE_OK;
 }
 
@@ -981,7 +1197,15 @@ static int enqueue_halo(minife_ctx *c, VecOf vec, bool comm = false, bool prepac
 }
 
 // int64 SUM of the exact accumulators over all ranks (which = 0: pAp, 1: rr)
-static int enqueue_allreduce(minife_ctx *c, int which) {
+static int enqueue_allreduce(minife_ctx *c, int which, int k) {
+    if (devcomm(c)) {           // every part stores its words into every rank's inbox
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            LAUNCH(c, launch_acc_push(upd_args(c, p, 0), k, which,
+                                      which ? p.acc_rr() : p.acc_pAp(), launch_stream(c, p)));
+        }
+        return MINIFE_OK;
+    }
     if (c->world == 1) return MINIFE_OK;
     if (c->mode == MINIFE_MODE_VIRTUAL) {
         std::vector<unsigned long long *> accs;
@@ -1016,6 +1240,15 @@ static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
     a.st = p.d_st;
     a.x_late = c->opt.x_late;
     a.cl_dd = c->opt.cluster_dd;
+    if (devcomm(c)) {
+        a.dc.region = p.d_comm_ptrs;
+        a.dc.local = p.d_comm;
+        a.dc.nbr_rank = p.d_nbr_rank;
+        a.dc.n_nbr = (int)p.plan.nbr.size();
+        a.dc.rank = p.plan.rank;
+        a.dc.world = c->world;
+        a.dc.timeout_ns = (long long)c->opt.comm_timeout_ms * 1000000ll;
+    }
     if (which_in == 0) {          // K6: in = pAp, out = rr
         a.acc_in = p.acc_pAp();
         a.acc_out = p.acc_rr();
@@ -1089,12 +1322,13 @@ static bool overlap_sym(const minife_ctx *c) {
 static int enqueue_k7_with_halo(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
     if (push_mode(c)) {                  // device-initiated: p_(k+1) halo stored by the sender
-        TRY(enqueue_push(c, k, 1, false));
+        const bool last = k == c->cur_max_iters;     // no SpMV(k+1) reads it
+        if (!last) TRY(enqueue_push(c, k, 1, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
             LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
         }
-        return push_wait(c);
+        return last ? MINIFE_OK : push_wait(c, k + 1);
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1148,7 +1382,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
         a.acc_out = p.acc_rr();
         LAUNCH(c, launch_init_vectors(a, p.grid_upd, s));
     }
-    TRY(enqueue_allreduce(c, 1));
+    TRY(enqueue_allreduce(c, 1, 0));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 0);
@@ -1221,14 +1455,14 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         if (!t) TRY(tw_mark(c, k, true));
     }
     if (t) t->mark(0);
-    TRY(enqueue_allreduce(c, 0));
+    TRY(enqueue_allreduce(c, 0, k));
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         LAUNCH(c, launch_update_xr(upd_args(c, p, 0), k, p.grid_upd, launch_stream(c, p)));
     }
     if (t) t->mark(1);
-    TRY(enqueue_allreduce(c, 1));
+    TRY(enqueue_allreduce(c, 1, k));
     if (t) t->mark(3);
     if (osym) {
         TRY(enqueue_k7_with_halo(c, k));
@@ -1366,14 +1600,14 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
                                 launch_stream(c, p)));
     }
     TRY(tw_mark(c, k, true));
-    TRY(enqueue_allreduce(c, 0));
+    TRY(enqueue_allreduce(c, 0, k));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs u6 = upd_args(c, p, 0);
         u6.alpha_hist = p.d_alpha;
         LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
     }
-    TRY(enqueue_allreduce(c, 1));
+    TRY(enqueue_allreduce(c, 1, k));
     if (halo) {
         // as enqueue_k7_with_halo: the send slots' p_(k+1) ahead of K7, exchanged on the
         // transport stream into the halo of the buffer p_(k+1) goes to, while K7 runs
@@ -1417,6 +1651,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
 
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
     if (!t) c->tw_armed = false;
+    c->cur_max_iters = max_iters;
     if (!t && x2_mode(c) && !small_mode(c)) {
         TRY(enqueue_init(c, tol));
         if (c->parts.size() > 1 || c->world > 1)      // halo of p_1 = b (buffer of odd k)
@@ -1487,7 +1722,10 @@ static int read_result(minife_ctx *c, int max_iters, minife_cg_result *res, doub
     c->solved = true;
     const int status = st.status == 6 ? MINIFE_ENOTSPD
                        : st.status == 7 ? MINIFE_EDIVERGED
+                       : st.status == 9 ? MINIFE_ECOMM
                                         : MINIFE_OK;
+    if (status == MINIFE_ECOMM)
+        set_err(c, "device comm: a peer did not signal within %d ms", c->opt.comm_timeout_ms);
     if (res) {
         res->status = status;
         res->iterations = st.iters;
@@ -1519,44 +1757,98 @@ static int check_solve_args(minife_ctx *c, int max_iters, double tol) {
     return ensure_fused_buffers(c);
 }
 
+// Wait for the end of an enqueued solve.  With NCCL comms, poll ncclCommGetAsyncError while
+// waiting: a failed or dead peer surfaces as MINIFE_ENCCL (communicators aborted) instead of a
+// hang.
+static int wait_solve(minife_ctx *c, cudaEvent_t done) {
+    bool any_comm = false;
+    for (auto &p : c->parts) any_comm |= p.comm != nullptr;
+    if (!any_comm || !nccl()->CommGetAsyncError) {
+        CUDA_TRY(c, cudaEventSynchronize(done));
+        return MINIFE_OK;
+    }
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(done);
+        if (q == cudaSuccess) return MINIFE_OK;
+        if (q != cudaErrorNotReady) CUDA_TRY(c, q);
+        for (auto &p : c->parts) {
+            if (!p.comm) continue;
+            ncclResult_t ae = ncclSuccess;
+            if (nccl()->CommGetAsyncError(p.comm, &ae) != ncclSuccess || ae != ncclSuccess) {
+                set_err(c, "NCCL asynchronous error: %s", nccl()->GetErrorString(ae));
+                for (auto &q2 : c->parts)
+                    if (q2.comm) {
+                        nccl()->CommAbort(q2.comm);
+                        q2.comm = nullptr;
+                    }
+                return MINIFE_ENCCL;
+            }
+        }
+        struct timespec ts = {0, 50000};
+        nanosleep(&ts, nullptr);
+    }
+}
+
 extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_cg_result *res) {
     TRY(check_solve_args(c, max_iters, tol));
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
     DevGuard g(p0.dev);
-    // option "graph" = 0: enqueue every solve directly instead of replaying a captured graph
-    // (an escape hatch for environments where capturing the NCCL calls of RANK ctxs fails)
-    bool eager = c->mode == MINIFE_MODE_MULTI || !c->opt.graph || c->eager;
-    if (!eager && (!c->gexec || c->g_iters != max_iters || c->g_tol != tol)) {
+    // MULTI with device comm: one graph per device (no cross-device dependency other than the
+    // in-kernel flags); MULTI with NCCL reductions: enqueued directly.  Option "graph" = 0:
+    // enqueue every solve directly (an escape hatch should capturing NCCL calls fail).
+    const bool per_part = c->mode == MINIFE_MODE_MULTI && devcomm(c);
+    bool eager = (c->mode == MINIFE_MODE_MULTI && !per_part) || !c->opt.graph || c->eager;
+    const bool have = per_part ? !c->gexec_parts.empty() : c->gexec != nullptr;
+    if (!eager && (!have || c->g_iters != max_iters || c->g_tol != tol)) {
         drop_graph(c);
-        // capture on the ctx's own stream (a torch stream may be the legacy default one)
-        cudaStream_t cap = p0.stream;
+        // capture on the ctx's own streams (a torch stream may be the legacy default one)
         cudaStream_t saved = c->user_stream;
         c->user_stream = nullptr;
-        CUDA_TRY(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        std::vector<cudaStream_t> caps;
+        if (per_part)
+            for (auto &p : c->parts) caps.push_back(p.stream);
+        else
+            caps.push_back(p0.stream);
+        cudaError_t e = cudaSuccess;
+        size_t begun = 0;
+        for (size_t i = 0; i < caps.size() && e == cudaSuccess; ++i) {
+            DevGuard gg(per_part ? c->parts[i].dev : p0.dev);
+            e = cudaStreamBeginCapture(caps[i], cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) ++begun;
+        }
         const int64_t k0 = c->enq_kernels;
-        int st = enqueue_solve(c, max_iters, tol, nullptr);
+        int st = e == cudaSuccess ? enqueue_solve(c, max_iters, tol, nullptr) : MINIFE_OK;
         const int64_t captured = c->enq_kernels - k0;
         c->enq_kernels = k0;
-        cudaGraph_t graph = nullptr;
-        cudaError_t e = cudaStreamEndCapture(cap, &graph);
-        c->user_stream = saved;
-        if (st == MINIFE_OK && e == cudaSuccess) {
-            e = cudaGraphInstantiate(&c->gexec, graph, 0);
-            if (e != cudaSuccess) c->gexec = nullptr;
+        std::vector<cudaGraphExec_t> execs;
+        for (size_t i = 0; i < begun; ++i) {
+            DevGuard gg(per_part ? c->parts[i].dev : p0.dev);
+            cudaGraph_t graph = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(caps[i], &graph);
+            if (e == cudaSuccess) e = e2;
+            cudaGraphExec_t ex = nullptr;
+            if (st == MINIFE_OK && e == cudaSuccess) {
+                e = cudaGraphInstantiate(&ex, graph, 0);
+                if (e == cudaSuccess) execs.push_back(ex);
+            }
+            if (graph) cudaGraphDestroy(graph);
         }
-        if (graph) cudaGraphDestroy(graph);
-        if (st != MINIFE_OK || e != cudaSuccess) {
+        c->user_stream = saved;
+        if (st != MINIFE_OK || e != cudaSuccess || execs.size() != caps.size()) {
+            for (auto ex : execs) cudaGraphExecDestroy(ex);
             // a multi-rank job whose capture failed (every rank takes the same path) runs
             // this and later solves directly; anything else is an error
-            if (c->world > 1 && c->mode == MINIFE_MODE_RANK) {
+            if (c->world > 1 && (c->mode == MINIFE_MODE_RANK || per_part)) {
                 cudaGetLastError();
                 c->eager = eager = true;
             } else {
                 if (st != MINIFE_OK) return st;
-                CUDA_TRY(c, e);
+                CUDA_TRY(c, e != cudaSuccess ? e : cudaErrorUnknown);
             }
         } else {
+            if (per_part) c->gexec_parts = execs;
+            else c->gexec = execs[0];
             c->g_iters = max_iters;
             c->g_tol = tol;
             c->g_kernels = captured;
@@ -1567,18 +1859,26 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         CUDA_TRY(c, cudaEventRecord(c->ev0, launch_stream(c, p0)));
         TRY(enqueue_solve(c, max_iters, tol, nullptr));
         CUDA_TRY(c, cudaEventRecord(c->ev1, launch_stream(c, p0)));
-        for (auto &p : c->parts) {
-            DevGuard gg(p.dev);
-            CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+    } else if (per_part) {
+        CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
+        for (size_t i = 0; i < c->parts.size(); ++i) {
+            DevGuard gg(c->parts[i].dev);
+            CUDA_TRY(c, cudaGraphLaunch(c->gexec_parts[i], c->parts[i].stream));
         }
+        CUDA_TRY(c, cudaEventRecord(c->ev1, p0.stream));
+        c->kernel_launches += c->g_kernels;
     } else {
         cudaStream_t s = launch_stream(c, p0);
         CUDA_TRY(c, cudaEventRecord(c->ev0, s));
         CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
-        c->kernel_launches += c->g_kernels;
         CUDA_TRY(c, cudaEventRecord(c->ev1, s));
+        c->kernel_launches += c->g_kernels;
     }
-    CUDA_TRY(c, cudaEventSynchronize(c->ev1));
+    TRY(wait_solve(c, c->ev1));
+    for (auto &p : c->parts) {
+        DevGuard gg(p.dev);
+        CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+    }
     float ms = 0.f;
     CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     return read_result(c, max_iters, res, ms * 1e-3);

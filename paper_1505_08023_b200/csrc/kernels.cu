@@ -1094,11 +1094,124 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 // CG init (C6 step 1): x = 0, r = b, p = b, rr = dot(r, r)
 // ----------------------------------------------------------------------------------------
 
+// ----------------------------------------------------------------------------------------
+// Device-initiated communication (DevComm, kernels.h): release/acquire flags at
+// system scope, payloads stored straight into the receiver's region.
+// ----------------------------------------------------------------------------------------
+
+static_assert(ACC_WORDS == 72, "comm_words() assumes 72-word accumulators");
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long comm_gen(const DevComm &dc) {
+    return *(volatile const unsigned long long *)dc.local;
+}
+
+// Spin until *flag >= seq.  A peer that never signals (dead rank, broken mapping) ends the
+// wait after dc.timeout_ns: the error is recorded in the region and in the CG state (status 9
+// -> MINIFE_ECOMM), and every later kernel of the solve returns at its done test.
+__device__ bool comm_spin(const DevComm &dc, const unsigned long long *flag,
+                          unsigned long long seq, CgState *st) {
+    if (ld_acquire_sys(flag) >= seq) return true;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flag) < seq) {
+        if (*(volatile const unsigned long long *)(dc.local + 2)) return false;
+        __nanosleep(100);
+        if (global_ns() - t0 > (unsigned long long)dc.timeout_ns) {
+            atomicExch(dc.local + 2, 1ull);
+            st->status = 9;
+            st->done = 1;
+            __threadfence();
+            return false;
+        }
+    }
+    return true;
+}
+
+// The all-reduced accumulator `which` (0 pAp_k, 1 rr_k) into shared memory: the local words
+// (one part, or all-reduced by the host-launched transport) or, with device comm, the int64
+// sum over every rank's inbox slot (two's-complement sums: the same value an int64-SUM
+// all-reduce produces, independent of the rank order).  Block-uniform; false on a timeout.
+__device__ bool acc_in_load(unsigned long long *s_in, const UpdArgs &a, int k, int which) {
+    const DevComm &dc = a.dc;
+    if (!dc.local) {
+        acc_load_shared(s_in, a.acc_in);
+        return true;
+    }
+    __shared__ int s_ok;
+    const unsigned long long gen = comm_gen(dc);
+    const int gp = (int)(gen & 1);
+    const unsigned long long seq = comm_seq(gen, k, which);
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
+        if (!comm_spin(dc, dc.local + comm_acc_flag(dc.world, gp, which, t), seq, a.st)) s_ok = 0;
+    __syncthreads();
+    if (!s_ok) return false;
+    const unsigned long long *in =
+        dc.local + comm_inbox(dc.world) + (int64_t)(2 * gp + which) * dc.world * ACC_WORDS;
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
+        unsigned long long sum = 0ull;
+        for (int t = 0; t < dc.world; ++t) sum += __ldcv(in + (int64_t)t * ACC_WORDS + i);
+        s_in[i] = sum;
+    }
+    return true;
+}
+
+// Reduction `which` of iteration k: this part's accumulator into slot `rank` of every rank's
+// inbox (its own included), then one release flag per rank.  Slot reuse is safe with two
+// generation parities x {pAp, rr}: a rank writes reduction n+2 only after it has consumed
+// n+1, which needs every rank's contribution to n+1, which each rank stores only after it has
+// consumed n (stream order); a new solve (next generation) uses the other parity.
+__global__ void k_acc_push(UpdArgs a, int k, int which, const unsigned long long *acc) {
+    if (k > 0 && a.st->done) return;     // k = 0 (rr_0): the state is not initialised yet
+    const DevComm &dc = a.dc;
+    const unsigned long long gen = comm_gen(dc);
+    const int gp = (int)(gen & 1);
+    const int64_t off =
+        comm_inbox(dc.world) + ((int64_t)(2 * gp + which) * dc.world + dc.rank) * ACC_WORDS;
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
+        const unsigned long long w = __ldcg(acc + i);
+        for (int t = 0; t < dc.world; ++t) dc.region[t][off + i] = w;
+    }
+    __threadfence_system();
+    __syncthreads();
+    const unsigned long long seq = comm_seq(gen, k, which);
+    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
+        st_release_sys(dc.region[t] + comm_acc_flag(dc.world, gp, which, dc.rank), seq);
+}
+
+// Before SpMV(k): every neighbor's halo values of p_k have landed (k_push signalled).
+__global__ void k_halo_wait(UpdArgs a, int k) {
+    if (a.st->done) return;
+    const DevComm &dc = a.dc;
+    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k);
+    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
+        comm_spin(dc, dc.local + comm_halo_flag(dc.world, dc.nbr_rank[t]), seq, a.st);
+}
+
 template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     __shared__ unsigned long long sacc[ACC_WORDS];
     __shared__ int sdig[ACC_DIG16];
     acc_zero_shared(sacc, sdig);
+    // device comm: a new solve generation (every later kernel of the solve reads it)
+    if (a.dc.local && blockIdx.x == 0 && threadIdx.x == 0) {
+        a.dc.local[0] += 1ull;
+        a.dc.local[1] = 0ull;
+        a.dc.local[2] = 0ull;
+    }
     __syncthreads();
     Expansion ex;
     ex.init();
@@ -1136,7 +1249,9 @@ __device__ __forceinline__ void cg_state_init(const UpdArgs &a, double rr0, doub
 
 __global__ void k_init_finalize(UpdArgs a, double tol) {
     __shared__ unsigned long long s_in[ACC_WORDS];
-    acc_load_shared(s_in, a.acc_out);
+    UpdArgs ai = a;
+    ai.acc_in = a.acc_out;
+    if (!acc_in_load(s_in, ai, 0, 1)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) cg_state_init(a, fin, tol);
@@ -1236,7 +1351,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     __shared__ int s_stop;
     if (a.st->done) return;
     acc_zero_shared(sacc, sdig);
-    acc_load_shared(s_in, a.acc_in);
+    if (!acc_in_load(s_in, a, k, 0)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
@@ -1774,7 +1889,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     __shared__ double s_beta, s_alpha;
     __shared__ int s_stop;
     if (a.st->done) return;              // K6 stopped (pAp test): no x update for this k
-    acc_load_shared(s_in, a.acc_in);
+    if (!acc_in_load(s_in, a, k, 1)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
@@ -1889,7 +2004,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
     __shared__ double s_beta;
     __shared__ int s_stop;
     if (a.st->done) return;              // K6 stopped: x_finish applies what is pending
-    acc_load_shared(s_in, a.acc_in);
+    if (!acc_in_load(s_in, a, k, 1)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
@@ -2016,7 +2131,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_pack_next_p(UpdArgs a, int k,
     __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta;
     if (a.st->done) return;
-    acc_load_shared(s_in, a.acc_in);
+    if (!acc_in_load(s_in, a, k, 1)) return;
     __syncthreads();
     if (threadIdx.x < 32) {
         const double rr_new = acc_finalize_warp(s_in);
@@ -2029,11 +2144,14 @@ __global__ void __launch_bounds__(UPD_THREADS) k_pack_next_p(UpdArgs a, int k,
         sendbuf[i] = __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, a.p[send_col[i]]));
 }
 
-// a1, device-initiated (MINIFE_TRANSPORT_PUSH): every send slot's value is stored straight
-// into the receiving part's halo column -- another part's array on this GPU (VIRTUAL) or a
-// peer GPU's array over NVLink (MULTI, peer access).  No pack, no wire, no unpack.
+// a1, device-initiated (MINIFE_TRANSPORT_PUSH / device comm): every send slot's value is
+// stored straight into the receiving part's halo column -- another part's array on this GPU
+// (VIRTUAL), a peer GPU's array over NVLink (MULTI, peer access) or a CUDA-IPC mapping of
+// another rank's array (RANK).  No pack, no wire, no unpack.
 // mode 0: the value is p[send_col]; mode 1: p_(k+1) = fl(r + fl(beta_k p)) as k_pack_next_p.
-__global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode,
+// With device comm (a.dc.local) the last CTA to finish raises each neighbor's halo flag for
+// iteration k_halo (release, after every CTA's stores are fenced at system scope).
+__global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode, int k_halo,
                                                       const int32_t *send_row,
                                                       const int32_t *send_col,
                                                       const uint8_t *slot_nbr,
@@ -2041,9 +2159,10 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode
                                                       double *const *dst_ptr, int64_t n) {
     __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta;
+    __shared__ int s_last;
     if (mode == 1) {
         if (a.st->done) return;
-        acc_load_shared(s_in, a.acc_in);
+        if (!acc_in_load(s_in, a, k, 1)) return;
         __syncthreads();
         if (threadIdx.x < 32) {
             const double rr_new = acc_finalize_warp(s_in);
@@ -2058,6 +2177,20 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode
         const double v = mode == 1 ? __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, pv)) : pv;
         dst_ptr[slot_nbr[i]][dst_col[i]] = v;
     }
+    const DevComm &dc = a.dc;
+    if (!dc.local) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_last = atomicAdd(reinterpret_cast<unsigned long long *>(dc.local + 1), 1ull) ==
+                 (unsigned long long)(gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence_system();
+    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k_halo);
+    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
+        st_release_sys(dc.region[dc.nbr_rank[t]] + comm_halo_flag(dc.world, dc.rank), seq);
+    if (threadIdx.x == 0) dc.local[1] = 0ull;       // ticket for the next launch
 }
 
 // ----------------------------------------------------------------------------------------
@@ -2074,7 +2207,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_r(UpdArgs a, int k,
     __shared__ int s_stop;
     if (a.st->done) return;
     acc_zero_shared(sacc, sdig);
-    acc_load_shared(s_in, a.acc_in);
+    if (!acc_in_load(s_in, a, k, 0)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
@@ -2716,8 +2849,22 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
                         double *const *dst_ptr, int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
-    k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, send_row, send_col, slot_nbr, dst_col, dst_ptr,
-                                     n);
+    const int k_halo = mode == 1 ? k + 1 : (k > 0 ? k : 1);
+    k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, k_halo, send_row, send_col, slot_nbr, dst_col,
+                                     dst_ptr, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_acc_push(const UpdArgs &a, int k, int which, const unsigned long long *acc,
+                            cudaStream_t s) {
+    if (!a.dc.local) return cudaErrorInvalidValue;
+    k_acc_push<<<1, 128, 0, s>>>(a, k, which, acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_wait(const UpdArgs &a, int k, cudaStream_t s) {
+    if (!a.dc.local) return cudaErrorInvalidValue;
+    k_halo_wait<<<1, 32, 0, s>>>(a, k);
     return cudaGetLastError();
 }
 

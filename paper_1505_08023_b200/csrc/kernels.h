@@ -106,6 +106,46 @@ struct SpmvArgs {
     CgState *stw;                       // writable state (decisions)
 };
 
+// Device-initiated communication between parts/ranks:
+// every part owns one COMM REGION in its device memory; the other parts store into it
+// directly (same device: VIRTUAL; peer access over NVLink: MULTI; CUDA-IPC mappings: RANK)
+// and raise release flags; the owner waits with acquire loads.  No host-launched collective
+// remains in the CG iteration.  Region layout (64-bit words, W = world):
+//   [0] solve generation (bumped by k_init_vectors), [1] k_push CTA ticket, [2] error flag
+//   [COMM_HDR + (4 gp + 2 .. ) ...] acc flags [gen parity 2][which 2][sender W]
+//   [COMM_HDR + 4W + sender]       halo flags
+//   [comm_inbox(W) + ((2 gp + which) W + sender) ACC_WORDS + i]  accumulator inbox
+// A flag holds seq = gen * 2^21 + (2k + which) (acc) or gen * 2^21 + k (halo of p_k).
+constexpr int COMM_HDR = 8;
+__host__ __device__ constexpr int64_t comm_acc_flag(int W, int gp, int which, int sender) {
+    return COMM_HDR + (int64_t)((2 * gp + which) * W + sender);
+}
+__host__ __device__ constexpr int64_t comm_halo_flag(int W, int sender) {
+    return COMM_HDR + 4 * (int64_t)W + sender;
+}
+__host__ __device__ constexpr int64_t comm_inbox(int W) {
+    return ((COMM_HDR + 5 * (int64_t)W) + 15) / 16 * 16;
+}
+__host__ __device__ constexpr int64_t comm_words(int W) {
+    return comm_inbox(W) + 4 * (int64_t)W * 72;
+}
+__host__ __device__ constexpr unsigned long long comm_seq(unsigned long long gen, int k, int which) {
+    return (gen << 21) + 2ull * (unsigned)k + (unsigned)which;
+}
+__host__ __device__ constexpr unsigned long long comm_halo_seq(unsigned long long gen, int k) {
+    return (gen << 21) + (unsigned)k;
+}
+
+struct DevComm {
+    unsigned long long *const *region;  // [world] regions as seen from this device (own incl.)
+    unsigned long long *local;          // this part's region; null: accumulators all-reduced
+                                        // by the host-launched transport instead
+    const int32_t *nbr_rank;            // [n_nbr] neighbor ranks (halo signals / waits)
+    int n_nbr;
+    int rank, world;
+    long long timeout_ns;               // spin limit; exceeded -> CgState.status = 9 (ECOMM)
+};
+
 struct UpdArgs {
     Geom g;
     double *x, *r;                      // [rows]
@@ -123,6 +163,7 @@ struct UpdArgs {
     const double *ring[8];
     int xdef;
     int x_late;                         // K7 applies x += alpha p (1, default) or K6 does (0)
+    DevComm dc;                         // device-initiated reductions / halo (dc.local != null)
     int cl_dd;                          // cluster solver: DSMEM digit pushes (1, default)
 };
 constexpr int XDEF_MAX = 8;
@@ -175,6 +216,13 @@ cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
 cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_row,
                         const int32_t *send_col, const uint8_t *slot_nbr, const int32_t *dst_col,
                         double *const *dst_ptr, int64_t n, cudaStream_t s);
+
+// Device-initiated comm (dc.local != null): store this part's accumulator `acc` (reduction
+// `which` of iteration k: 0 pAp_k, 1 rr_k) into every rank's inbox and raise the flags.
+cudaError_t launch_acc_push(const UpdArgs &a, int k, int which, const unsigned long long *acc,
+                            cudaStream_t s);
+// Wait until every neighbor has signalled the halo of p_k (k_push's signal), then return.
+cudaError_t launch_halo_wait(const UpdArgs &a, int k, cudaStream_t s);
 
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,

@@ -110,11 +110,13 @@ def test_elongated_meshes(n, fmt):
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((10, 10, 10), 4),
                                  ((12, 11, 10), 8), ((33, 32, 31), 5), ((3, 2, 2), 4),
                                  ((1, 1, 12), 4), ((12, 1, 1), 3), ((40, 3, 2), 6)])
-@pytest.mark.parametrize("transport", [0, 1, 2])
+@pytest.mark.parametrize("transport", [0, 1, 2, 3])
 def test_virtual_ranks_bit_identical(n, p, fmt, transport):
     """P10 / S:394: any partition gives bitwise the 1-rank (= oracle) results.  transport 1
     runs the multi-GPU wire protocol (pack -> per-neighbor receive blocks -> unpack), 2 the
-    device-initiated push (each sender stores into the receivers' halo columns)."""
+    device-initiated push (each sender stores into the receivers' halo columns), 3 the whole
+    device-initiated protocol of MULTI/RANK ctxs (push + halo flags + in-kernel reductions
+    through every part's inbox, no host-launched collective)."""
     s = oracle_system(n)
     with M.Minife(*n, virtual=p, fmt=fmt) as g:
         g.set_transport(transport)
@@ -128,7 +130,7 @@ def test_virtual_ranks_bit_identical(n, p, fmt, transport):
 
 @pytest.mark.parametrize("fmt", [M.FMT_SEG, M.FMT_SYM])
 @pytest.mark.parametrize("n,p", [((40, 8, 6), 2), ((12, 40, 9), 4), ((33, 32, 31), 8)])
-@pytest.mark.parametrize("transport", [0, 1, 2])
+@pytest.mark.parametrize("transport", [0, 1, 2, 3])
 def test_overlapped_halo_split_bit_identical(n, p, transport, fmt):
     """SEG parts store interior slices first; the interior SpMV runs while the halo
     is in flight on a second stream, the boundary slices after it lands.  SYM parts compute
@@ -268,6 +270,39 @@ def test_rank_mode_world1_nccl_path(fmt):
         g.assemble()
         check_matrix(g, oracle_system(n))
         check_cg(g, n, 200, 0.0)
+
+
+@pytest.mark.parametrize("graph", [1, 0])
+@pytest.mark.parametrize("n", [(10, 10, 10), (23, 17, 9)])
+def test_rank_mode_world1_device_comm(n, graph):
+    """RANK ctx built through the CUDA-IPC exchange (NCCL all-gather of the handles, transport
+    agreement) with the device-initiated reductions forced at world 1: every dot goes through
+    k_acc_push -> inbox -> flag-waiting consumers.  Bitwise the oracle, graph and eager."""
+    uid = M.nccl_unique_id()
+    with M.Minife(*n, rank=(0, 1, 0, uid), options={"device_comm": 1, "graph": graph,
+                                                    "small_solver": 0}) as g:
+        g.assemble()
+        check_cg(g, n, 200, 0.0)
+        check_cg(g, n, 100, 1e-10)
+        info = g.get_info()
+        assert info.kernel_launches > 0
+
+
+def test_device_comm_launch_count_has_no_host_collective():
+    """VIRTUAL parts on the device protocol: every kernel of the solve is ours (the count the
+    library reports equals the kernels it enqueued) and the solve is bitwise the oracle."""
+    n, p = (12, 11, 10), 4
+    with M.Minife(*n, virtual=p) as g:
+        g.set_transport(M.TRANSPORT_DEVICE)
+        g.assemble()
+        before = g.get_info().kernel_launches
+        check_cg(g, n, 50, 0.0)
+        launched = g.get_info().kernel_launches - before
+        # per part: init_vectors, acc_push, init_finalize, push + wait (p_1); per iteration:
+        # SpMV, acc_push, K6, acc_push, push, K7, halo wait (none after the last K7)
+        parts = [g.part_info(q) for q in range(p)]
+        assert all(q.n_neighbors > 0 for q in parts)
+        assert launched == p * (5 + 7 * 50 - 2)
 
 
 def test_errors_and_states():
