@@ -284,6 +284,11 @@ int minife_spmv_device(minife_ctx *ctx, const double *d_x, double *d_y, void *st
 /* ---- getters --------------------------------------------------------------------------- */
 
 int minife_get_info(const minife_ctx *ctx, minife_info *out);
+
+/* Device time (CUDA events on every part's queue, max over the ctx's parts, milliseconds) of
+ * the last minife_assemble (0 for MINIFE_FMT_CRS, whose sizing pass syncs with the host) and
+ * of the last minife_cg_solve.  Errors: MINIFE_EINVAL (NULL). */
+int minife_get_timings(const minife_ctx *ctx, double *assemble_ms, double *solve_ms);
 int minife_get_part_info(const minife_ctx *ctx, int part, minife_part_info *out);
 
 /* Canonical global CSR of the assembled system (rows in global id order, columns ascending,

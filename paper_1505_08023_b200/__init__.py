@@ -113,6 +113,7 @@ SIGNATURES = {
     "minife_spmv": (_I, [_P, _P, _P]),
     "minife_spmv_device": (_I, [_P, _P, _P, _P]),
     "minife_get_info": (_I, [_P, ctypes.POINTER(minife_info)]),
+    "minife_get_timings": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_get_part_info": (_I, [_P, _I, ctypes.POINTER(minife_part_info)]),
     "minife_export_csr": (_I, [_P, _P, _P, _P]),
     "minife_export_rows": (_I, [_P, _I64, _P, _P, _P, _P]),
@@ -272,6 +273,13 @@ class Minife:
         out = minife_info()
         self._check(minife_get_info(self.h, ctypes.byref(out)), "minife_get_info")
         return out
+
+    def timings(self):
+        """(assemble ms, solve ms) of the last calls: device time, max over the ctx's parts."""
+        a, s = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        self._check(minife_get_timings(self.h, ctypes.byref(a), ctypes.byref(s)),
+                    "minife_get_timings")
+        return a.value, s.value
 
     def part_info(self, part: int) -> minife_part_info:
         out = minife_part_info()

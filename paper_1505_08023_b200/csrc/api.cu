@@ -133,6 +133,7 @@ struct Part {
     cudaStream_t stream = nullptr;
     cudaStream_t cstream = nullptr;               // halo transport, overlapped with the SpMV
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;    // per-part timing of assemble / solve
     int grid_spmv = 1, grid_upd = 1;
     size_t bytes = 0, matrix_bytes = 0;
     unsigned long long *acc_pAp(int par = 0) const { return d_acc + (2 * (par & 1)) * ACC_WORDS; }
@@ -195,6 +196,7 @@ struct minife_ctx {
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
     int cur_max_iters = 0;                       // max_iters of the solve being enqueued
+    double last_asm_ms = 0.0, last_solve_ms = 0.0;   // device time, max over the parts
     std::vector<cudaGraphExec_t> gexec_parts;    // MULTI + device comm: one graph per device
     // kernel launch accounting: enq_kernels counts launch_* calls as they are enqueued (into a
     // capture or directly); g_kernels = kernels in the captured solve graph; kernel_launches =
@@ -312,6 +314,8 @@ static void free_part(Part &p) {
     if (p.comm) nccl()->CommDestroy(p.comm);
     if (p.ev_push) cudaEventDestroy(p.ev_push);
     if (p.ev_fork) cudaEventDestroy(p.ev_fork);
+    if (p.ev_t0) cudaEventDestroy(p.ev_t0);
+    if (p.ev_t1) cudaEventDestroy(p.ev_t1);
     if (p.ev_join) cudaEventDestroy(p.ev_join);
     if (p.cstream) cudaStreamDestroy(p.cstream);
     if (p.stream) cudaStreamDestroy(p.stream);
@@ -366,6 +370,8 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     p.nnz = plan.local_nnz();
     p.nns = plan.local_nns();
     CUDA_TRY(c, cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreate(&p.ev_t0));
+    CUDA_TRY(c, cudaEventCreate(&p.ev_t1));
     TRY(dalloc(c, p, &p.d_slice_off, p.nslices + 1));
     TRY(dalloc(c, p, &p.d_row_len, p.nslices * 32));
     TRY(dalloc(c, p, &p.d_width, p.nslices));
@@ -670,6 +676,30 @@ static int push_wait(minife_ctx *c, int k) {
         DevGuard g(p.dev);
         for (int q : p.plan.nbr) CUDA_TRY(c, cudaStreamWaitEvent(p.stream, c->parts[q].ev_push, 0));
     }
+    return MINIFE_OK;
+}
+
+// Device time of an operation enqueued on every part: events on each part's queue before
+// and after; the duration is the max over the parts (CUDA events, not host clocks).
+// (assembly runs on every part's own queue, the solve on launch_stream)
+static int mark_parts(minife_ctx *c, bool end, bool assembly = false) {
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        cudaStream_t s = assembly ? stream_of(c, p) : launch_stream(c, p);
+        CUDA_TRY(c, cudaEventRecord(end ? p.ev_t1 : p.ev_t0, s));
+    }
+    return MINIFE_OK;
+}
+static int elapsed_parts(minife_ctx *c, double *ms_out) {
+    double mx = 0.0;
+    for (auto &p : c->parts) {
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaEventSynchronize(p.ev_t1));
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, p.ev_t0, p.ev_t1));
+        mx = std::max(mx, (double)ms);
+    }
+    *ms_out = mx;
     return MINIFE_OK;
 }
 
@@ -1030,6 +1060,9 @@ static Matrix matrix_of(const minife_ctx *c, const Part &p) {
 
 extern "C" int minife_assemble(minife_ctx *c) {
     if (!c) return MINIFE_EINVAL;
+    // CRS sizes its arrays from a device pass read back to the host: its time is host-split
+    const bool timed = c->fmt != MINIFE_FMT_CRS;
+    if (timed) TRY(mark_parts(c, false, true));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         cudaStream_t s = stream_of(c, p);
@@ -1084,10 +1117,13 @@ extern "C" int minife_assemble(minife_ctx *c) {
         LAUNCH(c, launch_assemble(a, s));
         p.grid_spmv = spmv_grid(p.nslices, c->fmt);
     }
+    if (timed) TRY(mark_parts(c, true, true));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         CUDA_TRY(c, cudaStreamSynchronize(stream_of(c, p)));
     }
+    c->last_asm_ms = 0.0;
+    if (timed) TRY(elapsed_parts(c, &c->last_asm_ms));
     c->assembled = true;
     c->solved = false;
     return MINIFE_OK;
@@ -1854,34 +1890,27 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
             c->g_kernels = captured;
         }
     }
+    TRY(mark_parts(c, false));
     if (eager) {
         // one host thread drives every device: launch the sequence directly
-        CUDA_TRY(c, cudaEventRecord(c->ev0, launch_stream(c, p0)));
         TRY(enqueue_solve(c, max_iters, tol, nullptr));
-        CUDA_TRY(c, cudaEventRecord(c->ev1, launch_stream(c, p0)));
     } else if (per_part) {
-        CUDA_TRY(c, cudaEventRecord(c->ev0, p0.stream));
         for (size_t i = 0; i < c->parts.size(); ++i) {
             DevGuard gg(c->parts[i].dev);
             CUDA_TRY(c, cudaGraphLaunch(c->gexec_parts[i], c->parts[i].stream));
         }
-        CUDA_TRY(c, cudaEventRecord(c->ev1, p0.stream));
         c->kernel_launches += c->g_kernels;
     } else {
-        cudaStream_t s = launch_stream(c, p0);
-        CUDA_TRY(c, cudaEventRecord(c->ev0, s));
-        CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
-        CUDA_TRY(c, cudaEventRecord(c->ev1, s));
+        CUDA_TRY(c, cudaGraphLaunch(c->gexec, launch_stream(c, p0)));
         c->kernel_launches += c->g_kernels;
     }
-    TRY(wait_solve(c, c->ev1));
+    TRY(mark_parts(c, true));
     for (auto &p : c->parts) {
         DevGuard gg(p.dev);
-        CUDA_TRY(c, cudaStreamSynchronize(launch_stream(c, p)));
+        TRY(wait_solve(c, p.ev_t1));
     }
-    float ms = 0.f;
-    CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    return read_result(c, max_iters, res, ms * 1e-3);
+    TRY(elapsed_parts(c, &c->last_solve_ms));
+    return read_result(c, max_iters, res, c->last_solve_ms * 1e-3);
 }
 
 extern "C" int minife_set_timing_window(minife_ctx *c, int first_iter, int n_iters) {
@@ -2122,6 +2151,13 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
         o->sell_entries += p.entries;
         o->device_bytes += (int64_t)p.bytes;
     }
+    return MINIFE_OK;
+}
+
+extern "C" int minife_get_timings(const minife_ctx *c, double *assemble_ms, double *solve_ms) {
+    if (!c || !assemble_ms || !solve_ms) return MINIFE_EINVAL;
+    *assemble_ms = c->last_asm_ms;
+    *solve_ms = c->last_solve_ms;
     return MINIFE_OK;
 }
 

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running (large meshes)")
+    config.addinivalue_line("markers", "gpu2: needs >= 2 CUDA devices (skipped otherwise)")
 
 
 def _has_cuda():

@@ -59,7 +59,62 @@ def test_gpu_arm_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
     assert "traffic" in r
     assert d["gpu_launches"] > 0
+    a = d["assembly_roofline"]
+    assert a["ms"] > 0 and a["bytes"] > 0 and abs(a["frac"] - a["achieved"] / a["peak"]) < 1e-12
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     # the e2e number moves the step's inputs and the solution across the host boundary
     assert d["e2e"]["d2h_bytes_per_step"] >= 8 * 31 ** 3
+
+
+def _bench_module():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_bench", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("gpus,env,mode,mesh", [
+    (1, {}, "single", (300, 300, 300)),
+    (2, {}, "multi", (600, 300, 300)),
+    (4, {}, "multi", (600, 600, 300)),
+    (8, {}, "multi", (600, 600, 600)),
+    (1, {"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"}, "rank", (300, 300, 300)),
+    (8, {"WORLD_SIZE": "8", "RANK": "3", "LOCAL_RANK": "3"}, "rank", (600, 600, 600)),
+])
+def test_launch_forms(gpus, env, mode, mesh):
+    """Both launch forms of `bench.py --gpus N` use N GPUs and say so: torchrun -> one RANK
+    ctx per process; plain `--gpus N` -> one MULTI ctx over devices 0..N-1 (weak scaling,
+    configs[4], by default)."""
+    b = _bench_module()
+    r = b.plan_run(gpus, "weak", env)
+    assert r["mode"] == mode and r["n_gpus"] == gpus == r["world"]
+    assert tuple(r["mesh"]) == mesh
+    if mode == "multi":
+        assert r["gpu_indices"] == list(range(gpus))
+    if mode == "rank":
+        assert r["rank"] == int(env["RANK"]) and r["gpu_indices"] == [int(env["LOCAL_RANK"])]
+    s = b.plan_run(gpus, "strong", env)
+    assert tuple(s["mesh"]) == (400, 400, 400) and s["n_gpus"] == gpus
+
+
+def test_launch_form_errors():
+    b = _bench_module()
+    with pytest.raises(SystemExit):
+        b.plan_run(2, "weak", {"WORLD_SIZE": "4"})          # --gpus must equal WORLD_SIZE
+    with pytest.raises(SystemExit):
+        b.plan_run(3, "weak", {})                           # weak scaling: 1/2/4/8 only
+    assert b.plan_run(3, "strong", {})["mode"] == "multi"
+
+
+def test_assembly_bytes_model():
+    """SYM at 300^3: 14 value slots x 8 B + 9 run starts x 4 B + a 4 B mask per storage row
+    (rows padded to 32) + b: the 4.36 GB per assembly VERDICT r01 measured against."""
+    b = _bench_module()
+
+    class Info:
+        rows = local_rows = 301 ** 3
+        sell_entries = 14 * 32 * ((301 ** 3 + 31) // 32)
+    by = b.assembly_bytes(Info, "sym")
+    assert abs(by / 1e9 - 4.36) < 0.01

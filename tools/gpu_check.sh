@@ -1,9 +1,10 @@
 #!/bin/bash
-# One GPU call: parity tests, smoke, default bench, launch list (ncu) of the same bench.
-set -x
-mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+# One GPU call: build, parity tests, smoke, default bench (into gpurun_out/$1, default "check").
+D=gpurun_out/${1:-check}
+mkdir -p $D
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $D/smi.txt
+free -g >> $D/smi.txt
+python -c "import __graft_entry__ as g; g.build()" > $D/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=15 > $D/gpu_tests.log 2>&1; echo "tests rc=$?" >> $D/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1; echo "smoke rc=$?" >> $D/smoke.log
+timeout 900 python bench.py > $D/bench.log 2>&1; echo "bench rc=$?" >> $D/bench.log
