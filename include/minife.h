@@ -128,7 +128,9 @@ typedef struct minife_info {
     int64_t sell_entries;     /* held by this ctx                                         */
     int64_t device_bytes;     /* device memory held by this ctx                           */
     int32_t format;           /* MINIFE_FMT_*                                             */
-    int32_t reserved;
+    int32_t comm;             /* transport of the next solve: 0 none (one part) or device-
+                                 local copies (VIRTUAL DIRECT/WIRE/PUSH), 1 NCCL, 2 device-
+                                 initiated (peer/IPC stores + flags, or TRANSPORT_DEVICE)  */
     int64_t local_nns;        /* non-zero segments (x-runs) of the rows held here */
     int64_t kernel_launches;  /* kernels of this library launched by this ctx since creation
                                  (graph replays counted per kernel node; NCCL's own kernels

@@ -67,7 +67,7 @@ class minife_info(ctypes.Structure):
                 ("max_part_rows", ctypes.c_int64), ("max_part_nnz", ctypes.c_int64),
                 ("max_part_externals", ctypes.c_int64), ("sell_entries", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("format", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("local_nns", ctypes.c_int64),
+                ("comm", ctypes.c_int32), ("local_nns", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64)]
 
 

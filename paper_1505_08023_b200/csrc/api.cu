@@ -2141,6 +2141,7 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
     o->nnz = c->mesh.nnz();
     o->format = c->fmt;
     o->kernel_launches = c->kernel_launches + c->enq_kernels;
+    o->comm = devcomm(c) ? 2 : ((c->world > 1 && c->mode != MINIFE_MODE_VIRTUAL) ? 1 : 0);
     for (auto &p : c->parts) {
         o->local_rows += p.rows;
         o->local_nnz += p.nnz;

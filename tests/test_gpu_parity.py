@@ -285,7 +285,7 @@ def test_rank_mode_world1_device_comm(n, graph):
         check_cg(g, n, 200, 0.0)
         check_cg(g, n, 100, 1e-10)
         info = g.get_info()
-        assert info.kernel_launches > 0
+        assert info.kernel_launches > 0 and info.comm == 2
 
 
 def test_device_comm_launch_count_has_no_host_collective():
@@ -293,7 +293,9 @@ def test_device_comm_launch_count_has_no_host_collective():
     library reports equals the kernels it enqueued) and the solve is bitwise the oracle."""
     n, p = (12, 11, 10), 4
     with M.Minife(*n, virtual=p) as g:
+        assert g.get_info().comm == 0
         g.set_transport(M.TRANSPORT_DEVICE)
+        assert g.get_info().comm == 2
         g.assemble()
         before = g.get_info().kernel_launches
         check_cg(g, n, 50, 0.0)
