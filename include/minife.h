@@ -365,6 +365,32 @@ int minife_dot(int device, int64_t n, const double *u, const double *v, double *
  * Errors: MINIFE_EINVAL (NULL), MINIFE_ENODEV, MINIFE_ENOMEM, MINIFE_ECUDA. */
 int minife_exact_round(int device, const int64_t *words, double *out);
 
+/* ---- verification and report data (rooted collectives) ---------------------------------- */
+
+/* Verification of the last solve ("compare the FE solution with the analytical solution";
+ * S:420-437; C8): for each of the n probe nodes gids[i] (global ids, identical on every rank),
+ * u_fe[i] = x at the node and u_exact[i] = the separation-of-variables series of the unit-cube
+ * problem with `nterms` odd terms per index (>= 151 recommended), evaluated on
+ * the device of the part owning the node at the coordinates fl(i_a / n_a);
+ * *max_abs_err = max_i |u_fe[i] - u_exact[i]|.  Only rank 0 needs these, so multi-GPU ctxs
+ * combine them with ROOTED collectives (§3.2: "Allreduce -> Reduce"): ncclReduce(SUM)
+ * of the per-rank probe arrays (each probe has one owner, zeros elsewhere: exact) and
+ * ncclReduce(MAX) of the per-rank largest error, to rank 0.  Outputs are written on rank 0 (and
+ * in one-process ctxs) only.  The series is deterministic but not bit-equal to a host libm
+ * (verification data, compared within 1e-13).  Collective in RANK mode.
+ * Errors: MINIFE_EINVAL (NULL, n < 0, a gid out of range, nterms < 1), MINIFE_ESTATE (no solve
+ * yet), MINIFE_ECUDA, MINIFE_ENCCL. */
+int minife_verify(minife_ctx *ctx, int64_t n, const int64_t *gids, int nterms, double *u_fe,
+                  double *u_exact, double *max_abs_err);
+
+/* Per-rank device times of the last minife_assemble and minife_cg_solve (ms):
+ * per_rank[2r] = assembly, per_rank[2r+1] = solve of rank/part r (SPEC's per-phase report,
+ * S:465-468).  RANK mode: a ROOTED gather ("Allgather -> Gather": each rank sends its two
+ * numbers to rank 0 by ncclSend/ncclRecv); per_rank[2 world] is written on rank 0 only.
+ * Other modes: one entry per part of the ctx.  Collective in RANK mode.
+ * Errors: MINIFE_EINVAL, MINIFE_ECUDA, MINIFE_ENCCL. */
+int minife_gather_times(minife_ctx *ctx, double *per_rank);
+
 /* Library version string. */
 const char *minife_version(void);
 

@@ -114,6 +114,8 @@ SIGNATURES = {
     "minife_spmv_device": (_I, [_P, _P, _P, _P]),
     "minife_get_info": (_I, [_P, ctypes.POINTER(minife_info)]),
     "minife_get_timings": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
+    "minife_verify": (_I, [_P, _I64, _P, _I, _P, _P, ctypes.POINTER(_D)]),
+    "minife_gather_times": (_I, [_P, _P]),
     "minife_get_part_info": (_I, [_P, _I, ctypes.POINTER(minife_part_info)]),
     "minife_export_csr": (_I, [_P, _P, _P, _P]),
     "minife_export_rows": (_I, [_P, _I64, _P, _P, _P, _P]),
@@ -399,6 +401,24 @@ class Minife:
         self._check(minife_get_history(self.h, _ptr(h), cap, ctypes.byref(n)),
                     "minife_get_history")
         return h[: n.value].copy()
+
+    def verify(self, gids, nterms: int = 200):
+        """(u_fe, u_exact, max |error|) at probe nodes (rank 0 / one-process ctxs)."""
+        gids = np.ascontiguousarray(gids, dtype=np.int64)
+        fe = np.zeros(max(gids.size, 1))
+        ex = np.zeros(max(gids.size, 1))
+        mx = ctypes.c_double(0.0)
+        self._check(minife_verify(self.h, gids.size, _ptr(gids), nterms, _ptr(fe), _ptr(ex),
+                                  ctypes.byref(mx)), "minife_verify")
+        return fe[:gids.size], ex[:gids.size], mx.value
+
+    def gather_times(self) -> np.ndarray:
+        """Per-rank (assembly ms, solve ms) of the last calls, gathered to rank 0."""
+        i = self.get_info()
+        n = i.world if i.mode == MODE_RANK else max(i.nparts, 1)
+        out = np.zeros(2 * n)
+        self._check(minife_gather_times(self.h, _ptr(out)), "minife_gather_times")
+        return out.reshape(n, 2)
 
     def owned_ids(self) -> np.ndarray:
         out = np.zeros(self.get_info().local_rows, dtype=np.int64)

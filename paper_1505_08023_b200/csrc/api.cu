@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -134,6 +135,7 @@ struct Part {
     cudaStream_t cstream = nullptr;               // halo transport, overlapped with the SpMV
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;    // per-part timing of assemble / solve
+    double t_asm_ms = 0.0, t_solve_ms = 0.0;          // last assemble / solve, this part
     int grid_spmv = 1, grid_upd = 1;
     size_t bytes = 0, matrix_bytes = 0;
     unsigned long long *acc_pAp(int par = 0) const { return d_acc + (2 * (par & 1)) * ACC_WORDS; }
@@ -690,13 +692,14 @@ static int mark_parts(minife_ctx *c, bool end, bool assembly = false) {
     }
     return MINIFE_OK;
 }
-static int elapsed_parts(minife_ctx *c, double *ms_out) {
+static int elapsed_parts(minife_ctx *c, double *ms_out, double Part::*per_part) {
     double mx = 0.0;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         CUDA_TRY(c, cudaEventSynchronize(p.ev_t1));
         float ms = 0.f;
         CUDA_TRY(c, cudaEventElapsedTime(&ms, p.ev_t0, p.ev_t1));
+        p.*per_part = ms;
         mx = std::max(mx, (double)ms);
     }
     *ms_out = mx;
@@ -1123,7 +1126,7 @@ extern "C" int minife_assemble(minife_ctx *c) {
         CUDA_TRY(c, cudaStreamSynchronize(stream_of(c, p)));
     }
     c->last_asm_ms = 0.0;
-    if (timed) TRY(elapsed_parts(c, &c->last_asm_ms));
+    if (timed) TRY(elapsed_parts(c, &c->last_asm_ms, &Part::t_asm_ms));
     c->assembled = true;
     c->solved = false;
     return MINIFE_OK;
@@ -1909,7 +1912,7 @@ extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_
         DevGuard gg(p.dev);
         TRY(wait_solve(c, p.ev_t1));
     }
-    TRY(elapsed_parts(c, &c->last_solve_ms));
+    TRY(elapsed_parts(c, &c->last_solve_ms, &Part::t_solve_ms));
     return read_result(c, max_iters, res, c->last_solve_ms * 1e-3);
 }
 
@@ -2153,6 +2156,165 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
         o->device_bytes += (int64_t)p.bytes;
     }
     return MINIFE_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// verification and report data: rooted collectives (§3.2: data only process 0
+// needs travels by Reduce / Gather, not Allreduce / Allgather)
+// ----------------------------------------------------------------------------------------
+
+extern "C" int minife_verify(minife_ctx *c, int64_t n, const int64_t *gids, int nterms,
+                             double *u_fe, double *u_exact, double *max_abs_err) {
+    if (!c || n < 0 || n > (1 << 24) || nterms < 1 || nterms > 4096 || !max_abs_err ||
+        (n && (!gids || !u_fe || !u_exact)))
+        return MINIFE_EINVAL;
+    if (!c->solved) return MINIFE_ESTATE;
+    const Mesh &m = c->mesh;
+    for (int64_t i = 0; i < n; ++i)
+        if (gids[i] < 0 || gids[i] >= m.rows()) return MINIFE_EINVAL;
+    const bool use_nccl = c->mode == MINIFE_MODE_RANK || (c->mode == MINIFE_MODE_MULTI && c->world > 1);
+    const bool root = c->mode != MINIFE_MODE_RANK || c->rank == 0;
+    std::vector<double> total(2 * n, 0.0);
+    double max_err = 0.0;
+    std::vector<double *> bufs(c->parts.size(), nullptr);
+    int st = MINIFE_OK;
+    for (size_t q = 0; q < c->parts.size() && st == MINIFE_OK; ++q) {
+        Part &p = c->parts[q];
+        DevGuard g(p.dev);
+        cudaStream_t s = launch_stream(c, p);
+        std::vector<int64_t> lrow;
+        std::vector<int32_t> ijk, slot;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t gid = gids[i];
+            const int64_t ix = gid % m.NX(), iy = (gid / m.NX()) % m.NY(), iz = gid / (m.NX() * m.NY());
+            if (!p.plan.owns(ix, iy, iz)) continue;
+            lrow.push_back(p.plan.owned_local(ix, iy, iz));
+            ijk.insert(ijk.end(), {(int32_t)ix, (int32_t)iy, (int32_t)iz});
+            slot.push_back((int32_t)i);
+        }
+        const int k = (int)lrow.size();
+        // one device block: [2n + 1 doubles out | k rows | 3k ijk | k slots]
+        const size_t bytes = 8 * (2 * (size_t)n + 1) + 8 * (size_t)k + 4 * (size_t)(4 * k) + 16;
+        char *blk = nullptr;
+        CUDA_TRY(c, cudaMalloc((void **)&blk, bytes));
+        bufs[q] = (double *)blk;
+        double *out = (double *)blk;
+        int64_t *d_row = (int64_t *)(blk + 8 * (2 * (size_t)n + 1));
+        int32_t *d_ijk = (int32_t *)(d_row + k);
+        int32_t *d_slot = d_ijk + 3 * k;
+        cudaError_t e = cudaMemsetAsync(out, 0, 8 * (2 * (size_t)n + 1), s);
+        if (e == cudaSuccess && k) e = cudaMemcpyAsync(d_row, lrow.data(), 8 * (size_t)k, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && k) e = cudaMemcpyAsync(d_ijk, ijk.data(), 12 * (size_t)k, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && k) e = cudaMemcpyAsync(d_slot, slot.data(), 4 * (size_t)k, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && k) {
+            e = launch_verify(p.d_x, m.nx, m.ny, m.nz, d_row, d_ijk, d_slot, k, nterms, out, s);
+            if (e == cudaSuccess) ++c->enq_kernels;
+        }
+        // this part's largest |u_fe - u_exact| over its own probes -> word 2n of its block
+        std::vector<double> mine(2 * n);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(mine.data(), out, 16 * (size_t)n, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        double local_max = 0.0;
+        for (int j = 0; j < k; ++j)
+            local_max = std::max(local_max, std::fabs(mine[2 * slot[j]] - mine[2 * slot[j] + 1]));
+        if (e == cudaSuccess) e = cudaMemcpy(out + 2 * n, &local_max, 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            set_err(c, "verify: %s", cudaGetErrorString(e));
+            st = MINIFE_ECUDA;
+        }
+        if (!use_nccl) {                 // one process, device-local parts: add on the host
+            for (int j = 0; j < k; ++j) {
+                total[2 * slot[j]] = mine[2 * slot[j]];
+                total[2 * slot[j] + 1] = mine[2 * slot[j] + 1];
+            }
+            max_err = std::max(max_err, local_max);
+        }
+    }
+    if (st == MINIFE_OK && use_nccl) {
+        // every probe has exactly one owner and zeros elsewhere: the SUM reduce to rank 0 is
+        // exact; the largest error by a MAX reduce of one word (rooted)
+        ncclResult_t r = nccl()->GroupStart();
+        for (size_t q = 0; q < c->parts.size() && r == ncclSuccess; ++q) {
+            Part &p = c->parts[q];
+            r = nccl()->Reduce(bufs[q], bufs[q], 2 * (size_t)n, ncclFloat64, ncclSum, 0, p.comm,
+                               launch_stream(c, p));
+            if (r == ncclSuccess)
+                r = nccl()->Reduce(bufs[q] + 2 * n, bufs[q] + 2 * n, 1, ncclFloat64, ncclMax, 0,
+                                   p.comm, launch_stream(c, p));
+        }
+        ncclResult_t r2 = nccl()->GroupEnd();
+        if (r == ncclSuccess) r = r2;
+        if (r != ncclSuccess) {
+            set_err(c, "verify reduce: %s", nccl()->GetErrorString(r));
+            st = MINIFE_ENCCL;
+        }
+        if (st == MINIFE_OK && root) {
+            Part &p = c->parts[0];
+            DevGuard g(p.dev);
+            if (cudaStreamSynchronize(launch_stream(c, p)) != cudaSuccess ||
+                cudaMemcpy(total.data(), bufs[0], 16 * (size_t)n, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(&max_err, bufs[0] + 2 * n, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+                st = MINIFE_ECUDA;
+        }
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            if (cudaStreamSynchronize(launch_stream(c, p)) != cudaSuccess) st = MINIFE_ECUDA;
+        }
+    }
+    for (size_t q = 0; q < c->parts.size(); ++q) {
+        DevGuard g(c->parts[q].dev);
+        if (bufs[q]) cudaFree(bufs[q]);
+    }
+    if (st != MINIFE_OK || !root) return st;
+    for (int64_t i = 0; i < n; ++i) {
+        u_fe[i] = total[2 * i];
+        u_exact[i] = total[2 * i + 1];
+    }
+    *max_abs_err = max_err;
+    return MINIFE_OK;
+}
+
+extern "C" int minife_gather_times(minife_ctx *c, double *per_rank) {
+    if (!c || !per_rank) return MINIFE_EINVAL;
+    if (c->mode != MINIFE_MODE_RANK) {
+        for (size_t q = 0; q < c->parts.size(); ++q) {
+            per_rank[2 * q] = c->parts[q].t_asm_ms;
+            per_rank[2 * q + 1] = c->parts[q].t_solve_ms;
+        }
+        return MINIFE_OK;
+    }
+    // rooted Gather (Allgather -> Gather): rank r sends its two numbers to rank 0 only
+    Part &p = c->parts[0];
+    DevGuard g(p.dev);
+    cudaStream_t s = launch_stream(c, p);
+    double *d = nullptr;
+    const size_t words = 2 * (size_t)c->world;
+    CUDA_TRY(c, cudaMalloc((void **)&d, 8 * words));
+    const double mine[2] = {p.t_asm_ms, p.t_solve_ms};
+    int st = MINIFE_OK;
+    cudaError_t e = cudaMemcpyAsync(d + 2 * c->rank, mine, 16, cudaMemcpyHostToDevice, s);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess) {
+        r = nccl()->GroupStart();
+        if (c->rank == 0) {
+            for (int q = 1; q < c->world && r == ncclSuccess; ++q)
+                r = nccl()->Recv(d + 2 * q, 2, ncclFloat64, q, p.comm, s);
+        } else if (r == ncclSuccess) {
+            r = nccl()->Send(d + 2 * c->rank, 2, ncclFloat64, 0, p.comm, s);
+        }
+        ncclResult_t r2 = nccl()->GroupEnd();
+        if (r == ncclSuccess) r = r2;
+    }
+    if (e == cudaSuccess && r == ncclSuccess && c->rank == 0)
+        e = cudaMemcpyAsync(per_rank, d, 8 * words, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = MINIFE_ECUDA;
+    if (r != ncclSuccess) {
+        set_err(c, "gather: %s", nccl()->GetErrorString(r));
+        st = MINIFE_ENCCL;
+    }
+    cudaFree(d);
+    return st;
 }
 
 extern "C" int minife_get_timings(const minife_ctx *c, double *assemble_ms, double *solve_ms) {

@@ -2975,6 +2975,58 @@ cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStr
     return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------------------
+// Verification ("compare the FE solution with the analytical solution", C8):
+// one CTA per probe node owned by this part.  u_exact is the separation-of-variables series of
+// Laplace's equation on the unit cube with u = 1 on x = 1,
+//   u = sum_{m,n odd} 16/(m n pi^2) e^{lam(x-1)} (1 - e^{-2 lam x}) / (1 - e^{-2 lam})
+//       sin(m pi y) sin(n pi z),  lam = pi sqrt(m^2 + n^2),
+// with `nterms` odd values per index (the ratio form cannot overflow); the node's
+// coordinates are fl(i_a / n_a).  Each thread sums its terms in index order, the CTA adds the
+// thread sums by a fixed tree: deterministic (not bit-equal to a host libm; verification data
+// only, compared within 1e-13).  u_fe = x of the node (owned row).
+// ----------------------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_verify(const double *x, int nx, int ny, int nz,
+                                                const int64_t *local_row, const int32_t *ijk,
+                                                const int32_t *slot, int n, int nterms,
+                                                double *out) {
+    __shared__ double part[256];
+    const int q = blockIdx.x;
+    if (q >= n) return;
+    const double px = (double)ijk[3 * q] / (double)nx;
+    const double py = (double)ijk[3 * q + 1] / (double)ny;
+    const double pz = (double)ijk[3 * q + 2] / (double)nz;
+    const double pi = 3.14159265358979323846;
+    double acc = 0.0;
+    const int64_t total = (int64_t)nterms * nterms;
+    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const int m = 2 * (int)(t / nterms) + 1, nn = 2 * (int)(t % nterms) + 1;
+        const double lam = pi * sqrt((double)m * m + (double)nn * nn);
+        const double ratio = exp(lam * (px - 1.0)) * (1.0 - exp(-2.0 * lam * px)) /
+                             (1.0 - exp(-2.0 * lam));
+        acc += 16.0 / ((double)m * nn * pi * pi) * ratio * sin(m * pi * py) * sin(nn * pi * pz);
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[2 * slot[q]] = x[local_row[q]];
+        out[2 * slot[q] + 1] = part[0];
+    }
+}
+
+cudaError_t launch_verify(const double *x, int nx, int ny, int nz, const int64_t *local_row,
+                          const int32_t *ijk, const int32_t *slot, int n, int nterms,
+                          double *out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_verify<<<n, 256, 0, s>>>(x, nx, ny, nz, local_row, ijk, slot, n, nterms, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_extract_rows(const Matrix &m, const Geom &g, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,
                                 cudaStream_t s) {

@@ -235,6 +235,13 @@ cudaError_t launch_dot(const double *u, const double *v, int64_t n, unsigned lon
                        cudaStream_t s);
 cudaError_t launch_acc_round(const unsigned long long *acc, double *out, cudaStream_t s);
 
+// Verification (C8): for probe q < n (a node owned by this part: local_row[q], mesh
+// indices ijk[3q..3q+2]) out[2 slot[q]] = x[local_row[q]], out[2 slot[q] + 1] = the analytic
+// series with nterms odd terms per index at the node.  One CTA per probe.
+cudaError_t launch_verify(const double *x, int nx, int ny, int nz, const int64_t *local_row,
+                          const int32_t *ijk, const int32_t *slot, int n, int nterms,
+                          double *out, cudaStream_t s);
+
 // Parity helper: rows[] (local) -> up to 27 (extended column, value) pairs each
 cudaError_t launch_extract_rows(const Matrix &m, const Geom &g, const int64_t *rows, int64_t n,
                                 int32_t *out_col, double *out_val, int32_t *out_len,
