@@ -184,72 +184,6 @@ __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int 
     for (int j = 0; j < NEXP; ++j) flush_value_digits(ex.c[j], dig, acc);
 }
 
-// Spill path of ExpansionT::add_dig: one double into the CTA's 16-bit digit counters
-// (dig[D] weighs 2^(16 D - 1074), int32) with at most five native 32-bit shared atomics
-// (RED) instead of three 64-bit ones (CAS loops, which serialise when a warp's lanes spill
-// values of similar magnitude onto the same words).  Exact.  Each chunk is < 2^16 in
-// magnitude: a counter must be drained (drain_digits) before 2^15 full chunks can reach it.
-__device__ __forceinline__ void spill_digits(double x, int *dig, unsigned long long *acc) {
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-    const int e = (int)((bits >> 52) & 0x7ff);
-    const unsigned long long frac = bits & 0xfffffffffffffull;
-    if (e == 0x7ff) {                      // inf / nan: flag word
-        acc_add(acc, x);
-        return;
-    }
-    if (e == 0 && frac == 0) return;
-    const unsigned long long m = e ? (frac | (1ull << 52)) : frac;
-    const int pos = e ? e - 1 : 0;
-    const int d16 = pos >> 4, s16 = pos & 15;
-    const unsigned long long mlo = m << s16;
-    const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
-    const int sg = (bits >> 63) ? -1 : 1;
-    const int ch[5] = {(int)(mlo & 0xffff), (int)((mlo >> 16) & 0xffff),
-                       (int)((mlo >> 32) & 0xffff), (int)(mlo >> 48), (int)mhi};
-#pragma unroll
-    for (int q = 0; q < 5; ++q)
-        if (ch[q]) atomicAdd(&dig[d16 + q], sg * ch[q]);
-}
-
-// Move counters D = first, first + step, ... of dig into the 64-bit words (atomic exchange:
-// safe while other warps keep adding).  Lane-parallel, warp-collective not required.
-__device__ __forceinline__ void drain_digits(int *dig, unsigned long long *acc, int first,
-                                             int step) {
-    for (int D = first + step * (int)(threadIdx.x & 31u); D < ACC_DIG16; D += 32 * step) {
-        const int v = atomicExch(&dig[D], 0);
-        if (v) {
-            const long long val = (long long)v * ((D & 1) ? 65536ll : 1ll);
-            atomicAdd(&acc[D >> 1], (unsigned long long)val);
-        }
-    }
-}
-
-// Expansion whose spills go to the calling warp's PRIVATE 16-bit digit counters (spill_digits:
-// native 32-bit shared atomics, no CAS loops) -- for long streaming sums whose terms span
-// hundreds of binades late in CG (K6's rr).  Each lane drains its share of its warp's counters
-// (D = lane + 32 j) every DRAIN adds; the lanes of a warp advance together, so a counter gains
-// < 32 x (DRAIN + 1) x 2^16 < 2^31 between drains.  Exact.
-struct ExpansionD {
-    static constexpr int DRAIN = 512;
-    double c[NEXP];
-    int *dig;                              // this warp's ACC_DIG16 counters
-    int n;
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int j = 0; j < NEXP; ++j) c[j] = 0.0;
-        n = 0;
-    }
-    __device__ __forceinline__ void add(double x, unsigned long long *acc) {
-#pragma unroll
-        for (int j = 0; j < NEXP; ++j) two_sum(c[j], x, c[j], x);
-        if (x != 0.0) spill_digits(x, dig, acc);
-        if (++n == DRAIN) {
-            n = 0;
-            drain_digits(dig, acc, 0, 1);
-        }
-    }
-};
-
 // Tiered expansion for long per-thread sums: what the first expansion (N1 terms) cannot hold
 // -- a term far below its running total, e.g. late in CG the Dirichlet rows' tiny products --
 // goes to a second one (N2 terms), then a third (N3, optional), and only what none holds
@@ -279,31 +213,8 @@ template <int N1, int N2, int N3 = 0> struct ExpansionT {
             if (x != 0.0) acc_add(spill, x);  // also routes NaN to the flag word
         }
     }
-    // add() with the last spill into 16-bit digit counters (spill_digits)
-    __device__ __forceinline__ void add_dig(double x, int *dig, unsigned long long *acc) {
-#pragma unroll
-        for (int j = 0; j < N1; ++j) two_sum(a[j], x, a[j], x);
-        if (x != 0.0) {
-#pragma unroll
-            for (int j = 0; j < N2; ++j) two_sum(b[j], x, b[j], x);
-            if (N3 > 0 && x != 0.0) {
-#pragma unroll
-                for (int j = 0; j < N3; ++j) two_sum(c[j], x, c[j], x);
-            }
-            if (x != 0.0) spill_digits(x, dig, acc);
-        }
-    }
 };
 using Expansion2 = ExpansionT<NEXP, NEXP>;
-
-// ExpansionD: its components into the CTA counters, then the warp's private counters (all of
-// them, by this lane's share) into the 64-bit words
-__device__ __forceinline__ void expansion_flush_digits(const ExpansionD &ex, int *dig,
-                                                       unsigned long long *acc) {
-#pragma unroll
-    for (int j = 0; j < NEXP; ++j) flush_value_digits(ex.c[j], dig, acc);
-    drain_digits(ex.dig, acc, 0, 1);
-}
 
 template <int N1, int N2, int N3>
 __device__ __forceinline__ void expansion_flush_digits(const ExpansionT<N1, N2, N3> &ex, int *dig,

@@ -1075,16 +1075,12 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 if (lane == 0) mbar_arrive(&empty_bar[st]);
                 if (row >= 0) {
                     a.y[row] = sum;
-                    if (DOT) ex.add_dig(__dmul_rn(xd, sum), sdig, sacc);
+                    if (DOT) ex.add(__dmul_rn(xd, sum), sacc);
                 }
             } else {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[st]);
             }
-            // the spill digits stay inside int32: each consumer warp drains its share of the
-            // counters every 32 tiles (the warps move through the tiles in lockstep, so a
-            // counter gains < 13 warps x 34 tiles x 2^21 < 2^31 between drains)
-            if (DOT && (i & 31) == 31) drain_digits(sdig, sacc, warp, NW);
         }
         if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
@@ -1347,17 +1343,14 @@ __device__ __forceinline__ void r_step(double &r, double ap, double alpha, EX &e
     ex.add(__dmul_rn(r, r), sacc);
 }
 
-template <bool IDENT, bool XL, class EX = ExpansionD>
+template <bool IDENT, bool XL, class EX = Expansion>
 __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) {
     __shared__ unsigned long long sacc[ACC_WORDS], s_in[ACC_WORDS];
     __shared__ int sdig[ACC_DIG16];
-    __shared__ int wdig[UPD_THREADS / 32][ACC_DIG16];   // ExpansionD: per-warp spill digits
     __shared__ double s_alpha;
     __shared__ int s_stop;
     if (a.st->done) return;
     acc_zero_shared(sacc, sdig);
-    for (int i = threadIdx.x; i < (UPD_THREADS / 32) * ACC_DIG16; i += blockDim.x)
-        (&wdig[0][0])[i] = 0;
     if (!acc_in_load(s_in, a, k, 0)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
@@ -1371,7 +1364,6 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     const double alpha = s_alpha;
     EX ex;
     ex.init();
-    if constexpr (sizeof(EX) > sizeof(Expansion)) ex.dig = wdig[threadIdx.x >> 5];
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t rows = a.g.rows;
