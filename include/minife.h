@@ -340,6 +340,11 @@ int minife_bandwidth_probe(int device, int64_t bytes, int reps, double *read_gbs
  * minife_bandwidth_probe call on this process (48 MB buffer re-read); 0 before any probe. */
 double minife_probe_l2_read_gbs(void);
 
+/* Pure-write stream rate (GB/s, streaming stores over the probe's buffer) measured by the last
+ * minife_bandwidth_probe call on this process: the roof of the assembly kernel, which writes
+ * the matrix and reads nothing; 0 before any probe. */
+double minife_probe_write_gbs(void);
+
 /* ---- exact dot products (reading C5) --------------------------------------- */
 
 #define MINIFE_ACC_WORDS 72    /* device superaccumulator: words 0..67 = signed int64 digits,

@@ -127,6 +127,7 @@ SIGNATURES = {
     "minife_plan_lists": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "minife_bandwidth_probe": (_I, [_I, _I64, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "minife_probe_l2_read_gbs": (_D, []),
+    "minife_probe_write_gbs": (_D, []),
     "minife_dot": (_I, [_I, _I64, _P, _P, ctypes.POINTER(_D)]),
     "minife_set_timing_window": (_I, [_P, _I, _I]),
     "minife_get_timing_window": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)]),

@@ -1027,8 +1027,10 @@ extern "C" int minife_exact_round(int device, const int64_t *words, double *out)
 
 namespace minife {
 extern double g_l2_read_gbs;
+extern double g_write_gbs;
 }
 extern "C" double minife_probe_l2_read_gbs(void) { return minife::g_l2_read_gbs; }
+extern "C" double minife_probe_write_gbs(void) { return minife::g_write_gbs; }
 extern "C" const char *minife_version(void) { return MINIFE_VERSION; }
 
 // ----------------------------------------------------------------------------------------

@@ -144,6 +144,8 @@ __global__ void k_rowlen_widths(Geom g, uint8_t *row_len, uint8_t *width, int64_
 // a0.3 + a0.4 + a0.5: element operator, gather-assembly, Dirichlet elimination
 // ----------------------------------------------------------------------------------------
 
+constexpr uint32_t SYM_FULL_MASK = (1u << 27) - 1;        // all 27 stencil slots present
+
 // C1: K(d) for one of the 8 difference patterns d = dx | dy<<1 | dz<<2 of an (hx,hy,hz) brick.
 __device__ double element_operator_d(int nx, int ny, int nz, int d) {
     const double h[3] = {__ddiv_rn(1.0, (double)nx), __ddiv_rn(1.0, (double)ny),
@@ -173,6 +175,19 @@ __device__ __forceinline__ void assembly_table(const Geom &g, double (*sKc)[9]) 
     __syncthreads();
 }
 
+// The 27 slot values of a row none of whose stencil nodes is on the boundary (deep interior):
+// no Dirichlet elimination touches it and every c(i,j) is 8 / 4 / 2 / 1 (two elements per
+// axis), so slot t holds sKc[d(t)][c(t)] -- the same entries the general loop produces.
+__device__ __forceinline__ void interior_table(const double (*sKc)[9], double *sInt) {
+    if (threadIdx.x < 27) {
+        const int t = threadIdx.x;
+        const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
+        const int c = (dx ? 1 : 2) * (dy ? 1 : 2) * (dz ? 1 : 2);
+        sInt[t] = sKc[(dx != 0) | ((dy != 0) << 1) | ((dz != 0) << 2)][c];
+    }
+    __syncthreads();
+}
+
 // One thread per local row (all 32 lanes of the last slice run: padding lanes write the
 // slice's padding).  Entry (i,j) = fold from +0.0 of K(d(i,j)) over the c(i,j) elements that
 // share nodes i and j (C2: every term is the same K(d); c = per-axis product of 1 where the
@@ -183,8 +198,9 @@ __global__ void k_assemble(AsmArgs a) {
     const Geom &g = a.g;
     // C1 and C2's folds of c copies of K(d) (c = 0..8) as a table, once per CTA; the grid is
     // a few CTAs per SM looping over the rows, so the divisions are not paid per 256 rows
-    __shared__ double sKc[8][9];
+    __shared__ double sKc[8][9], sInt[27];
     assembly_table(g, sKc);
+    interior_table(sKc, sInt);
     const int64_t nslices = (g.rows + 31) >> 5;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (row >> 5) < nslices;
          row += (int64_t)gridDim.x * blockDim.x) {
@@ -219,6 +235,22 @@ __global__ void k_assemble(AsmArgs a) {
     const int ix = g.own_lo[0] + lx, iy = g.own_lo[1] + ly, iz = g.own_lo[2] + lz;
     // extended-box coordinates of the row's node
     const int ex = lx + g.off[0], ey = ly + g.off[1], ez = lz + g.off[2];
+    // deep interior (no stencil node on the boundary): constant values, all 27 slots, b = 0
+    // -- the general loop below gives exactly these; ~96 % of the rows at 300^3, so the
+    // kernel stays bound by its stores rather than by this loop's instructions
+    if (a.fmt != FMT_CRS && ix >= 2 && ix <= g.nx - 2 && iy >= 2 && iy <= g.ny - 2 && iz >= 2 &&
+        iz <= g.nz - 2) {
+        const int64_t E0 = g.ext_n[0], E01 = (int64_t)g.ext_n[0] * g.ext_n[1];
+        const int64_t c0 = (int64_t)(ex - 1) + E0 * ey + E01 * ez;
+#pragma unroll
+        for (int j = 0; j < 9; ++j)
+            a.seg[(9 * s + j) * 32 + lane] = (int32_t)(c0 + E0 * (j % 3 - 1) + E01 * (j / 3 - 1));
+#pragma unroll
+        for (int t = sym ? 13 : 0; t < 27; ++t) *vptr(t) = sInt[t];
+        a.mask[s * 32 + lane] = SYM_FULL_MASK;
+        a.b[row] = 0.0;
+        continue;
+    }
     const bool row_bc = on_boundary(ix, iy, iz, g.nx, g.ny, g.nz);
     const int n_el[3] = {(ix > 0) + (ix < g.nx), (iy > 0) + (iy < g.ny), (iz > 0) + (iz < g.nz)};
     double b = 0.0;
@@ -289,8 +321,9 @@ __global__ void k_assemble(AsmArgs a) {
 __global__ void k_assemble_symx(AsmArgs a) {
     const Geom &g = a.g;
     // C1 and C2's fold table once per CTA; grid-stride over the extended box (as k_assemble)
-    __shared__ double sKc[8][9];
+    __shared__ double sKc[8][9], sInt[27];
     assembly_table(g, sKc);
+    interior_table(sKc, sInt);
     const int64_t nslices = (g.ncols + 31) >> 5;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (c >> 5) < nslices;
          c += (int64_t)gridDim.x * blockDim.x) {
@@ -309,6 +342,21 @@ __global__ void k_assemble_symx(AsmArgs a) {
     const int ey = (int)(line - plane * (unsigned)g.ext_n[1]), ez = (int)plane;
     const int ix = g.ext_lo[0] + ex, iy = g.ext_lo[1] + ey, iz = g.ext_lo[2] + ez;
     const int64_t row = col_to_row(g, c);
+    // deep interior and all 26 neighbours inside the extended box: constants (as k_assemble)
+    if (ix >= 2 && ix <= g.nx - 2 && iy >= 2 && iy <= g.ny - 2 && iz >= 2 && iz <= g.nz - 2 &&
+        ex >= 1 && ex <= g.ext_n[0] - 2 && ey >= 1 && ey <= g.ext_n[1] - 2 && ez >= 1 &&
+        ez <= g.ext_n[2] - 2) {
+        const int64_t E0 = g.ext_n[0], E01 = (int64_t)g.ext_n[0] * g.ext_n[1];
+        const int64_t c0 = (int64_t)(ex - 1) + E0 * ey + E01 * ez;
+#pragma unroll
+        for (int j = 0; j < 9; ++j)
+            a.seg[(9 * s + j) * 32 + lane] = (int32_t)(c0 + E0 * (j % 3 - 1) + E01 * (j / 3 - 1));
+#pragma unroll
+        for (int t = 13; t < 27; ++t) a.val[(14 * s + (t - 13)) * 32 + lane] = sInt[t];
+        a.mask[c] = SYM_FULL_MASK | (row >= 0 ? SYM_OWNED : 0u);
+        if (row >= 0) a.b[row] = 0.0;
+        continue;
+    }
     const bool row_bc = on_boundary(ix, iy, iz, g.nx, g.ny, g.nz);
     const int n_el[3] = {(ix > 0) + (ix < g.nx), (iy > 0) + (iy < g.ny), (iz > 0) + (iz < g.nz)};
     double b = 0.0;
@@ -2398,6 +2446,15 @@ __global__ void __launch_bounds__(256) k_copy_stream(const double2 *__restrict__
     for (; i < n2; i += stride) __stcs(dst + i, __ldcs(src + i));
 }
 
+__global__ void __launch_bounds__(256) k_write_stream(double2 *__restrict__ dst, int64_t n2) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const double2 v = make_double2(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride)
+        __stcs(dst + i, v);
+}
+
+double g_write_gbs = 0.0;                 // last probe_bandwidth: pure-write stream rate
+
 cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *copy_gbs) {
     query_occupancy();
     const int64_t n2 = bytes / 16;
@@ -2427,6 +2484,20 @@ cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *c
         if (e == cudaSuccess) e = cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         if (r > 0) best_c = std::min(best_c, ms);
+    }
+    // pure-write stream (the roof of the assembly kernel, which reads nothing)
+    {
+        float best_w = 1e30f;
+        for (int r = 0; e == cudaSuccess && r < reps + 1; ++r) {
+            float ms = 0.f;
+            cudaEventRecord(e0);
+            k_write_stream<<<grid, 256>>>(b, n2);
+            cudaEventRecord(e1);
+            e = cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r > 0) best_w = std::min(best_w, ms);
+        }
+        g_write_gbs = (double)(n2 * 16) / (best_w * 1e-3) / 1e9;
     }
     // the bulk-copy engine's read rate (what the TMA-pipelined kernels can draw)
     static unsigned long long attr = 0;
