@@ -2667,12 +2667,19 @@ cudaError_t launch_rowlen_widths(const Geom &g, uint8_t *row_len, uint8_t *width
 }
 
 // grid-stride: at most 8 CTAs of 256 threads per SM (each builds the C1/C2 table once)
+#ifndef ASM_CTAS_PER_SM
+#define ASM_CTAS_PER_SM 128
+#endif
 cudaError_t launch_assemble(const AsmArgs &a, cudaStream_t s) {
     query_occupancy();
     const bool symx = a.fmt == FMT_SYM && !a.g.ident;
     const int64_t threads = (((symx ? a.g.ncols : a.g.rows) + 31) >> 5) * 32;
+    // many short grid-stride CTAs (128 per SM): CTAs retire at different times and the store
+    // streams of the next ones fill in.  B200, 300^3 SYM, interleaved A/B (profiles/r02/ab):
+    // 8 per SM 0.91 ms, 32 0.85, 64 0.80, 128 0.77 (0.86 of copy, 0.94 of the write probe),
+    // 256 0.83, one row per thread 1.36 (the C1 table per CTA dominates)
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((threads + 255) / 256,
-                                                                (int64_t)g_sms * 8));
+                                                                (int64_t)g_sms * ASM_CTAS_PER_SM));
     if (symx) k_assemble_symx<<<(unsigned)grid, 256, 0, s>>>(a);
     else k_assemble<<<(unsigned)grid, 256, 0, s>>>(a);
     return cudaGetLastError();
