@@ -209,6 +209,10 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *   "device_comm"     MULTI/RANK: -1 (default) device-initiated comm where it was set up at
  *                     creation, 0 NCCL transport; RANK at world 1: 1 forces the device
  *                     reduction kernels (self-exchange).  Set identically on every rank.
+ *   "fold_comm"       device comm, SYM: 1 (default) the accumulator pushes ride in the last
+ *                     CTA of the SpMV / r update / init kernels and the halo wait in the
+ *                     last CTA of the p update (4 launches per iteration); 0 separate
+ *                     k_acc_push / k_halo_wait launches (7)
  *   "comm_timeout_ms" device comm: how long a kernel waits for a peer's flag before the
  *                     solve fails with MINIFE_ECOMM (default 60000)
  * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,

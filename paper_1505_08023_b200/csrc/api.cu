@@ -194,6 +194,7 @@ struct minife_ctx {
         int x_late = 1;            // x += alpha p applied by K7 (1) or K6 (0)
         int cluster_dd = 1;        // cluster solver: DSMEM digit pushes
         int device_comm = -1;      // MULTI/RANK: 1 device-initiated comm, 0 NCCL, -1 auto
+        int fold_comm = 1;         // device comm: pushes / halo wait inside the producers
         int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
@@ -653,6 +654,13 @@ static bool devcomm(const minife_ctx *c) {
     return c->opt.device_comm != 0;
 }
 
+// Device comm with the pushes / halo wait folded into the producing kernels' last CTAs (the
+// SYM path; SEG/CRS keep the separate k_acc_push / k_halo_wait launches).  Option
+// "fold_comm" = 0 keeps the separate launches everywhere (tests compare both).
+static bool fold_comm(const minife_ctx *c) {
+    return devcomm(c) && c->fmt == MINIFE_FMT_SYM && c->opt.fold_comm != 0;
+}
+
 static bool push_mode(const minife_ctx *c) {
     if (devcomm(c)) return c->world > 1;
     return c->world > 1 && c->push_ready &&
@@ -899,6 +907,7 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"x_late", &c->opt.x_late, 0, 1},
         {"cluster_dd", &c->opt.cluster_dd, 0, 1},
         {"device_comm", &c->opt.device_comm, -1, 1},
+        {"fold_comm", &c->opt.fold_comm, 0, 1},
         {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
     };
     for (auto &t : table) {
@@ -1367,9 +1376,12 @@ static int enqueue_k7_with_halo(minife_ctx *c, int k) {
         if (!last) TRY(enqueue_push(c, k, 1, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
+            UpdArgs u7 = upd_args(c, p, 1);
+            // device comm: K7's last CTA waits for the neighbours' halo of p_(k+1)
+            if (fold_comm(c) && !last && !p.plan.nbr.empty()) u7.fold_wait_k = k + 1;
+            LAUNCH(c, launch_update_p(u7, k, p.grid_upd, launch_stream(c, p)));
         }
-        return last ? MINIFE_OK : push_wait(c, k + 1);
+        return (last || fold_comm(c)) ? MINIFE_OK : push_wait(c, k + 1);
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1421,9 +1433,10 @@ static int enqueue_init(minife_ctx *c, double tol) {
         CUDA_TRY(c, cudaMemsetAsync(p.d_acc, 0, 4 * ACC_WORDS * sizeof(unsigned long long), s));
         UpdArgs a = upd_args(c, p, 0);
         a.acc_out = p.acc_rr();
+        a.fold_push = fold_comm(c) ? 1 : 0;          // the last CTA pushes rr_0
         LAUNCH(c, launch_init_vectors(a, p.grid_upd, s));
     }
-    TRY(enqueue_allreduce(c, 1, 0));
+    if (!fold_comm(c)) TRY(enqueue_allreduce(c, 1, 0));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 0);
@@ -1479,8 +1492,13 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
-                                    launch_stream(c, p)));
+            SpmvArgs sa = spmv_args(c, p, p.d_p, p.d_Ap, true);
+            if (fold_comm(c)) {                      // the SpMV's last CTA pushes pAp_k
+                sa.dc = upd_args(c, p, 0).dc;
+                sa.fold_push = 1;
+                sa.k = k;
+            }
+            LAUNCH(c, launch_spmv(sa, true, p.grid_spmv, launch_stream(c, p)));
         }
         TRY(tw_mark(c, k, true));
     } else {
@@ -1496,14 +1514,16 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         if (!t) TRY(tw_mark(c, k, true));
     }
     if (t) t->mark(0);
-    TRY(enqueue_allreduce(c, 0, k));
+    if (!(osym && fold_comm(c))) TRY(enqueue_allreduce(c, 0, k));
     if (t) t->mark(3);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        LAUNCH(c, launch_update_xr(upd_args(c, p, 0), k, p.grid_upd, launch_stream(c, p)));
+        UpdArgs u6 = upd_args(c, p, 0);
+        u6.fold_push = fold_comm(c) ? 1 : 0;          // K6's last CTA pushes rr_k
+        LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
     }
     if (t) t->mark(1);
-    TRY(enqueue_allreduce(c, 1, k));
+    if (!fold_comm(c)) TRY(enqueue_allreduce(c, 1, k));
     if (t) t->mark(3);
     if (osym) {
         TRY(enqueue_k7_with_halo(c, k));

@@ -401,6 +401,150 @@ __global__ void k_assemble_symx(AsmArgs a) {
 }
 
 // ----------------------------------------------------------------------------------------
+// Device-initiated communication (DevComm, kernels.h; DESIGN.md §7): release/acquire flags at
+// system scope, payloads stored straight into the receiver's region.
+// ----------------------------------------------------------------------------------------
+
+static_assert(ACC_WORDS == 72, "comm_words() assumes 72-word accumulators");
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long comm_gen(const DevComm &dc) {
+    return *(volatile const unsigned long long *)dc.local;
+}
+
+// Spin until *flag >= seq.  A peer that never signals (dead rank, broken mapping) ends the
+// wait after dc.timeout_ns: the error is recorded in the region and in the CG state (status 9
+// -> MINIFE_ECOMM), and every later kernel of the solve returns at its done test.
+__device__ bool comm_spin(const DevComm &dc, const unsigned long long *flag,
+                          unsigned long long seq, CgState *st) {
+    if (ld_acquire_sys(flag) >= seq) return true;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flag) < seq) {
+        if (*(volatile const unsigned long long *)(dc.local + 2)) return false;
+        __nanosleep(100);
+        if (global_ns() - t0 > (unsigned long long)dc.timeout_ns) {
+            atomicExch(dc.local + 2, 1ull);
+            st->status = 9;
+            st->done = 1;
+            __threadfence();
+            return false;
+        }
+    }
+    return true;
+}
+
+// The all-reduced accumulator `which` (0 pAp_k, 1 rr_k) into shared memory: the local words
+// (one part, or all-reduced by the host-launched transport) or, with device comm, the int64
+// sum over every rank's inbox slot (two's-complement sums: the same value an int64-SUM
+// all-reduce produces, independent of the rank order).  Block-uniform; false on a timeout.
+__device__ bool acc_in_load(unsigned long long *s_in, const UpdArgs &a, int k, int which) {
+    const DevComm &dc = a.dc;
+    if (!dc.local) {
+        acc_load_shared(s_in, a.acc_in);
+        return true;
+    }
+    __shared__ int s_ok;
+    const unsigned long long gen = comm_gen(dc);
+    const int gp = (int)(gen & 1);
+    const unsigned long long seq = comm_seq(gen, k, which);
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
+        if (!comm_spin(dc, dc.local + comm_acc_flag(dc.world, gp, which, t), seq, a.st)) s_ok = 0;
+    __syncthreads();
+    if (!s_ok) return false;
+    const unsigned long long *in =
+        dc.local + comm_inbox(dc.world) + (int64_t)(2 * gp + which) * dc.world * ACC_WORDS;
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
+        unsigned long long sum = 0ull;
+        for (int t = 0; t < dc.world; ++t) sum += __ldcv(in + (int64_t)t * ACC_WORDS + i);
+        s_in[i] = sum;
+    }
+    return true;
+}
+
+// Reduction `which` of iteration k: this part's accumulator into slot `rank` of every rank's
+// inbox (its own included), then one release flag per rank.  Slot reuse is safe with two
+// generation parities x {pAp, rr}: a rank writes reduction n+2 only after it has consumed
+// n+1, which needs every rank's contribution to n+1, which each rank stores only after it has
+// consumed n (stream order); a new solve (next generation) uses the other parity.
+// The push itself (one CTA): the words of `acc` into slot `rank` of every rank's inbox, a
+// system-scope fence, then one release flag per rank.
+__device__ void acc_push_body(const DevComm &dc, const unsigned long long *acc, int k, int which) {
+    const unsigned long long gen = comm_gen(dc);
+    const int gp = (int)(gen & 1);
+    const int64_t off =
+        comm_inbox(dc.world) + ((int64_t)(2 * gp + which) * dc.world + dc.rank) * ACC_WORDS;
+    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
+        const unsigned long long w = __ldcg(acc + i);
+        for (int t = 0; t < dc.world; ++t) dc.region[t][off + i] = w;
+    }
+    __threadfence_system();
+    __syncthreads();
+    const unsigned long long seq = comm_seq(gen, k, which);
+    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
+        st_release_sys(dc.region[t] + comm_acc_flag(dc.world, gp, which, dc.rank), seq);
+}
+
+__global__ void k_acc_push(UpdArgs a, int k, int which, const unsigned long long *acc) {
+    if (k > 0 && a.st->done) return;     // k = 0 (rr_0): the state is not initialised yet
+    acc_push_body(a.dc, acc, k, which);
+}
+
+// The same push folded into the kernel that produced the accumulator: every CTA, after its
+// atomics into `acc`, takes a ticket; the last CTA (all others' atomics are then visible at
+// gpu scope) pushes.  Saves a launch per reduction.  All threads of the CTA call it.
+__device__ void acc_push_last_cta(const DevComm &dc, const unsigned long long *acc, int k,
+                                  int which, unsigned long long *ticket) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1ull) == (unsigned long long)(gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    acc_push_body(dc, acc, k, which);
+    if (threadIdx.x == 0) *ticket = 0ull;
+}
+
+// Before SpMV(k): every neighbor's halo values of p_k have landed (k_push signalled).
+__device__ void halo_wait_body(const DevComm &dc, int k, CgState *st) {
+    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k);
+    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
+        comm_spin(dc, dc.local + comm_halo_flag(dc.world, dc.nbr_rank[t]), seq, st);
+}
+
+__global__ void k_halo_wait(UpdArgs a, int k) {
+    if (a.st->done) return;
+    halo_wait_body(a.dc, k, a.st);
+}
+
+// The same wait folded into the end of K7 (whose p_(k+1) the neighbours' pushes complete):
+// the last CTA to finish waits, so the next SpMV starts only once the halo has landed.
+__device__ void halo_wait_last_cta(const DevComm &dc, int k, CgState *st,
+                                   unsigned long long *ticket) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1ull) == (unsigned long long)(gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    halo_wait_body(dc, k, st);
+    if (threadIdx.x == 0) *ticket = 0ull;
+}
+
+// ----------------------------------------------------------------------------------------
 // a2: SpMV  y = A x  (+ exact pAp epilogue)
 // ----------------------------------------------------------------------------------------
 
@@ -767,6 +911,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_spmv_tma(SpmvArgs a) {
     if (DOT) {
         __syncthreads();
         acc_merge_to_global(sacc, sdig, a.acc);
+        if (a.fold_push) acc_push_last_cta(a.dc, a.acc, a.k, 0, a.dc.local + 3);
     }
 }
 
@@ -897,6 +1042,7 @@ __global__ void __launch_bounds__(SyCfg<NW, NST>::THREADS, 1) k_spmv_sym(SpmvArg
     if (DOT) {
         __syncthreads();
         acc_merge_to_global(sacc, sdig, a.acc);
+        if (a.fold_push) acc_push_last_cta(a.dc, a.acc, a.k, 0, a.dc.local + 3);
     }
 }
 
@@ -1135,119 +1281,13 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     if (DOT) {
         __syncthreads();
         acc_merge_to_global(sacc, sdig, a.acc);
+        if (a.fold_push) acc_push_last_cta(a.dc, a.acc, a.k, 0, a.dc.local + 3);
     }
 }
 
 // ----------------------------------------------------------------------------------------
 // CG init (C6 step 1): x = 0, r = b, p = b, rr = dot(r, r)
 // ----------------------------------------------------------------------------------------
-
-// ----------------------------------------------------------------------------------------
-// Device-initiated communication (DevComm, kernels.h; DESIGN.md §7): release/acquire flags at
-// system scope, payloads stored straight into the receiver's region.
-// ----------------------------------------------------------------------------------------
-
-static_assert(ACC_WORDS == 72, "comm_words() assumes 72-word accumulators");
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned long long comm_gen(const DevComm &dc) {
-    return *(volatile const unsigned long long *)dc.local;
-}
-
-// Spin until *flag >= seq.  A peer that never signals (dead rank, broken mapping) ends the
-// wait after dc.timeout_ns: the error is recorded in the region and in the CG state (status 9
-// -> MINIFE_ECOMM), and every later kernel of the solve returns at its done test.
-__device__ bool comm_spin(const DevComm &dc, const unsigned long long *flag,
-                          unsigned long long seq, CgState *st) {
-    if (ld_acquire_sys(flag) >= seq) return true;
-    const unsigned long long t0 = global_ns();
-    while (ld_acquire_sys(flag) < seq) {
-        if (*(volatile const unsigned long long *)(dc.local + 2)) return false;
-        __nanosleep(100);
-        if (global_ns() - t0 > (unsigned long long)dc.timeout_ns) {
-            atomicExch(dc.local + 2, 1ull);
-            st->status = 9;
-            st->done = 1;
-            __threadfence();
-            return false;
-        }
-    }
-    return true;
-}
-
-// The all-reduced accumulator `which` (0 pAp_k, 1 rr_k) into shared memory: the local words
-// (one part, or all-reduced by the host-launched transport) or, with device comm, the int64
-// sum over every rank's inbox slot (two's-complement sums: the same value an int64-SUM
-// all-reduce produces, independent of the rank order).  Block-uniform; false on a timeout.
-__device__ bool acc_in_load(unsigned long long *s_in, const UpdArgs &a, int k, int which) {
-    const DevComm &dc = a.dc;
-    if (!dc.local) {
-        acc_load_shared(s_in, a.acc_in);
-        return true;
-    }
-    __shared__ int s_ok;
-    const unsigned long long gen = comm_gen(dc);
-    const int gp = (int)(gen & 1);
-    const unsigned long long seq = comm_seq(gen, k, which);
-    if (threadIdx.x == 0) s_ok = 1;
-    __syncthreads();
-    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
-        if (!comm_spin(dc, dc.local + comm_acc_flag(dc.world, gp, which, t), seq, a.st)) s_ok = 0;
-    __syncthreads();
-    if (!s_ok) return false;
-    const unsigned long long *in =
-        dc.local + comm_inbox(dc.world) + (int64_t)(2 * gp + which) * dc.world * ACC_WORDS;
-    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
-        unsigned long long sum = 0ull;
-        for (int t = 0; t < dc.world; ++t) sum += __ldcv(in + (int64_t)t * ACC_WORDS + i);
-        s_in[i] = sum;
-    }
-    return true;
-}
-
-// Reduction `which` of iteration k: this part's accumulator into slot `rank` of every rank's
-// inbox (its own included), then one release flag per rank.  Slot reuse is safe with two
-// generation parities x {pAp, rr}: a rank writes reduction n+2 only after it has consumed
-// n+1, which needs every rank's contribution to n+1, which each rank stores only after it has
-// consumed n (stream order); a new solve (next generation) uses the other parity.
-__global__ void k_acc_push(UpdArgs a, int k, int which, const unsigned long long *acc) {
-    if (k > 0 && a.st->done) return;     // k = 0 (rr_0): the state is not initialised yet
-    const DevComm &dc = a.dc;
-    const unsigned long long gen = comm_gen(dc);
-    const int gp = (int)(gen & 1);
-    const int64_t off =
-        comm_inbox(dc.world) + ((int64_t)(2 * gp + which) * dc.world + dc.rank) * ACC_WORDS;
-    for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) {
-        const unsigned long long w = __ldcg(acc + i);
-        for (int t = 0; t < dc.world; ++t) dc.region[t][off + i] = w;
-    }
-    __threadfence_system();
-    __syncthreads();
-    const unsigned long long seq = comm_seq(gen, k, which);
-    for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
-        st_release_sys(dc.region[t] + comm_acc_flag(dc.world, gp, which, dc.rank), seq);
-}
-
-// Before SpMV(k): every neighbor's halo values of p_k have landed (k_push signalled).
-__global__ void k_halo_wait(UpdArgs a, int k) {
-    if (a.st->done) return;
-    const DevComm &dc = a.dc;
-    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k);
-    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
-        comm_spin(dc, dc.local + comm_halo_flag(dc.world, dc.nbr_rank[t]), seq, a.st);
-}
 
 template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
@@ -1274,6 +1314,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
     expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
     acc_merge_to_global(sacc, sdig, a.acc_out);
+    if (a.fold_push) acc_push_last_cta(a.dc, a.acc_out, 0, 1, a.dc.local + 4);
 }
 
 // C6 step 1 decisions: rr_0, hist[0] = sqrt(rr_0), stop threshold fl(tol hist[0]) (one thread)
@@ -1502,6 +1543,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
     acc_merge_to_global(sacc, sdig, a.acc_out);
+    if (a.fold_push) acc_push_last_cta(a.dc, a.acc_out, k, 1, a.dc.local + 4);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -2036,6 +2078,9 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             }
         }
     }
+    // device comm: the next SpMV needs the neighbours' halo of p_(k+1) (their k_push ran
+    // before this kernel on their side); no wait once the solve stops (uniform decision)
+    if (a.fold_wait_k > 0 && !stop) halo_wait_last_cta(a.dc, a.fold_wait_k, a.st, a.dc.local + 5);
 }
 
 // K7 of the deferred-x scheme (launch_update_p2): the x update of iteration k is

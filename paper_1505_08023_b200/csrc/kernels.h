@@ -82,30 +82,6 @@ struct AsmArgs {
     const int32_t *slice_pos;           // SEG: row slice -> storage position (null: identity)
 };
 
-struct SpmvArgs {
-    Matrix m;
-    Geom g;
-    int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
-    int val_evict_first;                // SYMM: stream the values evict-first in L2
-    int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
-    int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
-    int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
-    const double *x;                    // [ncols], extended-box order
-    double *y;                          // [rows]
-    unsigned long long *acc;            // pAp accumulator (DOT only)
-    unsigned long long *acc_zero;       // accumulator to clear (CTA 0), may be null
-    const CgState *st;                  // early exit when st->done (may be null)
-    // fused CG iteration (one part, SEG format; DESIGN.md §5): the SpMV operand is
-    // p_k = r + beta_{k-1} p_{k-1} formed at gather time (p_1 = r), written to p_new for the
-    // own rows, and x += alpha_{k-1} p_{k-1} is applied for the own rows.
-    int fused_k;                        // 0: plain SpMV; k >= 1: fused iteration k
-    const double *r, *p_old;
-    double *p_new, *xsol;
-    unsigned long long *acc_rr_in;      // rr_{k-1} accumulator (k >= 2)
-    double *hist, *rr;
-    CgState *stw;                       // writable state (decisions)
-};
-
 // Device-initiated communication between parts/ranks:
 // every part owns one COMM REGION in its device memory; the other parts store into it
 // directly (same device: VIRTUAL; peer access over NVLink: MULTI; CUDA-IPC mappings: RANK)
@@ -146,6 +122,34 @@ struct DevComm {
     long long timeout_ns;               // spin limit; exceeded -> CgState.status = 9 (ECOMM)
 };
 
+struct SpmvArgs {
+    Matrix m;
+    Geom g;
+    int64_t s_begin, s_end;             // storage slices [s_begin, s_end) (SEG/CRS kernels)
+    int val_evict_first;                // SYMM: stream the values evict-first in L2
+    int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
+    int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
+    int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
+    const double *x;                    // [ncols], extended-box order
+    double *y;                          // [rows]
+    unsigned long long *acc;            // pAp accumulator (DOT only)
+    unsigned long long *acc_zero;       // accumulator to clear (CTA 0), may be null
+    const CgState *st;                  // early exit when st->done (may be null)
+    // fused CG iteration (one part, SEG format; DESIGN.md §5): the SpMV operand is
+    // p_k = r + beta_{k-1} p_{k-1} formed at gather time (p_1 = r), written to p_new for the
+    // own rows, and x += alpha_{k-1} p_{k-1} is applied for the own rows.
+    int fused_k;                        // 0: plain SpMV; k >= 1: fused iteration k
+    const double *r, *p_old;
+    double *p_new, *xsol;
+    unsigned long long *acc_rr_in;      // rr_{k-1} accumulator (k >= 2)
+    double *hist, *rr;
+    CgState *stw;                       // writable state (decisions)
+    // device comm (DevComm): fold_push = 1 -> the last CTA pushes the pAp accumulator of
+    // iteration k to every rank's inbox (SYM kernels), instead of a k_acc_push launch
+    DevComm dc;
+    int fold_push, k;
+};
+
 struct UpdArgs {
     Geom g;
     double *x, *r;                      // [rows]
@@ -164,6 +168,8 @@ struct UpdArgs {
     int xdef;
     int x_late;                         // K7 applies x += alpha p (1, default) or K6 does (0)
     DevComm dc;                         // device-initiated reductions / halo (dc.local != null)
+    int fold_push;                      // K6 / init: the last CTA pushes the rr accumulator
+    int fold_wait_k;                    // K7: > 0 -> the last CTA waits for the halo of p_k
     int cl_dd;                          // cluster solver: DSMEM digit pushes (1, default)
 };
 constexpr int XDEF_MAX = 8;

@@ -288,11 +288,14 @@ def test_rank_mode_world1_device_comm(n, graph):
         assert info.kernel_launches > 0 and info.comm == 2
 
 
-def test_device_comm_launch_count_has_no_host_collective():
+@pytest.mark.parametrize("fold", [1, 0])
+def test_device_comm_launch_count_has_no_host_collective(fold):
     """VIRTUAL parts on the device protocol: every kernel of the solve is ours (the count the
-    library reports equals the kernels it enqueued) and the solve is bitwise the oracle."""
+    library reports equals the kernels it enqueued) and the solve is bitwise the oracle --
+    with the accumulator pushes and the halo wait folded into the producing kernels' last
+    CTAs (fold_comm = 1, default) and as separate launches (0)."""
     n, p = (12, 11, 10), 4
-    with M.Minife(*n, virtual=p) as g:
+    with M.Minife(*n, virtual=p, options={"fold_comm": fold}) as g:
         assert g.get_info().comm == 0
         g.set_transport(M.TRANSPORT_DEVICE)
         assert g.get_info().comm == 2
@@ -300,11 +303,33 @@ def test_device_comm_launch_count_has_no_host_collective():
         before = g.get_info().kernel_launches
         check_cg(g, n, 50, 0.0)
         launched = g.get_info().kernel_launches - before
-        # per part: init_vectors, acc_push, init_finalize, push + wait (p_1); per iteration:
-        # SpMV, acc_push, K6, acc_push, push, K7, halo wait (none after the last K7)
         parts = [g.part_info(q) for q in range(p)]
         assert all(q.n_neighbors > 0 for q in parts)
-        assert launched == p * (5 + 7 * 50 - 2)
+        if fold:
+            # per part: init_vectors, init_finalize, push + wait (p_1); per iteration: SpMV,
+            # K6, push, K7 (no push after the last K7)
+            assert launched == p * (4 + 4 * 50 - 1)
+        else:
+            # per part: init_vectors, acc_push, init_finalize, push + wait (p_1); per
+            # iteration: SpMV, acc_push, K6, acc_push, push, K7, halo wait (none after the
+            # last K7)
+            assert launched == p * (5 + 7 * 50 - 2)
+
+
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
+@pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((12, 11, 10), 8)])
+def test_device_comm_unfolded_bit_identical(n, p, fmt):
+    """The device protocol with separate k_acc_push / k_halo_wait launches (fold_comm = 0):
+    bitwise the oracle, graph and profile mode."""
+    s = oracle_system(n)
+    with M.Minife(*n, virtual=p, fmt=fmt, options={"fold_comm": 0}) as g:
+        g.set_transport(M.TRANSPORT_DEVICE)
+        g.assemble()
+        check_spmv(g, s, 7)
+        check_cg(g, n, 200, 0.0)
+        check_cg(g, n, 100, 1e-10)
+        g.cg_profile(50)
+        check_cg(g, n, 200, 0.0)
 
 
 def test_errors_and_states():
