@@ -491,7 +491,10 @@ __device__ void acc_push_body(const DevComm &dc, const unsigned long long *acc, 
         const unsigned long long w = __ldcg(acc + i);
         for (int t = 0; t < dc.world; ++t) dc.region[t][off + i] = w;
     }
-    __threadfence_system();
+    // one system-scope fence after the CTA barrier covers every thread's stores (fences are
+    // cumulative over writes observed through bar.sync; the flag stores are releases too)
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
     __syncthreads();
     const unsigned long long seq = comm_seq(gen, k, which);
     for (int t = threadIdx.x; t < dc.world; t += blockDim.x)
@@ -509,12 +512,14 @@ __global__ void k_acc_push(UpdArgs a, int k, int which, const unsigned long long
 __device__ void acc_push_last_cta(const DevComm &dc, const unsigned long long *acc, int k,
                                   int which, unsigned long long *ticket) {
     __shared__ int s_last;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1ull) == (unsigned long long)(gridDim.x - 1);
+    if (threadIdx.x == 0) {
+        __threadfence();                   // this CTA's atomics into acc, before the ticket
+        s_last = atomicAdd(ticket, 1ull) == (unsigned long long)(gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     acc_push_body(dc, acc, k, which);
     if (threadIdx.x == 0) *ticket = 0ull;
 }
@@ -2272,14 +2277,15 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode
     }
     const DevComm &dc = a.dc;
     if (!dc.local) return;
-    __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+        __threadfence_system();            // this CTA's peer stores (cumulative via bar.sync)
         s_last = atomicAdd(reinterpret_cast<unsigned long long *>(dc.local + 1), 1ull) ==
                  (unsigned long long)(gridDim.x - 1);
+        if (s_last) __threadfence_system();
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence_system();
     const unsigned long long seq = comm_halo_seq(comm_gen(dc), k_halo);
     for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
         st_release_sys(dc.region[dc.nbr_rank[t]] + comm_halo_flag(dc.world, dc.rank), seq);
