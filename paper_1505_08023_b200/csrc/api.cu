@@ -122,6 +122,8 @@ struct Part {
     // device-initiated comm (DevComm, kernels.h): this part's comm region, the table of every
     // rank's region as seen from this device, the neighbor ranks; RANK: CUDA-IPC mappings of
     // the other ranks' regions and p arrays (closed on destroy)
+    int32_t *d_tile_order = nullptr;              // SYM SpMV: band-major tile order (or null)
+    int64_t tile_order_n = 0;
     unsigned long long *d_comm = nullptr;
     unsigned long long **d_comm_ptrs = nullptr;
     int32_t *d_nbr_rank = nullptr;
@@ -195,6 +197,7 @@ struct minife_ctx {
         int cluster_dd = 1;        // cluster solver: DSMEM digit pushes
         int device_comm = -1;      // MULTI/RANK: 1 device-initiated comm, 0 NCCL, -1 auto
         int fold_comm = 1;         // device comm: pushes / halo wait inside the producers
+        int band_rows = -1;        // SYM SpMV tile order: rows per band-plane (-1 auto, 0 off)
         int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
@@ -308,7 +311,7 @@ static void free_part(Part &p) {
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
                     p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha,
-                    p.d_comm,      p.d_comm_ptrs, p.d_nbr_rank};
+                    p.d_comm,      p.d_comm_ptrs, p.d_nbr_rank, p.d_tile_order};
     for (void *q : p.ipc_opened) cudaIpcCloseMemHandle(q);
     for (void *b : bufs)
         if (b) cudaFree(b);
@@ -908,6 +911,7 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"cluster_dd", &c->opt.cluster_dd, 0, 1},
         {"device_comm", &c->opt.device_comm, -1, 1},
         {"fold_comm", &c->opt.fold_comm, 0, 1},
+        {"band_rows", &c->opt.band_rows, -1, 1 << 30},
         {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
     };
     for (auto &t : table) {
@@ -1072,10 +1076,52 @@ static Matrix matrix_of(const minife_ctx *c, const Part &p) {
     return m;
 }
 
+// SYM SpMV tile order: a row's plane-back mirrors (its dz = -1 runs) come from
+// the row one plane earlier, which the SpMV streamed ~one plane of tiles ago; past ~14 MB of
+// matrix per plane (400^3: 24 MB) part of them is evicted from L2 before it is read again
+// (400^3 read 11-14 % above the algorithmic bytes).  With planes larger than ~1.25 x
+// `band_rows` rows the tiles are visited band-major: y-bands of B = band_rows / N0 lines,
+// each swept plane by plane, so the plane-back rows are B lines back instead of a plane.
+static constexpr int64_t BAND_ROWS_AUTO = 98304;
+static int build_tile_order(minife_ctx *c, Part &p) {
+    DevGuard g(p.dev);
+    dfree(p, p.d_tile_order, (size_t)p.tile_order_n);
+    p.tile_order_n = 0;
+    if (c->fmt != MINIFE_FMT_SYM) return MINIFE_OK;
+    const int64_t N0 = p.plan.ext_n[0], N1 = p.plan.ext_n[1];
+    const int64_t P = N0 * N1;
+    const int64_t target = c->opt.band_rows < 0 ? BAND_ROWS_AUTO : c->opt.band_rows;
+    if (target == 0 || P <= target + target / 4) return MINIFE_OK;
+    const int64_t B = std::max<int64_t>(8, target / N0);               // lines per band
+    const int64_t nslices = (p.ncols + 31) / 32;
+    const int64_t ntiles = (nslices + SYMM_NW - 1) / SYMM_NW;
+    std::vector<std::pair<int64_t, int32_t>> key(ntiles);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t r = t * SYMM_NW * 32;
+        const int64_t ey = (r / N0) % N1, ez = r / P;
+        key[t] = {(ey / B) * (int64_t)1e12 + ez * (int64_t)1e6 + 0, (int32_t)t};
+    }
+    std::stable_sort(key.begin(), key.end(),
+                     [](const std::pair<int64_t, int32_t> &x, const std::pair<int64_t, int32_t> &y) {
+                         return x.first < y.first;
+                     });
+    std::vector<int32_t> order(ntiles);
+    for (int64_t t = 0; t < ntiles; ++t) order[t] = key[t].second;
+    TRY(dalloc(c, p, &p.d_tile_order, (size_t)ntiles));
+    p.tile_order_n = ntiles;
+    CUDA_TRY(c, cudaMemcpy(p.d_tile_order, order.data(), 4 * (size_t)ntiles, cudaMemcpyHostToDevice));
+    return MINIFE_OK;
+}
+
 extern "C" int minife_assemble(minife_ctx *c) {
     if (!c) return MINIFE_EINVAL;
     // CRS sizes its arrays from a device pass read back to the host: its time is host-split
     const bool timed = c->fmt != MINIFE_FMT_CRS;
+    for (auto &p : c->parts) TRY(build_tile_order(c, p));   // (legacy-stream copy: before the
+    for (auto &p : c->parts) {                               //  kernels on the part streams)
+        DevGuard g(p.dev);
+        CUDA_TRY(c, cudaDeviceSynchronize());
+    }
     if (timed) TRY(mark_parts(c, false, true));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1334,6 +1380,7 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     a.x_prefetch = xpf >= 0 ? xpf : (8.0 * (double)p.ncols > 64e6 ? 1 : 0);
     a.sym_kernel = c->opt.sym_kernel;
     a.impl = c->opt.spmv_impl;
+    a.tile_order = c->fmt == MINIFE_FMT_SYM ? p.d_tile_order : nullptr;
     return a;
 }
 

@@ -1181,7 +1181,8 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             else
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
             int64_t i = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
+                const int64_t tile = a.tile_order ? (int64_t)a.tile_order[tau] : tau;
                 const int st = (int)(i % NST);
                 if (i >= NST) mbar_wait(&empty_bar[st], (uint32_t)(((i / NST) & 1) ^ 1));
                 const int64_t s0 = tile * NW;
@@ -1197,8 +1198,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                     // the run starts and masks of the tile this stage takes next: into L2
                     // now, so that stage's first barrier completes at L2 latency (large
                     // problems; 300^3 -0.7 % per iteration, 100^3 +0.7 %)
-                    const int64_t s2 = s0 + (int64_t)NST * gridDim.x * NW;
-                    if (s2 < m.nslices) {
+                    const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
+                    const int64_t s2 =
+                        (a.tile_order && tau2 < ntiles ? (int64_t)a.tile_order[tau2] : tau2) * NW;
+                    if (tau2 < ntiles && s2 < m.nslices) {
                         const int64_t r2 = m.nslices - s2;
                         const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
@@ -1238,7 +1241,8 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
         for (int g = 0; g < 5; ++g)
             madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
         int64_t i = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
+            const int64_t tile = a.tile_order ? (int64_t)a.tile_order[tau] : tau;
             const int st = (int)(i % NST);
             mbar_wait(&full_bar[st], (uint32_t)((i / NST) & 1));
             const int64_t s = tile * NW + warp;
@@ -2803,7 +2807,7 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
     // 300^3: 1.196 ms per CG iteration vs 1.243 with L1 mirror gathers, profiles/r01/session2);
     // the ctx option "sym_kernel" = 0 (or no tensor-map support) selects the L1-gather kernel
     if (a.sym_kernel != 0) {
-        const cudaError_t e = launch_symm<DOT, 13, 2>(a, s);
+        const cudaError_t e = launch_symm<DOT, SYMM_NW, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
         static bool warned = false;
         if (!warned) {

@@ -129,6 +129,7 @@ struct SpmvArgs {
     int val_evict_first;                // SYMM: stream the values evict-first in L2
     int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
     int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
+    const int32_t *tile_order;          // SYMM: tile visited at position tau (null: tau itself)
     int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]
@@ -260,6 +261,9 @@ cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *c
 // occupancy-derived grid sizes
 int spmv_grid(int64_t nslices, int fmt);
 int stream_grid(int64_t rows);
+
+// SYMM kernel tile: SYMM_NW slices of 32 rows (the unit of SpmvArgs::tile_order)
+constexpr int SYMM_NW = 13;
 
 constexpr int SPMV_THREADS = 256;
 constexpr int UPD_THREADS = 256;
