@@ -213,6 +213,10 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *                     CTA of the SpMV / r update / init kernels and the halo wait in the
  *                     last CTA of the p update (4 launches per iteration); 0 separate
  *                     k_acc_push / k_halo_wait launches (7)
+ *   "band_rows"       SYM SpMV tile order, applied at the next minife_assemble: -1 (default)
+ *                     band-major (y-bands of 65536 / N_x lines swept plane by plane) for
+ *                     planes of more than 122880 rows (400^3), natural order otherwise;
+ *                     0 natural order; n > 0 bands of n / N_x lines wherever planes exceed n
  *   "comm_timeout_ms" device comm: how long a kernel waits for a peer's flag before the
  *                     solve fails with MINIFE_ECOMM (default 60000)
  * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,

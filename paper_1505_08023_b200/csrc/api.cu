@@ -1079,10 +1079,13 @@ static Matrix matrix_of(const minife_ctx *c, const Part &p) {
 // SYM SpMV tile order: a row's plane-back mirrors (its dz = -1 runs) come from
 // the row one plane earlier, which the SpMV streamed ~one plane of tiles ago; past ~14 MB of
 // matrix per plane (400^3: 24 MB) part of them is evicted from L2 before it is read again
-// (400^3 read 11-14 % above the algorithmic bytes).  With planes larger than ~1.25 x
-// `band_rows` rows the tiles are visited band-major: y-bands of B = band_rows / N0 lines,
-// each swept plane by plane, so the plane-back rows are B lines back instead of a plane.
-static constexpr int64_t BAND_ROWS_AUTO = 98304;
+// (400^3 read 8-15 % above the algorithmic bytes).  Planes of more than BAND_MIN_PLANE rows
+// are visited band-major: y-bands of B = band_rows / N0 lines, each swept plane by plane, so
+// the plane-back rows are B lines back instead of a plane.  B200, interleaved A/B
+// (profiles/r02/ab): 400^3 band_rows 65536 SpMV 1.82 vs 1.89 ms, DRAM reads 10.37 vs
+// 10.8-11.6 GB (algorithmic 10.0), 49152 / 98304 / 131072 worse; 300^3 (90.6K-row planes)
+// is 10 % SLOWER banded at any band size with the same DRAM bytes, so it stays natural.
+static constexpr int64_t BAND_ROWS_AUTO = 65536, BAND_MIN_PLANE = 122880;
 static int build_tile_order(minife_ctx *c, Part &p) {
     DevGuard g(p.dev);
     dfree(p, p.d_tile_order, (size_t)p.tile_order_n);
@@ -1091,7 +1094,8 @@ static int build_tile_order(minife_ctx *c, Part &p) {
     const int64_t N0 = p.plan.ext_n[0], N1 = p.plan.ext_n[1];
     const int64_t P = N0 * N1;
     const int64_t target = c->opt.band_rows < 0 ? BAND_ROWS_AUTO : c->opt.band_rows;
-    if (target == 0 || P <= target + target / 4) return MINIFE_OK;
+    if (target == 0 || (c->opt.band_rows < 0 && P <= BAND_MIN_PLANE) || P <= target)
+        return MINIFE_OK;
     const int64_t B = std::max<int64_t>(8, target / N0);               // lines per band
     const int64_t nslices = (p.ncols + 31) / 32;
     const int64_t ntiles = (nslices + SYMM_NW - 1) / SYMM_NW;
