@@ -202,6 +202,7 @@ struct minife_ctx {
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
     int cur_max_iters = 0;                       // max_iters of the solve being enqueued
+    int ring_exported = 1;                       // RANK device comm: ring buffers mapped by peers
     double last_asm_ms = 0.0, last_solve_ms = 0.0;   // device time, max over the parts
     std::vector<cudaGraphExec_t> gexec_parts;    // MULTI + device comm: one graph per device
     // kernel launch accounting: enq_kernels counts launch_* calls as they are enqueued (into a
@@ -438,10 +439,13 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
 template <class RemoteP>
 static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
     const size_t ns = p.plan.send_idx.size();
+    const size_t nn = p.plan.nbr.size();
     std::vector<uint8_t> nb(ns);
     std::vector<int32_t> dst(ns);
-    std::vector<double *> ptr(p.plan.nbr.size());
-    for (size_t k = 0; k < p.plan.nbr.size(); ++k) {
+    // slot-major: entry [s][k] = neighbour k's ring buffer s (s = 0: its p; the deferred-x
+    // scheme's p_k lives in ring[(k - 1) % X]); null where that buffer does not exist
+    std::vector<double *> ptr(XDEF_MAX * nn, nullptr);
+    for (size_t k = 0; k < nn; ++k) {
         const int qr = p.plan.nbr[k];
         Plan qown;
         const Plan *qp = nullptr;
@@ -463,7 +467,7 @@ static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
             nb[p.plan.send_off[k] + j] = (uint8_t)k;
             dst[p.plan.send_off[k] + j] = (int32_t)q.ext_pos[q.recv_off[kq] + j];
         }
-        ptr[k] = remote_p(qr);
+        for (int s = 0; s < XDEF_MAX; ++s) ptr[s * nn + k] = remote_p(qr, s);
     }
     DevGuard g(p.dev);
     if (!p.d_push_nbr) {
@@ -485,7 +489,7 @@ static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
 
 static int setup_push(minife_ctx *c) {
     for (auto &p : c->parts)
-        TRY(build_push_tables(c, p, [c](int qr) { return c->parts[qr].d_p; }));
+        TRY(build_push_tables(c, p, [c](int qr, int s) { return c->parts[qr].ring(s); }));
     c->push_ready = true;
     return MINIFE_OK;
 }
@@ -536,8 +540,8 @@ static int setup_devcomm_local(minife_ctx *c) {
 // all-reduce) whether every mapping succeeded: if any rank failed (no P2P between some pair,
 // IPC unavailable), all of them keep the NCCL transport.  Collective over the ranks.
 struct IpcRecord {
-    cudaIpcMemHandle_t comm, p;
-    int32_t dev, ok;
+    cudaIpcMemHandle_t comm, p[XDEF_MAX];   // p[s] = ring buffer s (s = 0: p itself)
+    int32_t dev, ok, nring;
 };
 
 static int setup_devcomm_ipc(minife_ctx *c) {
@@ -545,10 +549,21 @@ static int setup_devcomm_ipc(minife_ctx *c) {
     DevGuard g(p.dev);
     TRY(alloc_comm_regions(c));
     const int W = c->world, R = c->rank;
+    // the deferred-x ring where it would be on: neighbours push p_(k+1)'s halo
+    // straight into the ring buffer it lives in, so every buffer is exported now
+    const int nring = (W > 1 && 40.0 * (double)p.ncols >= 64e6) ? XDEF_MAX : 1;
+    if (nring > 1) {
+        if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
+        for (int s = 2; s < nring; ++s)
+            if (!p.d_pr[s]) TRY(alloc_colvec(c, p, &p.d_pr[s]));
+        CUDA_TRY(c, cudaDeviceSynchronize());
+    }
     IpcRecord mine{};
     mine.dev = p.dev;
-    mine.ok = cudaIpcGetMemHandle(&mine.comm, p.d_comm) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.p, p.d_p) == cudaSuccess;
+    mine.nring = nring;
+    mine.ok = cudaIpcGetMemHandle(&mine.comm, p.d_comm) == cudaSuccess;
+    for (int s = 0; s < nring && mine.ok; ++s)
+        mine.ok = cudaIpcGetMemHandle(&mine.p[s], p.ring(s)) == cudaSuccess;
     cudaGetLastError();
     std::vector<IpcRecord> all(W);
     IpcRecord *d_all = nullptr;
@@ -571,15 +586,16 @@ static int setup_devcomm_ipc(minife_ctx *c) {
     }
     // map every other rank's region, and the neighbors' p arrays
     std::vector<unsigned long long *> regions(W, nullptr);
-    std::vector<double *> remote_p(W, nullptr);
+    std::vector<double *> remote_p((size_t)W * XDEF_MAX, nullptr);     // [rank][ring slot]
     int32_t ok = st == MINIFE_OK ? 1 : 0;
     for (int r = 0; r < W && ok; ++r) {
         if (!all[r].ok) ok = 0;
         if (r == R) {
             regions[r] = p.d_comm;
-            remote_p[r] = p.d_p;
+            for (int s = 0; s < nring; ++s) remote_p[(size_t)r * XDEF_MAX + s] = p.ring(s);
             continue;
         }
+        if (all[r].nring != nring) ok = 0;
         int can = 0;
         if (cudaDeviceCanAccessPeer(&can, p.dev, all[r].dev) != cudaSuccess || !can) ok = 0;
         void *q = nullptr;
@@ -591,11 +607,14 @@ static int setup_devcomm_ipc(minife_ctx *c) {
             ok = 0;
         }
         if (ok && std::binary_search(p.plan.nbr.begin(), p.plan.nbr.end(), r)) {
-            if (cudaIpcOpenMemHandle(&q, all[r].p, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
-                p.ipc_opened.push_back(q);
-                remote_p[r] = (double *)q;
-            } else {
-                ok = 0;
+            for (int s = 0; s < nring && ok; ++s) {
+                if (cudaIpcOpenMemHandle(&q, all[r].p[s], cudaIpcMemLazyEnablePeerAccess) ==
+                    cudaSuccess) {
+                    p.ipc_opened.push_back(q);
+                    remote_p[(size_t)r * XDEF_MAX + s] = (double *)q;
+                } else {
+                    ok = 0;
+                }
             }
         }
         cudaGetLastError();
@@ -624,8 +643,11 @@ static int setup_devcomm_ipc(minife_ctx *c) {
         return MINIFE_OK;
     }
     TRY(setup_comm_tables(c, [&regions](Part &, int r) { return regions[r]; }));
+    c->ring_exported = nring;
     if (W > 1) {
-        TRY(build_push_tables(c, p, [&remote_p](int qr) { return remote_p[qr]; }));
+        TRY(build_push_tables(c, p, [&remote_p](int qr, int s) {
+            return remote_p[(size_t)qr * XDEF_MAX + s];
+        }));
         c->push_ready = true;
     }
     c->devcomm_ready = true;
@@ -1200,14 +1222,22 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // Push the halo of p (mode 0: current p; mode 1: p_(k+1) ahead of K7) from every part, then
 // (MULTI) make every part's compute stream wait for its neighbors' pushes.  With mode 1 the
 // waits are placed by the caller after K7 (wait_now = false).
-static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now) {
+static int xdef_of(const minife_ctx *c);
+static double *x2_pbuf(const minife_ctx *c, const Part &p, int k);
+static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now, bool ring = false) {
+    // ring = the deferred-x sequence: p_k lives in ring((k - 1) % X); the pushed values go to
+    // the receiver's buffer of the p they belong to (mode 1: p_(k+1); mode 0 at k = 0: p_1)
+    const int X = ring ? xdef_of(c) : 0;
+    const int slot = X ? (mode == 1 ? k % X : (k > 0 ? (k - 1) % X : 0)) : 0;
     for (auto &p : c->parts) {
         const int64_t n = (int64_t)p.plan.send_idx.size();
         if (!n) continue;
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 1);           // acc_in = rr_k (mode 1), p, r, rr, st, dc
+        if (X && k > 0) a.p = x2_pbuf(c, p, k);  // p_k
         LAUNCH(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr, p.d_push_dst,
-                              p.d_push_ptr, n, launch_stream(c, p)));
+                              p.d_push_ptr + (size_t)slot * p.plan.nbr.size(), n,
+                              launch_stream(c, p)));
         if (c->mode == MINIFE_MODE_MULTI && !devcomm(c))
             CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
     }
@@ -1651,9 +1681,18 @@ static int xdef_of(const minife_ctx *c) {
     // partitioned (SYM with a halo, halo overlapped with K7 over the wire or device copies):
     // the exchange fills the halo of the buffer p_(k+1) goes to
     const bool single = c->parts.size() == 1 && c->world == 1;
-    const bool parts_ok = overlap_sym(c) && !push_mode(c);
+    // (device comm: the halo of p_(k+1) is pushed into the ring buffer it belongs to; RANK ctxs
+    // only as deep as the ring exported at creation)
+    const bool parts_ok = overlap_sym(c) && (!push_mode(c) || devcomm(c));
+    if (devcomm(c) && c->mode == MINIFE_MODE_RANK && c->world > 1 && c->ring_exported < 2)
+        return 0;
     if (!env || env == 1 || !(single || parts_ok) || fused_mode(c)) return 0;
-    if (env >= 2) return std::min(env, XDEF_MAX);
+    if (env >= 2) {
+        const int X = std::min(env, XDEF_MAX);
+        if (devcomm(c) && c->mode == MINIFE_MODE_RANK && c->world > 1 && X > c->ring_exported)
+            return 0;
+        return X;
+    }
     return 40.0 * (double)c->parts[0].ncols >= 64e6 ? XDEF_DEFAULT : 0;
 }
 static bool x2_mode(const minife_ctx *c) { return xdef_of(c) > 0; }
@@ -1661,12 +1700,21 @@ static bool x2_mode(const minife_ctx *c) { return xdef_of(c) > 0; }
 static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
     if (!(fused_mode(c) || x2_mode(c))) return MINIFE_OK;
     const int X = std::max(2, xdef_of(c));
+    bool fresh = false;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
+        if (!p.d_p2) {
+            TRY(alloc_colvec(c, p, &p.d_p2));
+            fresh = true;
+        }
         for (int i = 2; i < X; ++i)
-            if (!p.d_pr[i]) TRY(alloc_colvec(c, p, &p.d_pr[i]));
+            if (!p.d_pr[i]) {
+                TRY(alloc_colvec(c, p, &p.d_pr[i]));
+                fresh = true;
+            }
     }
+    // one-process ctxs push into the peers' ring buffers directly: refresh the tables
+    if (fresh && c->push_ready && c->mode != MINIFE_MODE_RANK) TRY(setup_push(c));
     return MINIFE_OK;
 }
 
@@ -1705,21 +1753,44 @@ static void set_ring(const minife_ctx *c, const Part &p, UpdArgs &u) {
 static int enqueue_iteration_x2(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
     const bool halo = c->parts.size() > 1 || c->world > 1;
+    const bool dev = devcomm(c), fold = fold_comm(c);
+    const bool last = k == c->cur_max_iters;
     TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        LAUNCH(c, launch_spmv(spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true), true, p.grid_spmv,
-                                launch_stream(c, p)));
+        SpmvArgs sa = spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true);
+        if (fold) {                                  // the SpMV's last CTA pushes pAp_k
+            sa.dc = upd_args(c, p, 0).dc;
+            sa.fold_push = 1;
+            sa.k = k;
+        }
+        LAUNCH(c, launch_spmv(sa, true, p.grid_spmv, launch_stream(c, p)));
     }
     TRY(tw_mark(c, k, true));
-    TRY(enqueue_allreduce(c, 0, k));
+    if (!fold) TRY(enqueue_allreduce(c, 0, k));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs u6 = upd_args(c, p, 0);
         u6.alpha_hist = p.d_alpha;
+        u6.fold_push = fold ? 1 : 0;
         LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
     }
-    TRY(enqueue_allreduce(c, 1, k));
+    if (!fold) TRY(enqueue_allreduce(c, 1, k));
+    if (halo && dev) {
+        // device comm: p_(k+1) at the send slots straight into the receivers' ring buffer of
+        // p_(k+1), then K7 (whose last CTA waits for the neighbours' pushes when folded)
+        if (!last) TRY(enqueue_push(c, k, 1, false, true));
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs u7 = upd_args(c, p, 1);
+            u7.alpha_hist = p.d_alpha;
+            set_ring(c, p, u7);
+            if (fold && !last && !p.plan.nbr.empty()) u7.fold_wait_k = k + 1;
+            LAUNCH(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1), p.grid_upd,
+                                       launch_stream(c, p)));
+        }
+        return (last || fold) ? MINIFE_OK : push_wait(c, k + 1);
+    }
     if (halo) {
         // as enqueue_k7_with_halo: the send slots' p_(k+1) ahead of K7, exchanged on the
         // transport stream into the halo of the buffer p_(k+1) goes to, while K7 runs
@@ -1766,8 +1837,10 @@ static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t
     c->cur_max_iters = max_iters;
     if (!t && x2_mode(c) && !small_mode(c)) {
         TRY(enqueue_init(c, tol));
-        if (c->parts.size() > 1 || c->world > 1)      // halo of p_1 = b (buffer of odd k)
-            TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+        if (c->parts.size() > 1 || c->world > 1) {    // halo of p_1 = b (buffer of odd k)
+            if (devcomm(c)) TRY(enqueue_push(c, 0, 0, true, true));
+            else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+        }
         for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration_x2(c, k));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);

@@ -2172,6 +2172,9 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
                 }
             }
         }
+        // device comm: the last CTA waits for the neighbours' halo of p_(k+1) (as k_update_p)
+        if (a.fold_wait_k > 0 && !stop)
+            halo_wait_last_cta(a.dc, a.fold_wait_k, a.st, a.dc.local + 5);
         return;
     }
     const int64_t rows = a.g.rows, n2 = rows >> 1;

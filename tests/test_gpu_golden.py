@@ -141,6 +141,15 @@ def test_weak_scaling_600x300x300():
         check(g, gold)
 
 
+def test_weak_scaling_600x300x300_device_protocol():
+    """configs[4] at 2 GPUs through the device-initiated protocol of MULTI/RANK ctxs (halo
+    pushed into the deferred-x ring, in-kernel reductions), on one GPU as 2 virtual parts."""
+    gold = load((600, 300, 300))
+    with M.Minife(600, 300, 300, virtual=2) as g:
+        g.set_transport(M.TRANSPORT_DEVICE)
+        check(g, gold, matrix=False)
+
+
 def test_weak_scaling_600x600x300():
     """configs[4] at 4 GPUs: 600x600x300 in 4 RCB parts."""
     gold = load((600, 600, 300))

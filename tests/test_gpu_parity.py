@@ -316,6 +316,25 @@ def test_device_comm_launch_count_has_no_host_collective(fold):
             assert launched == p * (5 + 7 * 50 - 2)
 
 
+@pytest.mark.parametrize("fold", [1, 0])
+@pytest.mark.parametrize("xdef", [2, 5, 8])
+@pytest.mark.parametrize("n,p", [((23, 17, 9), 3), ((12, 11, 10), 8), ((40, 8, 6), 2)])
+def test_device_comm_deferred_x_bit_identical(n, p, xdef, fold):
+    """The device protocol with the deferred-x ring (halo of p_(k+1) pushed into the ring
+    buffer it lives in): 200 iterations, a tolerance stop and an odd count -- bitwise the
+    oracle."""
+    s = oracle_system(n)
+    with M.Minife(*n, virtual=p, options={"x_defer": xdef, "fold_comm": fold}) as g:
+        g.set_transport(M.TRANSPORT_DEVICE)
+        g.assemble()
+        for iters, tol in ((200, 0.0), (200, 1e-8), (7, 0.0)):
+            r = g.cg_solve(iters, tol)
+            o = oracle_cg(n, iters, tol)
+            assert (r.status, r.iterations, r.converged) == (o.status, o.iters, o.converged)
+            assert _same(g.history(), o.hist)
+            assert _same(g.solution(), o.x)
+
+
 @pytest.mark.parametrize("fmt", ALL_FORMATS)
 @pytest.mark.parametrize("n,p", [((10, 10, 10), 2), ((23, 17, 9), 3), ((12, 11, 10), 8)])
 def test_device_comm_unfolded_bit_identical(n, p, fmt):
