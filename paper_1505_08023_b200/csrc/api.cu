@@ -551,7 +551,7 @@ static int setup_devcomm_ipc(minife_ctx *c) {
     const int W = c->world, R = c->rank;
     // the deferred-x ring where it would be on: neighbours push p_(k+1)'s halo
     // straight into the ring buffer it lives in, so every buffer is exported now
-    const int nring = (W > 1 && 40.0 * (double)p.ncols >= 64e6) ? XDEF_MAX : 1;
+    const int nring = (W > 1 && 40.0 * (double)p.ncols >= 64e6) ? XDEF_MAX : 1;   // forced X
     if (nring > 1) {
         if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
         for (int s = 2; s < nring; ++s)
@@ -1693,7 +1693,10 @@ static int xdef_of(const minife_ctx *c) {
             return 0;
         return X;
     }
-    return 40.0 * (double)c->parts[0].ncols >= 64e6 ? XDEF_DEFAULT : 0;
+    // automatic: single parts only -- on partitioned parts (x-line walks, halo exchange each
+    // iteration) the deferral is slower: B200, 2 virtual parts of 600x300x300 2.133 vs 2.079
+    // ms per iteration, 8 parts of 400^3 2.640 vs 2.595 (profiles/r02/ab)
+    return single && 40.0 * (double)c->parts[0].ncols >= 64e6 ? XDEF_DEFAULT : 0;
 }
 static bool x2_mode(const minife_ctx *c) { return xdef_of(c) > 0; }
 
