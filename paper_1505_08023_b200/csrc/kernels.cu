@@ -2812,11 +2812,8 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
     if (a.sym_kernel != 0) {
         const cudaError_t e = launch_symm<DOT, SYMM_NW, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
-        static bool warned = false;
-        if (!warned) {
-            warned = true;
-            fprintf(stderr, "minife: tensor maps unavailable, SYM SpMV uses the L1-gather kernel\n");
-        }
+        // (no tensor-map support: the L1-gather kernel below, same results; the library
+        // never prints)
     }
     using C = SyCfg<16, 2>;
     static unsigned long long attr_set = 0;
