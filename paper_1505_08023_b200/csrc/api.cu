@@ -122,6 +122,11 @@ struct Part {
     // device-initiated comm (DevComm, kernels.h): this part's comm region, the table of every
     // rank's region as seen from this device, the neighbor ranks; RANK: CUDA-IPC mappings of
     // the other ranks' regions and p arrays (closed on destroy)
+    // device comm, halo by r: this part's r-halo receive buffer [externals] (slot order), per
+    // send slot the receiver's slot index, per neighbour its r-halo buffer as seen from here
+    double *d_rhalo = nullptr;
+    int32_t *d_rdst = nullptr;
+    double **d_rhalo_ptr = nullptr;
     int32_t *d_tile_order = nullptr;              // SYM SpMV: band-major tile order (or null)
     int64_t tile_order_n = 0;
     unsigned long long *d_comm = nullptr;
@@ -202,7 +207,6 @@ struct minife_ctx {
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
     int cur_max_iters = 0;                       // max_iters of the solve being enqueued
-    int ring_exported = 1;                       // RANK device comm: ring buffers mapped by peers
     double last_asm_ms = 0.0, last_solve_ms = 0.0;   // device time, max over the parts
     std::vector<cudaGraphExec_t> gexec_parts;    // MULTI + device comm: one graph per device
     // kernel launch accounting: enq_kernels counts launch_* calls as they are enqueued (into a
@@ -312,7 +316,8 @@ static void free_part(Part &p) {
                     p.d_acc,       p.d_st,      p.d_hist,    p.d_rr,       p.d_send_col,
                     p.d_recv_pos,  p.d_sendbuf, p.d_recvbuf, p.d_slice_row, p.d_slice_pos,
                     p.d_send_row,  p.d_push_nbr, p.d_push_dst, p.d_push_ptr, p.d_alpha,
-                    p.d_comm,      p.d_comm_ptrs, p.d_nbr_rank, p.d_tile_order};
+                    p.d_comm,      p.d_comm_ptrs, p.d_nbr_rank, p.d_tile_order, p.d_rhalo,
+                    p.d_rdst,      p.d_rhalo_ptr};
     for (void *q : p.ipc_opened) cudaIpcCloseMemHandle(q);
     for (void *b : bufs)
         if (b) cudaFree(b);
@@ -494,6 +499,46 @@ static int setup_push(minife_ctx *c) {
     return MINIFE_OK;
 }
 
+// Halo by r (device comm): part p's send slot j for neighbour q lands in q's r-halo slot
+// recv_off_q[p] + j; rhalo_of(q) = q's r-halo buffer as seen from p's device.
+template <class RhaloOf>
+static int build_rhalo_tables(minife_ctx *c, Part &p, RhaloOf rhalo_of) {
+    const size_t ns = p.plan.send_idx.size(), nn = p.plan.nbr.size();
+    std::vector<uint8_t> nb(ns);
+    std::vector<int32_t> dst(ns);
+    std::vector<double *> ptr(nn);
+    for (size_t k = 0; k < nn; ++k) {
+        const int qr = p.plan.nbr[k];
+        Plan qown;
+        if (!build_plan(c->mesh, c->world, qr, qown)) return MINIFE_ESTATE;
+        auto it = std::lower_bound(qown.nbr.begin(), qown.nbr.end(), p.plan.rank);
+        const size_t kq = (size_t)(it - qown.nbr.begin());
+        if (kq >= qown.nbr.size() || qown.nbr[kq] != p.plan.rank ||
+            qown.recv_cnt[kq] != p.plan.send_cnt[k] || k > 255) {
+            set_err(c, "halo plan mismatch between parts %d and %d", p.plan.rank, qr);
+            return MINIFE_ESTATE;
+        }
+        for (int64_t j = 0; j < p.plan.send_cnt[k]; ++j) {
+            nb[p.plan.send_off[k] + j] = (uint8_t)k;
+            dst[p.plan.send_off[k] + j] = (int32_t)(qown.recv_off[kq] + j);
+        }
+        ptr[k] = rhalo_of(qr);
+    }
+    DevGuard g(p.dev);
+    if (!p.d_push_nbr) TRY(dalloc(c, p, &p.d_push_nbr, ns));
+    if (!p.d_rdst) TRY(dalloc(c, p, &p.d_rdst, ns));
+    if (!p.d_rhalo_ptr) TRY(dalloc(c, p, &p.d_rhalo_ptr, nn));
+    if (ns) {
+        CUDA_TRY(c, cudaMemcpy(p.d_push_nbr, nb.data(), ns, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaMemcpy(p.d_rdst, dst.data(), 4 * ns, cudaMemcpyHostToDevice));
+    }
+    if (nn)
+        CUDA_TRY(c, cudaMemcpy(p.d_rhalo_ptr, ptr.data(), sizeof(double *) * nn,
+                               cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    return MINIFE_OK;
+}
+
 // Device comm regions (DevComm, kernels.h) of every part of this ctx, zeroed, plus the
 // neighbor-rank lists; `region_of(p, r)` = rank r's region as seen from part p's device.
 template <class RegionOf>
@@ -519,6 +564,10 @@ static int alloc_comm_regions(minife_ctx *c) {
     const int64_t words = comm_words(c->world);
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
+        if (!p.d_rhalo) {
+            TRY(dalloc(c, p, &p.d_rhalo, (size_t)p.plan.n_ext));
+            CUDA_TRY(c, cudaMemset(p.d_rhalo, 0, 8 * (size_t)std::max<int64_t>(1, p.plan.n_ext)));
+        }
         if (!p.d_comm) TRY(dalloc(c, p, &p.d_comm, words));
         CUDA_TRY(c, cudaMemset(p.d_comm, 0, 8 * (size_t)words));
         CUDA_TRY(c, cudaDeviceSynchronize());
@@ -530,18 +579,20 @@ static int alloc_comm_regions(minife_ctx *c) {
 static int setup_devcomm_local(minife_ctx *c) {
     TRY(alloc_comm_regions(c));
     TRY(setup_comm_tables(c, [c](Part &, int r) { return c->parts[r].d_comm; }));
+    for (auto &p : c->parts)
+        TRY(build_rhalo_tables(c, p, [c](int qr) { return c->parts[qr].d_rhalo; }));
     c->devcomm_ready = true;
     return MINIFE_OK;
 }
 
-// RANK ctxs (one process per GPU, torchrun): the comm region and the p array of every rank
-// are exported as CUDA-IPC handles and exchanged once with an NCCL all-gather; each rank maps
-// every other rank's region and its neighbors' p arrays.  The ranks then agree (NCCL MIN
-// all-reduce) whether every mapping succeeded: if any rank failed (no P2P between some pair,
-// IPC unavailable), all of them keep the NCCL transport.  Collective over the ranks.
+// RANK ctxs (one process per GPU, torchrun): the comm region and the r-halo buffer of every
+// rank are exported as CUDA-IPC handles and exchanged once with an NCCL all-gather; each rank
+// maps every other rank's region and its neighbours' r-halo buffers.  The ranks then agree
+// (NCCL MIN all-reduce) whether every mapping succeeded: if any rank failed (no P2P between
+// some pair, IPC unavailable), all of them keep the NCCL transport.  Collective over the ranks.
 struct IpcRecord {
-    cudaIpcMemHandle_t comm, p[XDEF_MAX];   // p[s] = ring buffer s (s = 0: p itself)
-    int32_t dev, ok, nring;
+    cudaIpcMemHandle_t comm, rhalo;
+    int32_t dev, ok;
 };
 
 static int setup_devcomm_ipc(minife_ctx *c) {
@@ -549,21 +600,10 @@ static int setup_devcomm_ipc(minife_ctx *c) {
     DevGuard g(p.dev);
     TRY(alloc_comm_regions(c));
     const int W = c->world, R = c->rank;
-    // the deferred-x ring where it would be on: neighbours push p_(k+1)'s halo
-    // straight into the ring buffer it lives in, so every buffer is exported now
-    const int nring = (W > 1 && 40.0 * (double)p.ncols >= 64e6) ? XDEF_MAX : 1;   // forced X
-    if (nring > 1) {
-        if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
-        for (int s = 2; s < nring; ++s)
-            if (!p.d_pr[s]) TRY(alloc_colvec(c, p, &p.d_pr[s]));
-        CUDA_TRY(c, cudaDeviceSynchronize());
-    }
     IpcRecord mine{};
     mine.dev = p.dev;
-    mine.nring = nring;
-    mine.ok = cudaIpcGetMemHandle(&mine.comm, p.d_comm) == cudaSuccess;
-    for (int s = 0; s < nring && mine.ok; ++s)
-        mine.ok = cudaIpcGetMemHandle(&mine.p[s], p.ring(s)) == cudaSuccess;
+    mine.ok = cudaIpcGetMemHandle(&mine.comm, p.d_comm) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.rhalo, p.d_rhalo) == cudaSuccess;
     cudaGetLastError();
     std::vector<IpcRecord> all(W);
     IpcRecord *d_all = nullptr;
@@ -584,18 +624,17 @@ static int setup_devcomm_ipc(minife_ctx *c) {
                 nccl()->GetErrorString(nr));
         st = e != cudaSuccess ? MINIFE_ECUDA : MINIFE_ENCCL;
     }
-    // map every other rank's region, and the neighbors' p arrays
+    // map every other rank's region, and the neighbours' r-halo buffers
     std::vector<unsigned long long *> regions(W, nullptr);
-    std::vector<double *> remote_p((size_t)W * XDEF_MAX, nullptr);     // [rank][ring slot]
+    std::vector<double *> rhalo(W, nullptr);
     int32_t ok = st == MINIFE_OK ? 1 : 0;
     for (int r = 0; r < W && ok; ++r) {
         if (!all[r].ok) ok = 0;
         if (r == R) {
             regions[r] = p.d_comm;
-            for (int s = 0; s < nring; ++s) remote_p[(size_t)r * XDEF_MAX + s] = p.ring(s);
+            rhalo[r] = p.d_rhalo;
             continue;
         }
-        if (all[r].nring != nring) ok = 0;
         int can = 0;
         if (cudaDeviceCanAccessPeer(&can, p.dev, all[r].dev) != cudaSuccess || !can) ok = 0;
         void *q = nullptr;
@@ -607,14 +646,12 @@ static int setup_devcomm_ipc(minife_ctx *c) {
             ok = 0;
         }
         if (ok && std::binary_search(p.plan.nbr.begin(), p.plan.nbr.end(), r)) {
-            for (int s = 0; s < nring && ok; ++s) {
-                if (cudaIpcOpenMemHandle(&q, all[r].p[s], cudaIpcMemLazyEnablePeerAccess) ==
-                    cudaSuccess) {
-                    p.ipc_opened.push_back(q);
-                    remote_p[(size_t)r * XDEF_MAX + s] = (double *)q;
-                } else {
-                    ok = 0;
-                }
+            if (cudaIpcOpenMemHandle(&q, all[r].rhalo, cudaIpcMemLazyEnablePeerAccess) ==
+                cudaSuccess) {
+                p.ipc_opened.push_back(q);
+                rhalo[r] = (double *)q;
+            } else {
+                ok = 0;
             }
         }
         cudaGetLastError();
@@ -643,13 +680,7 @@ static int setup_devcomm_ipc(minife_ctx *c) {
         return MINIFE_OK;
     }
     TRY(setup_comm_tables(c, [&regions](Part &, int r) { return regions[r]; }));
-    c->ring_exported = nring;
-    if (W > 1) {
-        TRY(build_push_tables(c, p, [&remote_p](int qr, int s) {
-            return remote_p[(size_t)qr * XDEF_MAX + s];
-        }));
-        c->push_ready = true;
-    }
+    if (W > 1) TRY(build_rhalo_tables(c, p, [&rhalo](int qr) { return rhalo[qr]; }));
     c->devcomm_ready = true;
     return MINIFE_OK;
 }
@@ -1371,6 +1402,8 @@ static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
     a.x_late = c->opt.x_late;
     a.cl_dd = c->opt.cluster_dd;
     if (devcomm(c)) {
+        a.rhalo = p.d_rhalo;
+        a.halo_col = p.d_recv_pos;
         a.dc.region = p.d_comm_ptrs;
         a.dc.local = p.d_comm;
         a.dc.nbr_rank = p.d_nbr_rank;
@@ -1457,12 +1490,9 @@ static int enqueue_k7_with_halo(minife_ctx *c, int k) {
         if (!last) TRY(enqueue_push(c, k, 1, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            UpdArgs u7 = upd_args(c, p, 1);
-            // device comm: K7's last CTA waits for the neighbours' halo of p_(k+1)
-            if (fold_comm(c) && !last && !p.plan.nbr.empty()) u7.fold_wait_k = k + 1;
-            LAUNCH(c, launch_update_p(u7, k, p.grid_upd, launch_stream(c, p)));
+            LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
         }
-        return (last || fold_comm(c)) ? MINIFE_OK : push_wait(c, k + 1);
+        return last ? MINIFE_OK : push_wait(c, k + 1);
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1507,6 +1537,19 @@ struct PhaseTimer {
     }
 };
 
+// Halo by r (device comm): r_(kp) at every part's send slots into the receivers' r-halo
+// buffers, flags raised by the last CTA (kp = k + 1 after K6(k); kp = 1 at init: r_0 = b)
+static int enqueue_push_r(minife_ctx *c, int kp) {
+    for (auto &p : c->parts) {
+        const int64_t n = (int64_t)p.plan.send_idx.size();
+        if (!n) continue;
+        DevGuard g(p.dev);
+        LAUNCH(c, launch_push_r(upd_args(c, p, 1), kp, p.d_send_row, p.d_push_nbr, p.d_rdst,
+                                p.d_rhalo_ptr, n, launch_stream(c, p)));
+    }
+    return MINIFE_OK;
+}
+
 static int enqueue_init(minife_ctx *c, double tol) {
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1518,6 +1561,7 @@ static int enqueue_init(minife_ctx *c, double tol) {
         LAUNCH(c, launch_init_vectors(a, p.grid_upd, s));
     }
     if (!fold_comm(c)) TRY(enqueue_allreduce(c, 1, 0));
+    if (devcomm(c)) TRY(enqueue_push_r(c, 1));      // r_0 = b at the send slots (p_1's halo)
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
         UpdArgs a = upd_args(c, p, 0);
@@ -1525,6 +1569,14 @@ static int enqueue_init(minife_ctx *c, double tol) {
         a.acc_zero = p.acc_pAp();
         LAUNCH(c, launch_init_finalize(a, tol, launch_stream(c, p)));
     }
+    if (devcomm(c))
+        for (auto &p : c->parts) {                   // p_1's halo columns = r_0's halo
+            if (!p.plan.n_ext) continue;
+            DevGuard g(p.dev);
+            UpdArgs a = upd_args(c, p, 0);
+            a.halo_n = p.plan.n_ext;
+            LAUNCH(c, launch_halo_init(a, launch_stream(c, p)));
+        }
     return MINIFE_OK;
 }
 
@@ -1681,18 +1733,10 @@ static int xdef_of(const minife_ctx *c) {
     // partitioned (SYM with a halo, halo overlapped with K7 over the wire or device copies):
     // the exchange fills the halo of the buffer p_(k+1) goes to
     const bool single = c->parts.size() == 1 && c->world == 1;
-    // (device comm: the halo of p_(k+1) is pushed into the ring buffer it belongs to; RANK ctxs
-    // only as deep as the ring exported at creation)
+    // (device comm: each part completes the halo columns of p_(k+1) in the ring buffer itself)
     const bool parts_ok = overlap_sym(c) && (!push_mode(c) || devcomm(c));
-    if (devcomm(c) && c->mode == MINIFE_MODE_RANK && c->world > 1 && c->ring_exported < 2)
-        return 0;
     if (!env || env == 1 || !(single || parts_ok) || fused_mode(c)) return 0;
-    if (env >= 2) {
-        const int X = std::min(env, XDEF_MAX);
-        if (devcomm(c) && c->mode == MINIFE_MODE_RANK && c->world > 1 && X > c->ring_exported)
-            return 0;
-        return X;
-    }
+    if (env >= 2) return std::min(env, XDEF_MAX);
     // automatic: single parts only -- on partitioned parts (x-line walks, halo exchange each
     // iteration) the deferral is slower: B200, 2 virtual parts of 600x300x300 2.133 vs 2.079
     // ms per iteration, 8 parts of 400^3 2.640 vs 2.595 (profiles/r02/ab)
@@ -1756,8 +1800,7 @@ static void set_ring(const minife_ctx *c, const Part &p, UpdArgs &u) {
 static int enqueue_iteration_x2(minife_ctx *c, int k) {
     const bool virt = c->mode == MINIFE_MODE_VIRTUAL;
     const bool halo = c->parts.size() > 1 || c->world > 1;
-    const bool dev = devcomm(c), fold = fold_comm(c);
-    const bool last = k == c->cur_max_iters;
+    const bool fold = fold_comm(c);
     TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1779,21 +1822,6 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
         LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
     }
     if (!fold) TRY(enqueue_allreduce(c, 1, k));
-    if (halo && dev) {
-        // device comm: p_(k+1) at the send slots straight into the receivers' ring buffer of
-        // p_(k+1), then K7 (whose last CTA waits for the neighbours' pushes when folded)
-        if (!last) TRY(enqueue_push(c, k, 1, false, true));
-        for (auto &p : c->parts) {
-            DevGuard g(p.dev);
-            UpdArgs u7 = upd_args(c, p, 1);
-            u7.alpha_hist = p.d_alpha;
-            set_ring(c, p, u7);
-            if (fold && !last && !p.plan.nbr.empty()) u7.fold_wait_k = k + 1;
-            LAUNCH(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1), p.grid_upd,
-                                       launch_stream(c, p)));
-        }
-        return (last || fold) ? MINIFE_OK : push_wait(c, k + 1);
-    }
     if (halo) {
         // as enqueue_k7_with_halo: the send slots' p_(k+1) ahead of K7, exchanged on the
         // transport stream into the halo of the buffer p_(k+1) goes to, while K7 runs
@@ -1835,14 +1863,80 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
     return MINIFE_OK;
 }
 
+// Device-initiated comm: per iteration SpMV (its last CTA pushes pAp_k) |
+// K6 (its last CTA pushes rr_k) | the halo push of r_(k+1) (needs no reduction result, so it
+// overlaps the rr reduction) | K7, which also completes p_(k+1)'s halo columns from the
+// neighbours' r_(k+1).  With or without the deferred-x ring; profile mode marks the phases.
+static int enqueue_solve_dev(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
+    const int X = t ? 0 : xdef_of(c);
+    const bool fold = fold_comm(c);
+    TRY(enqueue_init(c, tol));
+    if (t) t->mark(-1);
+    for (int k = 1; k <= max_iters; ++k) {
+        const bool last = k == max_iters;
+        if (!t) TRY(tw_mark(c, k, false));
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            SpmvArgs sa = spmv_args(c, p, X ? x2_pbuf(c, p, k) : p.d_p, p.d_Ap, true);
+            if (fold) {                              // the SpMV's last CTA pushes pAp_k
+                sa.dc = upd_args(c, p, 0).dc;
+                sa.fold_push = 1;
+                sa.k = k;
+            }
+            LAUNCH(c, launch_spmv(sa, true, p.grid_spmv, launch_stream(c, p)));
+        }
+        if (!t) TRY(tw_mark(c, k, true));
+        if (t) t->mark(0);
+        if (!fold) TRY(enqueue_allreduce(c, 0, k));
+        if (t) t->mark(3);
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs u6 = upd_args(c, p, 0);
+            if (X) u6.alpha_hist = p.d_alpha;
+            u6.fold_push = fold ? 1 : 0;             // K6's last CTA pushes rr_k
+            LAUNCH(c, launch_update_xr(u6, k, p.grid_upd, launch_stream(c, p)));
+        }
+        if (t) t->mark(1);
+        if (!fold) TRY(enqueue_allreduce(c, 1, k));
+        if (!last) TRY(enqueue_push_r(c, k + 1));
+        if (t) t->mark(3);
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs u7 = upd_args(c, p, 1);
+            if (!last && p.plan.n_ext) {             // p_(k+1)'s halo columns, from r_(k+1)
+                u7.halo_n = p.plan.n_ext;
+                u7.halo_kp = k + 1;
+            }
+            if (X) {
+                u7.alpha_hist = p.d_alpha;
+                set_ring(c, p, u7);
+                LAUNCH(c, launch_update_p2(u7, k, x2_pbuf(c, p, k), x2_pbuf(c, p, k + 1),
+                                           p.grid_upd, launch_stream(c, p)));
+            } else {
+                LAUNCH(c, launch_update_p(u7, k, p.grid_upd, launch_stream(c, p)));
+            }
+        }
+        if (t) t->mark(2);
+    }
+    if (X)
+        for (auto &p : c->parts) {
+            DevGuard g(p.dev);
+            UpdArgs u = upd_args(c, p, 0);
+            u.alpha_hist = p.d_alpha;
+            set_ring(c, p, u);
+            LAUNCH(c, launch_x2_finish(u, launch_stream(c, p)));
+        }
+    return MINIFE_OK;
+}
+
 static int enqueue_solve(minife_ctx *c, int max_iters, double tol, PhaseTimer *t) {
     if (!t) c->tw_armed = false;
     c->cur_max_iters = max_iters;
+    if (devcomm(c) && !small_mode(c) && !fused_mode(c)) return enqueue_solve_dev(c, max_iters, tol, t);
     if (!t && x2_mode(c) && !small_mode(c)) {
         TRY(enqueue_init(c, tol));
         if (c->parts.size() > 1 || c->world > 1) {    // halo of p_1 = b (buffer of odd k)
-            if (devcomm(c)) TRY(enqueue_push(c, 0, 0, true, true));
-            else TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
+            TRY(enqueue_halo(c, [](Part &p) { return p.d_p; }));
         }
         for (int k = 1; k <= max_iters; ++k) TRY(enqueue_iteration_x2(c, k));
         for (auto &p : c->parts) {

@@ -536,18 +536,6 @@ __global__ void k_halo_wait(UpdArgs a, int k) {
     halo_wait_body(a.dc, k, a.st);
 }
 
-// The same wait folded into the end of K7 (whose p_(k+1) the neighbours' pushes complete):
-// the last CTA to finish waits, so the next SpMV starts only once the halo has landed.
-__device__ void halo_wait_last_cta(const DevComm &dc, int k, CgState *st,
-                                   unsigned long long *ticket) {
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1ull) == (unsigned long long)(gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    halo_wait_body(dc, k, st);
-    if (threadIdx.x == 0) *ticket = 0ull;
-}
 
 // ----------------------------------------------------------------------------------------
 // a2: SpMV  y = A x  (+ exact pAp epilogue)
@@ -1297,6 +1285,56 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
 // ----------------------------------------------------------------------------------------
 // CG init (C6 step 1): x = 0, r = b, p = b, rr = dot(r, r)
 // ----------------------------------------------------------------------------------------
+
+// Halo by r (device comm).  The owner of a halo node computes p_(k+1) there as
+// fl(r_(k+1) + fl(beta_k p_k)); the receiver holds p_k at that node (its halo column) and gets
+// beta_k from the same exact rr, so with r_(k+1) pushed by the owner it computes the same bits
+// itself -- and r_(k+1) is final after K6, so the push overlaps the rr reduction instead of
+// waiting for it.  All threads of the CTA call it.
+__device__ void halo_p_update(const UpdArgs &a, int kp, double beta, const double *pin,
+                              double *pout) {
+    const DevComm &dc = a.dc;
+    const unsigned long long seq = comm_halo_seq(comm_gen(dc), kp);
+    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
+        comm_spin(dc, dc.local + comm_halo_flag(dc.world, dc.nbr_rank[t]), seq, a.st);
+    __syncthreads();
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < a.halo_n;
+         h += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = a.halo_col[h];
+        const double rv = __ldcv(a.rhalo + h);     // stored by a peer: never a stale L1 line
+        pout[c] = pin ? __dadd_rn(rv, __dmul_rn(beta, pin[c])) : rv;
+    }
+}
+
+__global__ void __launch_bounds__(UPD_THREADS) k_push_r(UpdArgs a, int kp,
+                                                        const int32_t *send_row,
+                                                        const uint8_t *slot_nbr,
+                                                        const int32_t *dst_slot,
+                                                        double *const *dst_ptr, int64_t n) {
+    __shared__ int s_last;
+    if (kp > 1 && a.st->done) return;    // kp = 1 (r_0 = b): the state is not initialised yet
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst_ptr[slot_nbr[i]][dst_slot[i]] = a.r[send_row[i]];
+    const DevComm &dc = a.dc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();            // this CTA's peer stores (cumulative via bar.sync)
+        s_last = atomicAdd(reinterpret_cast<unsigned long long *>(dc.local + 1), 1ull) ==
+                 (unsigned long long)(gridDim.x - 1);
+        if (s_last) __threadfence_system();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    const unsigned long long seq = comm_halo_seq(comm_gen(dc), kp);
+    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
+        st_release_sys(dc.region[dc.nbr_rank[t]] + comm_halo_flag(dc.world, dc.rank), seq);
+    if (threadIdx.x == 0) dc.local[1] = 0ull;       // ticket for the next launch
+}
+
+__global__ void __launch_bounds__(UPD_THREADS) k_halo_init(UpdArgs a) {
+    halo_p_update(a, 1, 0.0, nullptr, a.p);
+}
 
 template <bool IDENT>
 __global__ void __launch_bounds__(UPD_THREADS) k_init_vectors(UpdArgs a) {
@@ -2087,9 +2125,9 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
             }
         }
     }
-    // device comm: the next SpMV needs the neighbours' halo of p_(k+1) (their k_push ran
-    // before this kernel on their side); no wait once the solve stops (uniform decision)
-    if (a.fold_wait_k > 0 && !stop) halo_wait_last_cta(a.dc, a.fold_wait_k, a.st, a.dc.local + 5);
+    // device comm: the halo columns of p_(k+1) from the neighbours' r_(k+1);
+    // not once the solve stops (a uniform decision)
+    if (a.halo_n > 0 && !stop) halo_p_update(a, a.halo_kp, beta, a.p, a.p);
 }
 
 // K7 of the deferred-x scheme (launch_update_p2): the x update of iteration k is
@@ -2172,9 +2210,8 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
                 }
             }
         }
-        // device comm: the last CTA waits for the neighbours' halo of p_(k+1) (as k_update_p)
-        if (a.fold_wait_k > 0 && !stop)
-            halo_wait_last_cta(a.dc, a.fold_wait_k, a.st, a.dc.local + 5);
+        // device comm: the halo columns of p_(k+1) (as k_update_p)
+        if (a.halo_n > 0 && !stop) halo_p_update(a, a.halo_kp, beta, pk, po);
         return;
     }
     const int64_t rows = a.g.rows, n2 = rows >> 1;
@@ -2985,6 +3022,23 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
     const int k_halo = mode == 1 ? k + 1 : (k > 0 ? k : 1);
     k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, k_halo, send_row, send_col, slot_nbr, dst_col,
                                      dst_ptr, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_push_r(const UpdArgs &a, int kp, const int32_t *send_row,
+                          const uint8_t *slot_nbr, const int32_t *dst_slot,
+                          double *const *dst_ptr, int64_t n, cudaStream_t s) {
+    if (!a.dc.local || n <= 0) return cudaErrorInvalidValue;
+    const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
+    k_push_r<<<g, UPD_THREADS, 0, s>>>(a, kp, send_row, slot_nbr, dst_slot, dst_ptr, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_init(const UpdArgs &a, cudaStream_t s) {
+    if (!a.dc.local || a.halo_n <= 0) return cudaErrorInvalidValue;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((a.halo_n + UPD_THREADS - 1) /
+                                                                  UPD_THREADS, 4 * 148));
+    k_halo_init<<<g, UPD_THREADS, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -170,7 +170,13 @@ struct UpdArgs {
     int x_late;                         // K7 applies x += alpha p (1, default) or K6 does (0)
     DevComm dc;                         // device-initiated reductions / halo (dc.local != null)
     int fold_push;                      // K6 / init: the last CTA pushes the rr accumulator
-    int fold_wait_k;                    // K7: > 0 -> the last CTA waits for the halo of p_k
+    // device comm, halo by r: K7 completes the halo columns itself,
+    // p_(kp)[c] = fl(rhalo[h] + fl(beta p_(kp-1)[c])), c = halo_col[h], once the neighbours'
+    // pushes of r_(kp) at their send slots have landed in rhalo (halo_n = 0: off)
+    const double *rhalo;
+    const int32_t *halo_col;
+    int64_t halo_n;
+    int halo_kp;
     int cl_dd;                          // cluster solver: DSMEM digit pushes (1, default)
 };
 constexpr int XDEF_MAX = 8;
@@ -217,6 +223,15 @@ bool cluster_solver_available();     // a CL_CTAS-CTA cluster fits this device (
 cudaError_t launch_pack_next_p(const UpdArgs &a, int k, const int32_t *send_row,
                                const int32_t *send_col, double *sendbuf, int64_t n,
                                cudaStream_t s);
+
+// Halo by r (device comm): dst_ptr[slot_nbr[i]][dst_slot[i]] = r[send_row[i]] (r_(kp) at the
+// send slots, into the receivers' r-halo buffers), then the last CTA raises each neighbour's
+// halo flag for kp.  Needs no reduction result: it runs right after K6.
+cudaError_t launch_push_r(const UpdArgs &a, int kp, const int32_t *send_row,
+                          const uint8_t *slot_nbr, const int32_t *dst_slot,
+                          double *const *dst_ptr, int64_t n, cudaStream_t s);
+// p_1's halo columns = the r_0 (= b) halo the neighbours pushed (after their flags for kp = 1)
+cudaError_t launch_halo_init(const UpdArgs &a, cudaStream_t s);
 
 // Halo push (a1, device-initiated): dst_ptr[slot_nbr[i]][dst_col[i]] = value of slot i, with
 // value = p[send_col[i]] (mode 0) or r[send_row[i]] + beta_k p[send_col[i]] (mode 1).

@@ -306,14 +306,12 @@ def test_device_comm_launch_count_has_no_host_collective(fold):
         parts = [g.part_info(q) for q in range(p)]
         assert all(q.n_neighbors > 0 for q in parts)
         if fold:
-            # per part: init_vectors, init_finalize, push + wait (p_1); per iteration: SpMV,
-            # K6, push, K7 (no push after the last K7)
+            # per part: init_vectors, push of r_0, init_finalize, halo init (p_1); per
+            # iteration: SpMV, K6, push of r_(k+1), K7 (no push after the last K6)
             assert launched == p * (4 + 4 * 50 - 1)
         else:
-            # per part: init_vectors, acc_push, init_finalize, push + wait (p_1); per
-            # iteration: SpMV, acc_push, K6, acc_push, push, K7, halo wait (none after the
-            # last K7)
-            assert launched == p * (5 + 7 * 50 - 2)
+            # + the separate accumulator pushes: one at init, two per iteration
+            assert launched == p * (5 + 6 * 50 - 1)
 
 
 @pytest.mark.parametrize("fold", [1, 0])
