@@ -86,15 +86,17 @@ extern "C" {
                                       each neighbor block into the receiver's contiguous
                                       receive buffer (device copies standing in for
                                       ncclSend/ncclRecv), unpack into the halo columns.       */
-#define MINIFE_TRANSPORT_PUSH 2    /* device-initiated: one kernel per
-                                      part stores every send slot straight into the receiver's
-                                      halo column.  MULTI ctxs use it over NVLink when every
-                                      device pair has peer access.                            */
-#define MINIFE_TRANSPORT_DEVICE 3  /* the device-initiated protocol of MULTI/RANK ctxs on one GPU:
-                                      PUSH for the halo plus in-kernel reductions -- every part
-                                      stores its exact accumulator into every part's inbox and
-                                      raises a release flag; consumers wait on acquire flags
-                                      (DESIGN.md §7).  No host-launched collective.          */
+#define MINIFE_TRANSPORT_PUSH 2    /* one kernel per part stores p_(k+1) at every send slot
+                                      straight into the receiver's halo column (reductions
+                                      stay device-local sums).  MULTI ctxs with option
+                                      device_comm = 0 use it over NVLink peer pointers.       */
+#define MINIFE_TRANSPORT_DEVICE 3  /* the device-initiated protocol of MULTI/RANK ctxs on one GPU
+                                      (DESIGN.md §7): every part pushes
+                                      r_(k+1) at its send slots into the receivers' r-halo
+                                      buffers right after the r update, the receivers complete
+                                      p_(k+1)'s halo columns themselves; every part stores its
+                                      exact accumulators into every part's inbox; release /
+                                      acquire flags.  No host-launched collective.           */
 
 typedef struct minife_ctx minife_ctx;
 

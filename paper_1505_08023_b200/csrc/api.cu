@@ -436,20 +436,17 @@ static int setup_part(minife_ctx *c, Part &p, int dev, const Plan &plan) {
     return MINIFE_OK;
 }
 
-// Push tables (MINIFE_TRANSPORT_PUSH / device comm): part p's slot j of its block for
-// neighbor q lands in q's halo slot recv_off_q[p] + j, i.e. q's extended column
-// ext_pos_q[...]; the store goes through q's p array as seen from p's device (the same
-// pointer on one device, a peer pointer in MULTI ctxs, a CUDA-IPC mapping in RANK ctxs:
-// `remote_p` gives it).  q's plan is recomputed on the host when q lives in another process.
+// Push tables (MINIFE_TRANSPORT_PUSH; MULTI ctxs with NCCL reductions): part p's slot j of
+// its block for neighbor q lands in q's halo slot recv_off_q[p] + j, i.e. q's extended column
+// ext_pos_q[...]; the store goes through q's p array as seen from p's device (the same pointer
+// on one device, a peer pointer in MULTI ctxs: `remote_p` gives it).
 template <class RemoteP>
 static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
     const size_t ns = p.plan.send_idx.size();
     const size_t nn = p.plan.nbr.size();
     std::vector<uint8_t> nb(ns);
     std::vector<int32_t> dst(ns);
-    // slot-major: entry [s][k] = neighbour k's ring buffer s (s = 0: its p; the deferred-x
-    // scheme's p_k lives in ring[(k - 1) % X]); null where that buffer does not exist
-    std::vector<double *> ptr(XDEF_MAX * nn, nullptr);
+    std::vector<double *> ptr(nn, nullptr);
     for (size_t k = 0; k < nn; ++k) {
         const int qr = p.plan.nbr[k];
         Plan qown;
@@ -472,7 +469,7 @@ static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
             nb[p.plan.send_off[k] + j] = (uint8_t)k;
             dst[p.plan.send_off[k] + j] = (int32_t)q.ext_pos[q.recv_off[kq] + j];
         }
-        for (int s = 0; s < XDEF_MAX; ++s) ptr[s * nn + k] = remote_p(qr, s);
+        ptr[k] = remote_p(qr);
     }
     DevGuard g(p.dev);
     if (!p.d_push_nbr) {
@@ -494,7 +491,7 @@ static int build_push_tables(minife_ctx *c, Part &p, RemoteP remote_p) {
 
 static int setup_push(minife_ctx *c) {
     for (auto &p : c->parts)
-        TRY(build_push_tables(c, p, [c](int qr, int s) { return c->parts[qr].ring(s); }));
+        TRY(build_push_tables(c, p, [c](int qr) { return c->parts[qr].d_p; }));
     c->push_ready = true;
     return MINIFE_OK;
 }
@@ -711,14 +708,14 @@ static bool devcomm(const minife_ctx *c) {
 }
 
 // Device comm with the pushes / halo wait folded into the producing kernels' last CTAs (the
-// SYM path; SEG/CRS keep the separate k_acc_push / k_halo_wait launches).  Option
+// SYM path; SEG/CRS keep the separate k_acc_push launches).  Option
 // "fold_comm" = 0 keeps the separate launches everywhere (tests compare both).
 static bool fold_comm(const minife_ctx *c) {
     return devcomm(c) && c->fmt == MINIFE_FMT_SYM && c->opt.fold_comm != 0;
 }
 
 static bool push_mode(const minife_ctx *c) {
-    if (devcomm(c)) return c->world > 1;
+    if (devcomm(c)) return false;                // device comm: halo by r (enqueue_solve_dev)
     return c->world > 1 && c->push_ready &&
            (c->mode == MINIFE_MODE_MULTI ||
             (c->mode == MINIFE_MODE_VIRTUAL && c->transport == MINIFE_TRANSPORT_PUSH));
@@ -726,17 +723,9 @@ static bool push_mode(const minife_ctx *c) {
 
 static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in);
 
-// Before SpMV(k): device comm -> a wait kernel per part (neighbors' halo flags); MULTI with
-// NCCL reductions -> each part's compute stream waits for its neighbors' push kernels
-static int push_wait(minife_ctx *c, int k) {
-    if (devcomm(c)) {
-        for (auto &p : c->parts) {
-            if (p.plan.nbr.empty()) continue;
-            DevGuard g(p.dev);
-            LAUNCH(c, launch_halo_wait(upd_args(c, p, 0), k, launch_stream(c, p)));
-        }
-        return MINIFE_OK;
-    }
+// MULTI with NCCL reductions and the push transport: each part's compute stream waits for
+// its neighbors' push kernels
+static int push_wait(minife_ctx *c) {
     if (c->mode != MINIFE_MODE_MULTI) return MINIFE_OK;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1253,26 +1242,17 @@ extern "C" int minife_assemble(minife_ctx *c) {
 // Push the halo of p (mode 0: current p; mode 1: p_(k+1) ahead of K7) from every part, then
 // (MULTI) make every part's compute stream wait for its neighbors' pushes.  With mode 1 the
 // waits are placed by the caller after K7 (wait_now = false).
-static int xdef_of(const minife_ctx *c);
-static double *x2_pbuf(const minife_ctx *c, const Part &p, int k);
-static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now, bool ring = false) {
-    // ring = the deferred-x sequence: p_k lives in ring((k - 1) % X); the pushed values go to
-    // the receiver's buffer of the p they belong to (mode 1: p_(k+1); mode 0 at k = 0: p_1)
-    const int X = ring ? xdef_of(c) : 0;
-    const int slot = X ? (mode == 1 ? k % X : (k > 0 ? (k - 1) % X : 0)) : 0;
+static int enqueue_push(minife_ctx *c, int k, int mode, bool wait_now) {
     for (auto &p : c->parts) {
         const int64_t n = (int64_t)p.plan.send_idx.size();
         if (!n) continue;
         DevGuard g(p.dev);
-        UpdArgs a = upd_args(c, p, 1);           // acc_in = rr_k (mode 1), p, r, rr, st, dc
-        if (X && k > 0) a.p = x2_pbuf(c, p, k);  // p_k
+        UpdArgs a = upd_args(c, p, 1);           // acc_in = rr_k (mode 1), p, r, rr, st
         LAUNCH(c, launch_push(a, k, mode, p.d_send_row, p.d_send_col, p.d_push_nbr, p.d_push_dst,
-                              p.d_push_ptr + (size_t)slot * p.plan.nbr.size(), n,
-                              launch_stream(c, p)));
-        if (c->mode == MINIFE_MODE_MULTI && !devcomm(c))
-            CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
+                              p.d_push_ptr, n, launch_stream(c, p)));
+        if (c->mode == MINIFE_MODE_MULTI) CUDA_TRY(c, cudaEventRecord(p.ev_push, p.stream));
     }
-    if (wait_now) return push_wait(c, mode == 1 ? k + 1 : (k > 0 ? k : 1));
+    if (wait_now) return push_wait(c);
     return MINIFE_OK;
 }
 
@@ -1492,7 +1472,7 @@ static int enqueue_k7_with_halo(minife_ctx *c, int k) {
             DevGuard g(p.dev);
             LAUNCH(c, launch_update_p(upd_args(c, p, 1), k, p.grid_upd, launch_stream(c, p)));
         }
-        return last ? MINIFE_OK : push_wait(c, k + 1);
+        return last ? MINIFE_OK : push_wait(c);
     }
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
@@ -1734,7 +1714,7 @@ static int xdef_of(const minife_ctx *c) {
     // the exchange fills the halo of the buffer p_(k+1) goes to
     const bool single = c->parts.size() == 1 && c->world == 1;
     // (device comm: each part completes the halo columns of p_(k+1) in the ring buffer itself)
-    const bool parts_ok = overlap_sym(c) && (!push_mode(c) || devcomm(c));
+    const bool parts_ok = overlap_sym(c) && !push_mode(c);
     if (!env || env == 1 || !(single || parts_ok) || fused_mode(c)) return 0;
     if (env >= 2) return std::min(env, XDEF_MAX);
     // automatic: single parts only -- on partitioned parts (x-line walks, halo exchange each
@@ -1747,21 +1727,12 @@ static bool x2_mode(const minife_ctx *c) { return xdef_of(c) > 0; }
 static int ensure_fused_buffers(minife_ctx *c) {   // never called while a stream captures
     if (!(fused_mode(c) || x2_mode(c))) return MINIFE_OK;
     const int X = std::max(2, xdef_of(c));
-    bool fresh = false;
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        if (!p.d_p2) {
-            TRY(alloc_colvec(c, p, &p.d_p2));
-            fresh = true;
-        }
+        if (!p.d_p2) TRY(alloc_colvec(c, p, &p.d_p2));
         for (int i = 2; i < X; ++i)
-            if (!p.d_pr[i]) {
-                TRY(alloc_colvec(c, p, &p.d_pr[i]));
-                fresh = true;
-            }
+            if (!p.d_pr[i]) TRY(alloc_colvec(c, p, &p.d_pr[i]));
     }
-    // one-process ctxs push into the peers' ring buffers directly: refresh the tables
-    if (fresh && c->push_ready && c->mode != MINIFE_MODE_RANK) TRY(setup_push(c));
     return MINIFE_OK;
 }
 

@@ -524,17 +524,6 @@ __device__ void acc_push_last_cta(const DevComm &dc, const unsigned long long *a
     if (threadIdx.x == 0) *ticket = 0ull;
 }
 
-// Before SpMV(k): every neighbor's halo values of p_k have landed (k_push signalled).
-__device__ void halo_wait_body(const DevComm &dc, int k, CgState *st) {
-    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k);
-    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
-        comm_spin(dc, dc.local + comm_halo_flag(dc.world, dc.nbr_rank[t]), seq, st);
-}
-
-__global__ void k_halo_wait(UpdArgs a, int k) {
-    if (a.st->done) return;
-    halo_wait_body(a.dc, k, a.st);
-}
 
 
 // ----------------------------------------------------------------------------------------
@@ -2291,9 +2280,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_pack_next_p(UpdArgs a, int k,
 // (VIRTUAL), a peer GPU's array over NVLink (MULTI, peer access) or a CUDA-IPC mapping of
 // another rank's array (RANK).  No pack, no wire, no unpack.
 // mode 0: the value is p[send_col]; mode 1: p_(k+1) = fl(r + fl(beta_k p)) as k_pack_next_p.
-// With device comm (a.dc.local) the last CTA to finish raises each neighbor's halo flag for
-// iteration k_halo (release, after every CTA's stores are fenced at system scope).
-__global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode, int k_halo,
+__global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode,
                                                       const int32_t *send_row,
                                                       const int32_t *send_col,
                                                       const uint8_t *slot_nbr,
@@ -2301,7 +2288,6 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode
                                                       double *const *dst_ptr, int64_t n) {
     __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta;
-    __shared__ int s_last;
     if (mode == 1) {
         if (a.st->done) return;
         if (!acc_in_load(s_in, a, k, 1)) return;
@@ -2319,21 +2305,6 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push(UpdArgs a, int k, int mode
         const double v = mode == 1 ? __dadd_rn(a.r[send_row[i]], __dmul_rn(beta, pv)) : pv;
         dst_ptr[slot_nbr[i]][dst_col[i]] = v;
     }
-    const DevComm &dc = a.dc;
-    if (!dc.local) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();            // this CTA's peer stores (cumulative via bar.sync)
-        s_last = atomicAdd(reinterpret_cast<unsigned long long *>(dc.local + 1), 1ull) ==
-                 (unsigned long long)(gridDim.x - 1);
-        if (s_last) __threadfence_system();
-    }
-    __syncthreads();
-    if (!s_last) return;
-    const unsigned long long seq = comm_halo_seq(comm_gen(dc), k_halo);
-    for (int t = threadIdx.x; t < dc.n_nbr; t += blockDim.x)
-        st_release_sys(dc.region[dc.nbr_rank[t]] + comm_halo_flag(dc.world, dc.rank), seq);
-    if (threadIdx.x == 0) dc.local[1] = 0ull;       // ticket for the next launch
 }
 
 // ----------------------------------------------------------------------------------------
@@ -3019,9 +2990,8 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
                         double *const *dst_ptr, int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int g = (int)std::min<int64_t>((n + UPD_THREADS - 1) / UPD_THREADS, 4 * 148);
-    const int k_halo = mode == 1 ? k + 1 : (k > 0 ? k : 1);
-    k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, k_halo, send_row, send_col, slot_nbr, dst_col,
-                                     dst_ptr, n);
+    k_push<<<g, UPD_THREADS, 0, s>>>(a, k, mode, send_row, send_col, slot_nbr, dst_col, dst_ptr,
+                                     n);
     return cudaGetLastError();
 }
 
@@ -3049,11 +3019,6 @@ cudaError_t launch_acc_push(const UpdArgs &a, int k, int which, const unsigned l
     return cudaGetLastError();
 }
 
-cudaError_t launch_halo_wait(const UpdArgs &a, int k, cudaStream_t s) {
-    if (!a.dc.local) return cudaErrorInvalidValue;
-    k_halo_wait<<<1, 32, 0, s>>>(a, k);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_update_p2(const UpdArgs &a, int k, const double *pk, double *po, int grid,
                              cudaStream_t s) {

@@ -243,8 +243,6 @@ cudaError_t launch_push(const UpdArgs &a, int k, int mode, const int32_t *send_r
 // `which` of iteration k: 0 pAp_k, 1 rr_k) into every rank's inbox and raise the flags.
 cudaError_t launch_acc_push(const UpdArgs &a, int k, int which, const unsigned long long *acc,
                             cudaStream_t s);
-// Wait until every neighbor has signalled the halo of p_k (k_push's signal), then return.
-cudaError_t launch_halo_wait(const UpdArgs &a, int k, cudaStream_t s);
 
 // Halo (a1): dst[didx ? didx[i] : i] = src[sidx ? sidx[i] : i], i < n
 cudaError_t launch_move(const double *src, const int32_t *sidx, double *dst,
