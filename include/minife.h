@@ -221,6 +221,9 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *                     0 natural order; n > 0 bands of n / N_x lines wherever planes exceed n
  *   "comm_timeout_ms" device comm: how long a kernel waits for a peer's flag before the
  *                     solve fails with MINIFE_ECOMM (default 60000)
+ *   "comm_fault_part" fault injection for tests: the part / rank with this id never pushes
+ *                     its accumulators or halo (device comm), so its peers time out into
+ *                     MINIFE_ECOMM; -1 (default) off
  * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,
  * value out of range). */
 int minife_set_option(minife_ctx *ctx, const char *name, int64_t value);

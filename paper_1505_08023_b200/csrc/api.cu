@@ -204,6 +204,7 @@ struct minife_ctx {
         int fold_comm = 1;         // device comm: pushes / halo wait inside the producers
         int band_rows = -1;        // SYM SpMV tile order: rows per band-plane (-1 auto, 0 off)
         int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
+        int comm_fault_part = -1;  // fault injection (tests): this rank / part never signals
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
     int cur_max_iters = 0;                       // max_iters of the solve being enqueued
@@ -955,6 +956,7 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"fold_comm", &c->opt.fold_comm, 0, 1},
         {"band_rows", &c->opt.band_rows, -1, 1 << 30},
         {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
+        {"comm_fault_part", &c->opt.comm_fault_part, -1, 1 << 20},
     };
     for (auto &t : table) {
         if (strcmp(t.name, name) != 0) continue;
@@ -1391,6 +1393,7 @@ static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
         a.dc.rank = p.plan.rank;
         a.dc.world = c->world;
         a.dc.timeout_ns = (long long)c->opt.comm_timeout_ms * 1000000ll;
+        a.dc.mute = c->opt.comm_fault_part == p.plan.rank ? 1 : 0;
     }
     if (which_in == 0) {          // K6: in = pAp, out = rr
         a.acc_in = p.acc_pAp();

@@ -483,6 +483,7 @@ __device__ bool acc_in_load(unsigned long long *s_in, const UpdArgs &a, int k, i
 // The push itself (one CTA): the words of `acc` into slot `rank` of every rank's inbox, a
 // system-scope fence, then one release flag per rank.
 __device__ void acc_push_body(const DevComm &dc, const unsigned long long *acc, int k, int which) {
+    if (dc.mute) return;                         // fault injection: a rank that never signals
     const unsigned long long gen = comm_gen(dc);
     const int gp = (int)(gen & 1);
     const int64_t off =
@@ -1302,6 +1303,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_push_r(UpdArgs a, int kp,
                                                         double *const *dst_ptr, int64_t n) {
     __shared__ int s_last;
     if (kp > 1 && a.st->done) return;    // kp = 1 (r_0 = b): the state is not initialised yet
+    if (a.dc.mute) return;                 // fault injection: a rank that never signals
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         dst_ptr[slot_nbr[i]][dst_slot[i]] = a.r[send_row[i]];

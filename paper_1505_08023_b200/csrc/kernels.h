@@ -120,6 +120,7 @@ struct DevComm {
     int n_nbr;
     int rank, world;
     long long timeout_ns;               // spin limit; exceeded -> CgState.status = 9 (ECOMM)
+    int mute;                           // fault injection (tests): this part never pushes
 };
 
 struct SpmvArgs {

@@ -203,6 +203,24 @@ def test_other_options_bit_identical(opts):
     _solver_variant((23, 17, 9), fmt, opts)
 
 
+@pytest.mark.parametrize("fold", [1, 0])
+def test_device_comm_dead_peer_fails_with_ecomm_then_recovers(fold):
+    """Fault injection: one virtual part never signals (option comm_fault_part).  Its peers'
+    spins time out after comm_timeout_ms and the solve fails with MINIFE_ECOMM instead of
+    hanging; with the fault cleared the next solve on the same ctx is bitwise the oracle."""
+    n, p = (12, 11, 10), 3
+    with M.Minife(*n, virtual=p, options={"fold_comm": fold, "comm_timeout_ms": 50}) as g:
+        g.set_transport(M.TRANSPORT_DEVICE)
+        g.assemble()
+        g.set_option("comm_fault_part", 1)
+        with pytest.raises(M.MinifeError) as e:
+            r = g.cg_solve(20, 0.0)
+            assert r.status == M.MINIFE_ECOMM     # (raised by the binding on ECOMM)
+        assert e.value.status == M.MINIFE_ECOMM
+        g.set_option("comm_fault_part", -1)
+        check_cg(g, n, 200, 0.0)
+
+
 def test_option_errors():
     with M.Minife(3, 3, 3) as g:
         for name, v in (("no_such_option", 1), ("x_defer", 9), ("graph", 2), ("small_solver", -2)):
