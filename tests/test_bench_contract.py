@@ -118,3 +118,20 @@ def test_assembly_bytes_model():
         sell_entries = 14 * 32 * ((301 ** 3 + 31) // 32)
     by = b.assembly_bytes(Info, "sym")
     assert abs(by / 1e9 - 4.36) < 0.01
+
+
+@pytest.mark.gpu
+def test_gpu_arm_under_torchrun_one_rank():
+    """The torchrun launch form (RANK ctx, NCCL process group, uid broadcast) end to end at
+    world size 1: same JSON contract, n_gpus 1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29581", os.path.join(ROOT, "bench.py"),
+           "--gpus", "1", "--mesh", "30", "30", "30", "--steps", "2", "--warmup", "3",
+           "--no-cpu-baseline", "--no-format-compare"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-3000:]
+    d = json.loads(lines[0])
+    check_base(d, 2, 3)
+    assert "torchrun" in d["config"]["parallelism"]
