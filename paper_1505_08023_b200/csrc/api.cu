@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing without a profiler
 
 #include <algorithm>
 #include <cmath>
@@ -163,6 +164,11 @@ struct DevGuard {
     ~DevGuard() {
         if (ok) cudaSetDevice(prev);
     }
+};
+// NVTX range per ABI phase (assemble, solve, profile, spmv, verify), visible to Nsight tools
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 }  // namespace
 
@@ -1162,6 +1168,7 @@ static int build_tile_order(minife_ctx *c, Part &p) {
 }
 
 extern "C" int minife_assemble(minife_ctx *c) {
+    NvtxRange nvtx_("minife_assemble");
     if (!c) return MINIFE_EINVAL;
     // CRS sizes its arrays from a device pass read back to the host: its time is host-split
     const bool timed = c->fmt != MINIFE_FMT_CRS;
@@ -2046,6 +2053,7 @@ static int wait_solve(minife_ctx *c, cudaEvent_t done) {
 }
 
 extern "C" int minife_cg_solve(minife_ctx *c, int max_iters, double tol, minife_cg_result *res) {
+    NvtxRange nvtx_("minife_cg_solve");
     TRY(check_solve_args(c, max_iters, tol));
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
@@ -2180,6 +2188,7 @@ extern "C" int minife_get_timing_window(minife_ctx *c, double *spmv_ms, double *
 }
 
 extern "C" int minife_cg_profile(minife_ctx *c, int max_iters, minife_kernel_times *out) {
+    NvtxRange nvtx_("minife_cg_profile");
     TRY(check_solve_args(c, max_iters, 0.0));
     TRY(ensure_hist(c, max_iters));
     Part &p0 = c->parts[0];
@@ -2259,6 +2268,7 @@ static void rows_to_cols(const Plan &pl, const double *rowv, double *colv) {
 // ----------------------------------------------------------------------------------------
 
 extern "C" int minife_spmv(minife_ctx *c, const double *x, double *y) {
+    NvtxRange nvtx_("minife_spmv");
     if (!c || !x || !y) return MINIFE_EINVAL;
     if (!c->assembled) return MINIFE_ESTATE;
     const bool global_io = c->mode != MINIFE_MODE_RANK;
@@ -2382,6 +2392,7 @@ extern "C" int minife_get_info(const minife_ctx *c, minife_info *o) {
 
 extern "C" int minife_verify(minife_ctx *c, int64_t n, const int64_t *gids, int nterms,
                              double *u_fe, double *u_exact, double *max_abs_err) {
+    NvtxRange nvtx_("minife_verify");
     if (!c || n < 0 || n > (1 << 24) || nterms < 1 || nterms > 4096 || !max_abs_err ||
         (n && (!gids || !u_fe || !u_exact)))
         return MINIFE_EINVAL;
