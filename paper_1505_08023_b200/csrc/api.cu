@@ -1138,14 +1138,25 @@ static Matrix matrix_of(const minife_ctx *c, const Part &p) {
 static constexpr int64_t BAND_ROWS_AUTO = 65536, BAND_MIN_PLANE = 122880;
 static int build_tile_order(minife_ctx *c, Part &p) {
     DevGuard g(p.dev);
-    dfree(p, p.d_tile_order, (size_t)p.tile_order_n);
-    p.tile_order_n = 0;
-    if (c->fmt != MINIFE_FMT_SYM) return MINIFE_OK;
+    // a captured solve graph holds the order's device pointer: the buffer is reused when the
+    // order keeps its size (re-assembly), and any other change drops the graph
+    auto drop_order = [&]() {
+        if (!p.d_tile_order) return;
+        dfree(p, p.d_tile_order, (size_t)p.tile_order_n);
+        p.tile_order_n = 0;
+        drop_graph(c);
+    };
+    if (c->fmt != MINIFE_FMT_SYM) {
+        drop_order();
+        return MINIFE_OK;
+    }
     const int64_t N0 = p.plan.ext_n[0], N1 = p.plan.ext_n[1];
     const int64_t P = N0 * N1;
     const int64_t target = c->opt.band_rows < 0 ? BAND_ROWS_AUTO : c->opt.band_rows;
-    if (target == 0 || (c->opt.band_rows < 0 && P <= BAND_MIN_PLANE) || P <= target)
+    if (target == 0 || (c->opt.band_rows < 0 && P <= BAND_MIN_PLANE) || P <= target) {
+        drop_order();
         return MINIFE_OK;
+    }
     const int64_t B = std::max<int64_t>(8, target / N0);               // lines per band
     const int64_t nslices = (p.ncols + 31) / 32;
     const int64_t ntiles = (nslices + SYMM_NW - 1) / SYMM_NW;
@@ -1161,8 +1172,12 @@ static int build_tile_order(minife_ctx *c, Part &p) {
                      });
     std::vector<int32_t> order(ntiles);
     for (int64_t t = 0; t < ntiles; ++t) order[t] = key[t].second;
-    TRY(dalloc(c, p, &p.d_tile_order, (size_t)ntiles));
-    p.tile_order_n = ntiles;
+    if (p.d_tile_order && p.tile_order_n != ntiles) drop_order();
+    if (!p.d_tile_order) {
+        TRY(dalloc(c, p, &p.d_tile_order, (size_t)ntiles));
+        p.tile_order_n = ntiles;
+        drop_graph(c);
+    }
     CUDA_TRY(c, cudaMemcpy(p.d_tile_order, order.data(), 4 * (size_t)ntiles, cudaMemcpyHostToDevice));
     return MINIFE_OK;
 }

@@ -221,6 +221,26 @@ def test_device_comm_dead_peer_fails_with_ecomm_then_recovers(fold):
         check_cg(g, n, 200, 0.0)
 
 
+@pytest.mark.parametrize("band", [1000, 4000])
+def test_band_order_bit_identical_across_reassembly(band):
+    """The band-major SYM tile order (forced at a small mesh with option band_rows) is bitwise
+    the oracle, also when the ctx re-assembles between solves (the captured graph holds the
+    order's device pointer: it must survive re-assembly) and when the option changes."""
+    n = (33, 32, 31)
+    s = oracle_system(n)
+    with M.Minife(*n, options={"band_rows": band, "small_solver": 0}) as g:
+        for rep in range(3):
+            g.assemble()
+            check_cg(g, n, 200, 0.0)
+            check_spmv(g, s, 3)
+        g.set_option("band_rows", 0)              # natural order: the order buffer goes away
+        g.assemble()
+        check_cg(g, n, 200, 0.0)
+        g.set_option("band_rows", band)
+        g.assemble()
+        check_cg(g, n, 100, 1e-10)
+
+
 def test_option_errors():
     with M.Minife(3, 3, 3) as g:
         for name, v in (("no_such_option", 1), ("x_defer", 9), ("graph", 2), ("small_solver", -2)):
