@@ -219,6 +219,9 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *                     band-major (y-bands of 65536 / N_x lines swept plane by plane) for
  *                     planes of more than 122880 rows (400^3), natural order otherwise;
  *                     0 natural order; n > 0 bands of n / N_x lines wherever planes exceed n
+ *   "snake"           SYM SpMV: odd iterations visit the tiles last to first, so they start
+ *                     on what the previous SpMV left in L2: -1 (default) auto (matrices of
+ *                     48-400 MB), 0 off, 1 on
  *   "comm_timeout_ms" device comm: how long a kernel waits for a peer's flag before the
  *                     solve fails with MINIFE_ECOMM (default 60000)
  *   "comm_fault_part" fault injection for tests: the part / rank with this id never pushes

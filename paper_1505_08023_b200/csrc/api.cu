@@ -209,6 +209,7 @@ struct minife_ctx {
         int device_comm = -1;      // MULTI/RANK: 1 device-initiated comm, 0 NCCL, -1 auto
         int fold_comm = 1;         // device comm: pushes / halo wait inside the producers
         int band_rows = -1;        // SYM SpMV tile order: rows per band-plane (-1 auto, 0 off)
+        int snake = -1;            // SYM SpMV: odd iterations visit the tiles last to first
         int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
         int comm_fault_part = -1;  // fault injection (tests): this rank / part never signals
     } opt;
@@ -961,6 +962,7 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"device_comm", &c->opt.device_comm, -1, 1},
         {"fold_comm", &c->opt.fold_comm, 0, 1},
         {"band_rows", &c->opt.band_rows, -1, 1 << 30},
+        {"snake", &c->opt.snake, -1, 1},
         {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
         {"comm_fault_part", &c->opt.comm_fault_part, -1, 1 << 20},
     };
@@ -1429,7 +1431,21 @@ static UpdArgs upd_args(const minife_ctx *c, Part &p, int which_in) {
     return a;
 }
 
-static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double *y, bool dot) {
+// SYM storage per slice of 32 rows: 14 values, 9 run starts, 1 mask word per row
+static constexpr int64_t SYM_SLICE_BYTES = 32 * (14 * 8 + 9 * 4 + 4);
+
+// Snake order (odd iterations walk the SYM tiles backwards) where the matrix is within a few
+// times the 126 MB L2: the tiles the previous SpMV read last are still resident when the next
+// one starts there (B200, per solve: 80^3 (81 MB) -1 %, 100^3 (157 MB) -4 %, 120^3 (268 MB)
+// -2 %, 150^3 none, 300^3 +2 %; profiles/r02/ab/snake_order.jsonl)
+static bool snake_of(const minife_ctx *c, const Part &p) {
+    if (c->opt.snake >= 0) return c->opt.snake > 0;
+    const double bytes = (double)SYM_SLICE_BYTES * (double)p.nslices;
+    return bytes > 48e6 && bytes < 400e6;
+}
+
+static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double *y, bool dot,
+                          int k = 0) {
     SpmvArgs a{};
     a.m = matrix_of(c, p);
     a.g = geom_of(c, p);
@@ -1453,6 +1469,10 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     a.sym_kernel = c->opt.sym_kernel;
     a.impl = c->opt.spmv_impl;
     a.tile_order = c->fmt == MINIFE_FMT_SYM ? p.d_tile_order : nullptr;
+    // L2 reuse of the matrix across the solve's SpMVs (snake_of): the visiting order does not
+    // change a bit of the result (every row's sum and the exact pAp are order-independent)
+    a.reverse = c->fmt == MINIFE_FMT_SYM && dot && snake_of(c, p) && (k & 1);
+    a.k = k;
     return a;
 }
 
@@ -1630,7 +1650,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            SpmvArgs sa = spmv_args(c, p, p.d_p, p.d_Ap, true);
+            SpmvArgs sa = spmv_args(c, p, p.d_p, p.d_Ap, true, k);
             if (fold_comm(c)) {                      // the SpMV's last CTA pushes pAp_k
                 sa.dc = upd_args(c, p, 0).dc;
                 sa.fold_push = 1;
@@ -1646,7 +1666,7 @@ static int enqueue_iteration(minife_ctx *c, int k, PhaseTimer *t) {
         if (!t) TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true), true, p.grid_spmv,
+            LAUNCH(c, launch_spmv(spmv_args(c, p, p.d_p, p.d_Ap, true, k), true, p.grid_spmv,
                                     launch_stream(c, p)));
         }
         if (!t) TRY(tw_mark(c, k, true));
@@ -1800,7 +1820,7 @@ static int enqueue_iteration_x2(minife_ctx *c, int k) {
     TRY(tw_mark(c, k, false));
     for (auto &p : c->parts) {
         DevGuard g(p.dev);
-        SpmvArgs sa = spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true);
+        SpmvArgs sa = spmv_args(c, p, x2_pbuf(c, p, k), p.d_Ap, true, k);
         if (fold) {                                  // the SpMV's last CTA pushes pAp_k
             sa.dc = upd_args(c, p, 0).dc;
             sa.fold_push = 1;
@@ -1873,7 +1893,7 @@ static int enqueue_solve_dev(minife_ctx *c, int max_iters, double tol, PhaseTime
         if (!t) TRY(tw_mark(c, k, false));
         for (auto &p : c->parts) {
             DevGuard g(p.dev);
-            SpmvArgs sa = spmv_args(c, p, X ? x2_pbuf(c, p, k) : p.d_p, p.d_Ap, true);
+            SpmvArgs sa = spmv_args(c, p, X ? x2_pbuf(c, p, k) : p.d_p, p.d_Ap, true, k);
             if (fold) {                              // the SpMV's last CTA pushes pAp_k
                 sa.dc = upd_args(c, p, 0).dc;
                 sa.fold_push = 1;

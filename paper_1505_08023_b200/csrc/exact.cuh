@@ -166,16 +166,19 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
 #pragma unroll
         for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
     }
+    // the 13 warp sums back to back (no branch between them), then lane t adds sum t
+    int mine = 0;
 #pragma unroll
     for (int t = 0; t < 13; ++t) {
-        const int D = lo + t;
-        const int q = D - d16;
+        const int q = lo + t - d16;
         int contrib = 0;
 #pragma unroll
         for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
         const int sum = __reduce_add_sync(FULL, contrib);
-        if (lane == 0 && sum != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], sum);
+        mine = lane == (unsigned)t ? sum : mine;
     }
+    const int D = lo + (int)lane;
+    if (lane < 13u && mine != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], mine);
 }
 
 __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int *dig,

@@ -53,7 +53,55 @@ static cudaError_t ensure_smem_attr(K kernel, int bytes, unsigned long long &mas
 // small helpers
 // ----------------------------------------------------------------------------------------
 
+#ifdef SYMM_TRACE
+// Diagnostic builds only (tools/build_flags.sh NAME -DSYMM_TRACE): per-CTA %globaltimer
+// stamps of the last SYMM launch, read with minife_dbg_symm_trace
+__device__ unsigned long long g_symm_trace[1024 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SYMM_STAMP(i) g_symm_trace[blockIdx.x * 8 + (i)] = gtime()
+extern "C" int minife_dbg_symm_trace(unsigned long long *out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_symm_trace, 8 * (size_t)n);
+}
+// per iteration k < 256 and kernel kind (0 SpMV, 1 K6, 2 K7): earliest CTA entry, latest exit
+__device__ unsigned long long g_kt[256 * 3 * 2];
+struct KtScope {
+    int i;
+    __device__ KtScope(int kind, int k) : i(((k & 255) * 3 + kind) * 2) {
+        if (threadIdx.x == 0) atomicMin(&g_kt[i], gtime());
+    }
+    __device__ ~KtScope() {
+        if (threadIdx.x == 0) atomicMax(&g_kt[i + 1], gtime());
+    }
+};
+#define KT_SCOPE(kind, k) KtScope kt_scope_((kind), (k))
+__device__ unsigned long long g_k6_trace[2048 * 16];
+#define K6_STAMP(i)                                                                   \
+    do {                                                                              \
+        if (threadIdx.x == 0 && blockIdx.x < 2048) g_k6_trace[blockIdx.x * 16 + (i)] = gtime(); \
+    } while (0)
+extern "C" int minife_dbg_k6_trace(unsigned long long *out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_k6_trace, 8 * (size_t)n);
+}
+extern "C" int minife_dbg_kt(unsigned long long *out, int reset) {
+    if (reset) {
+        static unsigned long long h[256 * 3 * 2];
+        for (int j = 0; j < 256 * 3 * 2; ++j) h[j] = (j & 1) ? 0ull : ~0ull;
+        return (int)cudaMemcpyToSymbol(g_kt, h, sizeof h);
+    }
+    return (int)cudaMemcpyFromSymbol(out, g_kt, 8 * 256 * 3 * 2);
+}
+#else
+#define SYMM_STAMP(i) ((void)0)
+#define KT_SCOPE(kind, k) ((void)0)
+#define K6_STAMP(i) ((void)0)
+#endif
+
 // Streaming (read-once) loads of the matrix: skip L1, evict-first in L2 so the re-used
+
 // x vector (3 planes at a time, ~2 MB at 300^3) stays L2-resident.
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;
@@ -1116,6 +1164,14 @@ __device__ __forceinline__ double symm_fold(const double *__restrict__ x, const 
     return sum;
 }
 
+// Tile visited at position tau: the band order (tile_order) and/or last to first (reverse;
+// every row's sum and the exact pAp are independent of the order, C4/C5)
+__device__ __forceinline__ int64_t symm_tile_at(const SpmvArgs &a, int64_t tau, int64_t ntiles) {
+    const int64_t t = a.reverse ? ntiles - 1 - tau : tau;
+    return a.tile_order ? (int64_t)a.tile_order[t] : t;
+}
+
+
 template <bool DOT, int NW, int NST>
 __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     k_spmv_symm(SpmvArgs a, const __grid_constant__ CUtensorMap tm3,
@@ -1128,9 +1184,12 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     __shared__ __align__(8) uint64_t full_bar[NST], val_bar[NST], empty_bar[NST];
     __shared__ unsigned long long sacc[ACC_WORDS];
     __shared__ int sdig[ACC_DIG16];
+    if (threadIdx.x == 0) SYMM_STAMP(0);
+    KT_SCOPE(0, a.k);
     if (DOT && a.st && a.st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
+        SYMM_STAMP(1);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&val_bar[s], 1);
@@ -1160,7 +1219,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
             int64_t i = 0;
             for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
-                const int64_t tile = a.tile_order ? (int64_t)a.tile_order[tau] : tau;
+                const int64_t tile = symm_tile_at(a, tau, ntiles);
                 const int st = (int)(i % NST);
                 if (i >= NST) mbar_wait(&empty_bar[st], (uint32_t)(((i / NST) & 1) ^ 1));
                 const int64_t s0 = tile * NW;
@@ -1177,8 +1236,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                     // now, so that stage's first barrier completes at L2 latency (large
                     // problems; 300^3 -0.7 % per iteration, 100^3 +0.7 %)
                     const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
-                    const int64_t s2 =
-                        (a.tile_order && tau2 < ntiles ? (int64_t)a.tile_order[tau2] : tau2) * NW;
+                    const int64_t s2 = tau2 < ntiles ? symm_tile_at(a, tau2, ntiles) * NW : m.nslices;
                     if (tau2 < ntiles && s2 < m.nslices) {
                         const int64_t r2 = m.nslices - s2;
                         const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
@@ -1220,9 +1278,10 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
         int64_t i = 0;
         for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
-            const int64_t tile = a.tile_order ? (int64_t)a.tile_order[tau] : tau;
+            const int64_t tile = symm_tile_at(a, tau, ntiles);
             const int st = (int)(i % NST);
             mbar_wait(&full_bar[st], (uint32_t)((i / NST) & 1));
+            if (i == 0 && threadIdx.x == 0) SYMM_STAMP(2);
             const int64_t s = tile * NW + warp;
             if (s < m.nslices) {
                 const unsigned char *buf = smem + (size_t)st * C::STAGE_B;
@@ -1253,6 +1312,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 // no shared-memory read of the stage can still be in flight)
                 asm volatile("" ::"d"(sum) : "memory");
                 __syncwarp();
+                if (i == 0 && threadIdx.x == 0) SYMM_STAMP(3);
                 if (lane == 0) mbar_arrive(&empty_bar[st]);
                 if (row >= 0) {
                     a.y[row] = sum;
@@ -1263,13 +1323,17 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 if (lane == 0) mbar_arrive(&empty_bar[st]);
             }
         }
+        if (threadIdx.x == 0) SYMM_STAMP(4);
         if (DOT) expansion_flush_digits(ex, sdig, sacc);
     }
     if (DOT) {
         __syncthreads();
+        if (threadIdx.x == 0) SYMM_STAMP(5);
         acc_merge_to_global(sacc, sdig, a.acc);
         if (a.fold_push) acc_push_last_cta(a.dc, a.acc, a.k, 0, a.dc.local + 3);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) SYMM_STAMP(6);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1476,17 +1540,30 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     __shared__ int sdig[ACC_DIG16];
     __shared__ double s_alpha;
     __shared__ int s_stop;
+    KT_SCOPE(1, k);
+    K6_STAMP(0);
     if (a.st->done) return;
+    K6_STAMP(1);
     acc_zero_shared(sacc, sdig);
     if (!acc_in_load(s_in, a, k, 0)) return;
     __syncthreads();
+    K6_STAMP(2);
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
+    K6_STAMP(7);
+#ifdef SYMM_TRACE
+    {   // the same rounding again: warm instruction cache
+        const double f2 = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;
+        if (threadIdx.x == 0 && f2 != fin) a.st->status = 99;
+        K6_STAMP(8);
+    }
+#endif
     if (threadIdx.x == 0) {
         double alpha;
         s_stop = xr_prologue(a, fin, k, alpha);
         s_alpha = alpha;
     }
     __syncthreads();
+    K6_STAMP(3);
     if (s_stop) return;
     const double alpha = s_alpha;
     EX ex;
@@ -1578,10 +1655,18 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
             a.r[i] = ri;
         }
     }
+    K6_STAMP(4);
+#ifdef SYMM_TRACE
+    __syncthreads();
+    K6_STAMP(9);
+#endif
     expansion_flush_digits(ex, sdig, sacc);
     __syncthreads();
+    K6_STAMP(5);
     acc_merge_to_global(sacc, sdig, a.acc_out);
     if (a.fold_push) acc_push_last_cta(a.dc, a.acc_out, k, 1, a.dc.local + 4);
+    __syncthreads();
+    K6_STAMP(6);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -2134,6 +2219,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
     __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta;
     __shared__ int s_stop;
+    KT_SCOPE(2, k);
     if (a.st->done) return;              // K6 stopped: x_finish applies what is pending
     if (!acc_in_load(s_in, a, k, 1)) return;
     __syncthreads();

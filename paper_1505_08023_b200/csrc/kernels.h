@@ -131,6 +131,7 @@ struct SpmvArgs {
     int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
     int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
     const int32_t *tile_order;          // SYMM: tile visited at position tau (null: tau itself)
+    int reverse;                        // SYMM: visit the positions last to first
     int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
     const double *x;                    // [ncols], extended-box order
     double *y;                          // [rows]

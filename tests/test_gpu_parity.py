@@ -196,7 +196,9 @@ def test_sym_fallback_kernel_bit_identical(n):
 
 @pytest.mark.parametrize("opts", [{"x_late": 0}, {"cluster_dd": 0, "small_solver": 2},
                                   {"graph": 0}, {"spmv_impl": 0}, {"val_evict_first": 1},
-                                  {"x_prefetch": 1, "small_solver": 0}])
+                                  {"x_prefetch": 1, "small_solver": 0},
+                                  {"snake": 1, "small_solver": 0},
+                                  {"snake": 1, "band_rows": 1000, "small_solver": 0}])
 def test_other_options_bit_identical(opts):
     fmt = M.FMT_SEG if "spmv_impl" in opts else M.FMT_SYM
     _solver_variant((10, 10, 10), fmt, opts)
