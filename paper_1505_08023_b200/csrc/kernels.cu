@@ -1465,8 +1465,8 @@ __device__ __forceinline__ void xr_step(double &x, double &r, double p, double a
 // Decisions of K6 (a3, C6): finalise pAp, stop tests, alpha.  Thread 0 of each CTA (s_in =
 // shared copy of the all-reduced accumulator); every CTA takes the same decision, CTA 0
 // records it.  Returns stop.
-__device__ __forceinline__ int xr_prologue(const UpdArgs &a, double pAp, int k, double &alpha) {
-    const double rr = a.rr[k - 1];
+__device__ __forceinline__ int xr_prologue_v(const UpdArgs &a, double pAp, int k, double rr,
+                                             double &alpha) {
     int stop = 0, status = 0, conv = 0;
     if (!isfinite(pAp)) {
         stop = 1;
@@ -1493,16 +1493,21 @@ __device__ __forceinline__ int xr_prologue(const UpdArgs &a, double pAp, int k, 
     return stop;
 }
 
-// Decisions after rr_k (a5, C6): finalise rr_k, hist[k], stop tests, beta_k.
-__device__ __forceinline__ int rr_decision(double rr_new, int k, double *hist, double *rr,
-                                           CgState *st, double &beta) {
+__device__ __forceinline__ int xr_prologue(const UpdArgs &a, double pAp, int k, double &alpha) {
+    return xr_prologue_v(a, pAp, k, a.rr[k - 1], alpha);
+}
+
+// Decisions after rr_k (a5, C6): finalise rr_k, hist[k], stop tests, beta_k.  rr_old =
+// rr[k-1] and stop_thr = st->stop, loaded by the caller (ahead of the accumulator rounding).
+__device__ __forceinline__ int rr_decision_v(double rr_new, int k, double rr_old,
+                                             double stop_thr, double *hist, double *rr,
+                                             CgState *st, double &beta) {
     const double h = __dsqrt_rn(rr_new);
-    const double rr_old = rr[k - 1];
     int stop = 0, status = 0, conv = 0;
     if (!isfinite(rr_new)) {
         stop = 1;
         status = 7;
-    } else if (rr_new == 0.0 || h <= st->stop) {
+    } else if (rr_new == 0.0 || h <= stop_thr) {
         stop = 1;
         conv = 1;
     }
@@ -1521,9 +1526,39 @@ __device__ __forceinline__ int rr_decision(double rr_new, int k, double *hist, d
     return stop;
 }
 
+__device__ __forceinline__ int rr_decision(double rr_new, int k, double *hist, double *rr,
+                                           CgState *st, double &beta) {
+    return rr_decision_v(rr_new, k, rr[k - 1], st->stop, hist, rr, st, beta);
+}
+
 // Decisions of K7 (a5, C6).
 __device__ __forceinline__ int p_prologue(const UpdArgs &a, double rr_new, int k, double &beta) {
     return rr_decision(rr_new, k, a.hist, a.rr, a.st, beta);
+}
+
+// Entry of K6 / K7 on one-rank accumulators (no device comm): the stop flag, the accumulator
+// words (threads < ACC_WORDS, into s_in) and the scalars thread 0's decision needs are loaded
+// together, one memory round trip instead of three dependent ones.  Returns false when the
+// solve has stopped.  With device comm: the flag wait of acc_in_load.
+struct PreScalars {
+    double rr_old, stop_thr, alpha;
+};
+__device__ __forceinline__ bool upd_entry(const UpdArgs &a, int k, int which,
+                                          unsigned long long *s_in, PreScalars &ps) {
+    const bool local = a.dc.local == nullptr;
+    unsigned long long w = 0ull;
+    if (local && threadIdx.x < ACC_WORDS) w = __ldcg(a.acc_in + threadIdx.x);
+    if (threadIdx.x == 0) {
+        ps.rr_old = a.rr[k - 1];
+        ps.stop_thr = a.st->stop;
+        ps.alpha = a.st->alpha;
+    }
+    if (a.st->done) return false;
+    if (local) {
+        if (threadIdx.x < ACC_WORDS) s_in[threadIdx.x] = w;
+        return true;
+    }
+    return acc_in_load(s_in, a, k, which);
 }
 
 // XL: x is updated by K7 (see launch_update_xr); K6 touches r only: 24 instead of 48 B/row.
@@ -1542,10 +1577,10 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     __shared__ int s_stop;
     KT_SCOPE(1, k);
     K6_STAMP(0);
-    if (a.st->done) return;
+    PreScalars ps;
+    if (!upd_entry(a, k, 0, s_in, ps)) return;
     K6_STAMP(1);
     acc_zero_shared(sacc, sdig);
-    if (!acc_in_load(s_in, a, k, 0)) return;
     __syncthreads();
     K6_STAMP(2);
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
@@ -1559,7 +1594,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
 #endif
     if (threadIdx.x == 0) {
         double alpha;
-        s_stop = xr_prologue(a, fin, k, alpha);
+        s_stop = xr_prologue_v(a, fin, k, ps.rr_old, alpha);
         s_alpha = alpha;
     }
     __syncthreads();
@@ -2101,14 +2136,14 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     __shared__ unsigned long long s_in[ACC_WORDS];
     __shared__ double s_beta, s_alpha;
     __shared__ int s_stop;
-    if (a.st->done) return;              // K6 stopped (pAp test): no x update for this k
-    if (!acc_in_load(s_in, a, k, 1)) return;
+    PreScalars ps;                       // K6 stopped (pAp test): no x update for this k
+    if (!upd_entry(a, k, 1, s_in, ps)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
-        if (XL) s_alpha = a.st->alpha;   // alpha_k, written by K6 before this launch
+        if (XL) s_alpha = ps.alpha;      // alpha_k, written by K6 before this launch
         double beta;
-        s_stop = p_prologue(a, fin, k, beta);
+        s_stop = rr_decision_v(fin, k, ps.rr_old, ps.stop_thr, a.hist, a.rr, a.st, beta);
         s_beta = beta;
     }
     __syncthreads();
@@ -2220,13 +2255,13 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p2(UpdArgs a, int k, con
     __shared__ double s_beta;
     __shared__ int s_stop;
     KT_SCOPE(2, k);
-    if (a.st->done) return;              // K6 stopped: x_finish applies what is pending
-    if (!acc_in_load(s_in, a, k, 1)) return;
+    PreScalars ps;                       // K6 stopped: x_finish applies what is pending
+    if (!upd_entry(a, k, 1, s_in, ps)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     if (threadIdx.x == 0) {
         double beta;
-        s_stop = p_prologue(a, fin, k, beta);
+        s_stop = rr_decision_v(fin, k, ps.rr_old, ps.stop_thr, a.hist, a.rr, a.st, beta);
         s_beta = beta;
     }
     __syncthreads();
