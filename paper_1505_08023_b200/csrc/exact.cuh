@@ -151,9 +151,12 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
     const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
     if (e == 0x7ff) acc_add(acc, v);                          // flag word
     if (dmax1 == 0u) return;                                  // warp-uniform
-    const int lo = (int)dmax1 - 1 - 8;
-    const bool inwin = nz && d16 >= lo;
+    const bool inwin = nz && d16 >= (int)dmax1 - 1 - 8;
     if (nz && !inwin) acc_add(acc, v);                        // far below: slow path
+    // window [lo, dmax + 4]: from the lowest in-window digit, so lanes of similar magnitude
+    // need ~6 warp sums instead of 13
+    const int lo = (int)__reduce_min_sync(FULL, inwin ? (unsigned)d16 : 0xffffffffu);
+    const int nsum = (int)dmax1 + 4 - lo;
     const unsigned long long mlo = m << s16;
     const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
     int ch[5];
@@ -166,19 +169,21 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
 #pragma unroll
         for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
     }
-    // the 13 warp sums back to back (no branch between them), then lane t adds sum t
+    // the nsum (<= 13) warp sums back to back, then lane t adds sum t
     int mine = 0;
 #pragma unroll
     for (int t = 0; t < 13; ++t) {
-        const int q = lo + t - d16;
-        int contrib = 0;
+        if (t < nsum) {                                       // warp-uniform
+            const int q = lo + t - d16;
+            int contrib = 0;
 #pragma unroll
-        for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
-        const int sum = __reduce_add_sync(FULL, contrib);
-        mine = lane == (unsigned)t ? sum : mine;
+            for (int qq = 0; qq < 5; ++qq) contrib = (inwin && q == qq) ? ch[qq] : contrib;
+            const int sum = __reduce_add_sync(FULL, contrib);
+            mine = lane == (unsigned)t ? sum : mine;
+        }
     }
     const int D = lo + (int)lane;
-    if (lane < 13u && mine != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], mine);
+    if ((int)lane < nsum && mine != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], mine);
 }
 
 __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int *dig,
@@ -339,10 +344,15 @@ __device__ __forceinline__ double acc_finalize_warp(const unsigned long long *s)
     const long long hprev = __shfl_up_sync(FULL, hi[2], 1);
     const long long u[3] = {lo[0] + (lane ? hprev : 0ll), lo[1] + hi[0], lo[2] + hi[1]};
     unsigned G = map_after(carry_map(u[2]), map_after(carry_map(u[1]), carry_map(u[0])));
+    // inclusive scan G_l o ... o G_0; a constant map (carry out independent of the carry in:
+    // the usual case for every lane) is its own prefix, so the scan is skipped when all are
+    const bool cst = map_at(G, 0) == map_at(G, 1) && map_at(G, 1) == map_at(G, 2);
+    if (!__all_sync(FULL, cst)) {
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {               // inclusive scan: G_l o ... o G_0
-        const unsigned prev = __shfl_up_sync(FULL, G, off);
-        if (lane >= off) G = map_after(G, prev);
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned prev = __shfl_up_sync(FULL, G, off);
+            if (lane >= off) G = map_after(G, prev);
+        }
     }
     const unsigned Gex = __shfl_up_sync(FULL, G, 1);
     long long c = lane ? (long long)map_at(Gex, 1) - 1 : 0ll;   // carry into digit 3l

@@ -1325,6 +1325,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
         }
         if (threadIdx.x == 0) SYMM_STAMP(4);
         if (DOT) expansion_flush_digits(ex, sdig, sacc);
+        if (threadIdx.x == 0) SYMM_STAMP(7);
     }
     if (DOT) {
         __syncthreads();

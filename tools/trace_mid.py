@@ -48,8 +48,9 @@ t = t[t[:, 0] > 0]
 t = t[t[:, 0] >= t[:, 0].max() - 10**7]          # this solve's last launch
 t0 = t[:, 0].min()
 ph = {}
-names = ["entry", "setup", "first_runs", "first_fold", "last_tile", "flush", "merge"]
-for j in range(7):
+names = ["entry", "setup", "first_runs", "first_fold", "last_tile", "flush", "merge",
+         "warp0_flushed"]
+for j in range(8):
     ph[names[j] + "_from_t0"] = [int(np.median(t[:, j] - t0)), int((t[:, j] - t0).max())]
 k6 = (ctypes.c_ulonglong * (2048 * 16))()
 assert lib.minife_dbg_k6_trace(k6, 2048 * 16) == 0
