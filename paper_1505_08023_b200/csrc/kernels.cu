@@ -1186,9 +1186,65 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     __shared__ int sdig[ACC_DIG16];
     if (threadIdx.x == 0) SYMM_STAMP(0);
     KT_SCOPE(0, a.k);
-    if (DOT && a.st && a.st->done) return;
+    // the stop flag is read while the first stages are already in flight (the matrix does
+    // not depend on it): one memory latency less at the head of every SpMV
+    const int done = (DOT && a.st) ? a.st->done : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
+    const Matrix &m = a.m;
+    const int64_t ntiles = (m.nslices + NW - 1) / NW;
+    const int64_t N0 = a.g.ext_n[0], P = (int64_t)a.g.ext_n[0] * a.g.ext_n[1];
+    const bool producer = warp == NW && lane == 0;
+    uint64_t pol = 0, pol_keep = 0;
+    // stage i of this CTA <- tile position tau (producer lane only)
+    auto issue = [&](int64_t tau, int64_t i) {
+        const int64_t tile = symm_tile_at(a, tau, ntiles);
+        const int st = (int)(i % NST);
+        if (i >= NST) mbar_wait(&empty_bar[st], (uint32_t)(((i / NST) & 1) ^ 1));
+        const int64_t s0 = tile * NW;
+        const int64_t rem = m.nslices - s0;
+        const int nsl = rem < NW ? (int)rem : NW;
+        unsigned char *buf = smem + (size_t)st * C::STAGE_B;
+        const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
+        const int64_t r0 = s0 * 32;
+        mbar_expect_tx(&full_bar[st], bs + bm);
+        bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
+        bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
+        if (a.x_prefetch) {
+            // the run starts and masks of the tile this stage takes next: into L2 now, so
+            // that stage's first barrier completes at L2 latency (large problems; 300^3
+            // -0.7 % per iteration, 100^3 +0.7 %)
+            const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
+            const int64_t s2 = tau2 < ntiles ? symm_tile_at(a, tau2, ntiles) * NW : m.nslices;
+            if (tau2 < ntiles && s2 < m.nslices) {
+                const int64_t r2 = m.nslices - s2;
+                const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             ::"l"(m.seg + s2 * 9 * 32), "r"(n2 * 9 * 32 * 4) : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             ::"l"(m.mask + s2 * 32), "r"(n2 * 32 * 4) : "memory");
+            }
+        }
+        mbar_expect_tx(&val_bar[st], bv + 4 * C::MIR3_B + C::MIR1_B);
+        bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &val_bar[st], pol_keep);
+        if (a.x_prefetch) {
+            // the tile's plane-ahead x (its dz = +1 runs) is read here for the first time:
+            // start it into L2 now, so the consumers' gathers hit L2, not HBM
+            int64_t lo = r0 + P - N0 - 1, hi = r0 + 32 * nsl + P + N0 + 1;
+            lo = ((lo < 0 ? 0 : lo) + 1) & ~(int64_t)1;
+            hi = (hi > a.g.ncols ? a.g.ncols : hi) & ~(int64_t)1;
+            if (hi > lo && !(reinterpret_cast<uintptr_t>(a.x) & 15))
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + lo),
+                             "r"((uint32_t)((hi - lo) * 8))
+                             : "memory");
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+            tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
+                     11 - 3 * g, &val_bar[st]);
+        tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
+                 &val_bar[st]);
+    };
+    if (producer) {
         SYMM_STAMP(1);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -1196,76 +1252,37 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
             mbar_init(&empty_bar[s], NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm1)) : "memory");
+        pol = evict_first_policy();
+        if (a.val_evict_first)
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_keep));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+        for (int64_t i = 0; i < NST && blockIdx.x + i * gridDim.x < ntiles; ++i)
+            issue(blockIdx.x + i * gridDim.x, i);
     }
-    if (DOT) {
-        acc_zero_shared(sacc, sdig);
-        if (blockIdx.x == 0 && a.acc_zero)
-            for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
+    if (DOT) acc_zero_shared(sacc, sdig);
+    __syncthreads();                                   // barrier inits visible to all warps
+    if (done) {
+        // the solve has stopped: nothing to compute, but the stages in flight must land
+        // before the CTA may exit
+        if (producer)
+            for (int64_t i = 0; i < NST && blockIdx.x + i * gridDim.x < ntiles; ++i) {
+                mbar_wait(&full_bar[i], 0u);
+                mbar_wait(&val_bar[i], 0u);
+            }
+        return;
     }
-    __syncthreads();
-    const Matrix &m = a.m;
-    const int64_t ntiles = (m.nslices + NW - 1) / NW;
-    const int64_t N0 = a.g.ext_n[0], P = (int64_t)a.g.ext_n[0] * a.g.ext_n[1];
+    if (DOT && blockIdx.x == 0 && a.acc_zero)
+        for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
 
     if (warp == NW) {
         if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm1)) : "memory");
-            const uint64_t pol = evict_first_policy();
-            uint64_t pol_keep;
-            if (a.val_evict_first)
-                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_keep));
-            else
-                asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
-            int64_t i = 0;
-            for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
-                const int64_t tile = symm_tile_at(a, tau, ntiles);
-                const int st = (int)(i % NST);
-                if (i >= NST) mbar_wait(&empty_bar[st], (uint32_t)(((i / NST) & 1) ^ 1));
-                const int64_t s0 = tile * NW;
-                const int64_t rem = m.nslices - s0;
-                const int nsl = rem < NW ? (int)rem : NW;
-                unsigned char *buf = smem + (size_t)st * C::STAGE_B;
-                const uint32_t bv = nsl * 14 * 32 * 8, bs = nsl * 9 * 32 * 4, bm = nsl * 32 * 4;
-                const int64_t r0 = s0 * 32;
-                mbar_expect_tx(&full_bar[st], bs + bm);
-                bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
-                bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
-                if (a.x_prefetch) {
-                    // the run starts and masks of the tile this stage takes next: into L2
-                    // now, so that stage's first barrier completes at L2 latency (large
-                    // problems; 300^3 -0.7 % per iteration, 100^3 +0.7 %)
-                    const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
-                    const int64_t s2 = tau2 < ntiles ? symm_tile_at(a, tau2, ntiles) * NW : m.nslices;
-                    if (tau2 < ntiles && s2 < m.nslices) {
-                        const int64_t r2 = m.nslices - s2;
-                        const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                     ::"l"(m.seg + s2 * 9 * 32), "r"(n2 * 9 * 32 * 4) : "memory");
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                     ::"l"(m.mask + s2 * 32), "r"(n2 * 32 * 4) : "memory");
-                    }
-                }
-                mbar_expect_tx(&val_bar[st], bv + 4 * C::MIR3_B + C::MIR1_B);
-                bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &val_bar[st], pol_keep);
-                if (a.x_prefetch) {
-                    // the tile's plane-ahead x (its dz = +1 runs) is read here for the first
-                    // time: start it into L2 now, so the consumers' gathers hit L2, not HBM
-                    int64_t lo = r0 + P - N0 - 1, hi = r0 + 32 * nsl + P + N0 + 1;
-                    lo = ((lo < 0 ? 0 : lo) + 1) & ~(int64_t)1;
-                    hi = (hi > a.g.ncols ? a.g.ncols : hi) & ~(int64_t)1;
-                    if (hi > lo && !(reinterpret_cast<uintptr_t>(a.x) & 15))
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + lo),
-                                     "r"((uint32_t)((hi - lo) * 8))
-                                     : "memory");
-                }
-#pragma unroll
-                for (int g = 0; g < 4; ++g)
-                    tma_box3(buf + C::MIR0 + g * C::MIR3_B, &tm3, 0, symm_box_slice(r0, g, N0, P),
-                             11 - 3 * g, &val_bar[st]);
-                tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
-                         &val_bar[st]);
-            }
+            int64_t i = NST;
+            for (int64_t tau = blockIdx.x + (int64_t)NST * gridDim.x; tau < ntiles;
+                 tau += gridDim.x, ++i)
+                issue(tau, i);
         }
     } else {
         SymmExpansion ex;
