@@ -1123,11 +1123,11 @@ constexpr unsigned SYM_FULL = (1u << 27) - 1;               // all 27 slots pres
 // faster while nothing spills but far slower late in CG (the tier overflows into the atomics);
 // a 4-term drained tier or a third 4-term tier spills registers (128 per thread: 4 warps on
 // an SM sub-partition share its 16 K registers).
-#ifndef SYMM_EXP_A
-#define SYMM_EXP_A 4
-#define SYMM_EXP_B 4
-#endif
-using SymmExpansion = ExpansionT<SYMM_EXP_A, SYMM_EXP_B>;
+// Two 2-term tiers where the solve is short of SpMV time (mid-size: fewer terms to flush at
+// the end of every launch; B200, per solve 60^3 -2.7 %, 100^3 -1.3 %) and two 4-term tiers on
+// large problems (300^3: +0.9 % with 2 + 2, the late iterations spill more);
+// profiles/r02/ab/symm_expansion_tiers.jsonl.  Any tiers give the same exact sum.
+constexpr int64_t SYMM_SMALL_TIER_SLICES = 1 << 17;        // 4.2 M rows
 
 // One row of a SYMM tile in the order of C4: the 13 mirrored lower entries, then the 14 stored
 // ones (diagonal first).  FULL: every slot present (warp-uniform), no predicates.  Returns the
@@ -1172,7 +1172,7 @@ __device__ __forceinline__ int64_t symm_tile_at(const SpmvArgs &a, int64_t tau, 
 }
 
 
-template <bool DOT, int NW, int NST>
+template <bool DOT, int NW, int NST, int EA, int EB>
 __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
     k_spmv_symm(SpmvArgs a, const __grid_constant__ CUtensorMap tm3,
                 const __grid_constant__ CUtensorMap tm1) {
@@ -1285,7 +1285,7 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                 issue(tau, i);
         }
     } else {
-        SymmExpansion ex;
+        ExpansionT<EA, EB> ex;
         ex.init();
         // box g of a tile starts at row r0 + K_g, K_g = 32 floor((off_g - 1) / 32): column c of
         // slot q sits at element madj[g] + q GS 32 + (c - r0) of the stage's mirror area
@@ -2935,20 +2935,29 @@ static bool sym_maps(const Matrix &m, int gs, CUtensorMap *m3, CUtensorMap *m1) 
                CUDA_SUCCESS;
 }
 
+template <bool DOT, int NW, int NST, int EA, int EB>
+static cudaError_t launch_symm_t(const SpmvArgs &a, const CUtensorMap &m3, const CUtensorMap &m1,
+                                 cudaStream_t s) {
+    using C = SymmCfg<NW, NST>;
+    static unsigned long long attr_set = 0;
+    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST, EA, EB>, C::SMEM, attr_set);
+    if (e != cudaSuccess) return e;
+    query_occupancy();
+    const int64_t ntiles = (a.m.nslices + NW - 1) / NW;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
+    k_spmv_symm<DOT, NW, NST, EA, EB><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
+    return cudaGetLastError();
+}
+
 template <bool DOT, int NW, int NST>
 static cudaError_t launch_symm(const SpmvArgs &a, cudaStream_t s) {
     using C = SymmCfg<NW, NST>;
     static_assert(C::SMEM + 1536 <= 232448, "SYMM tile exceeds shared memory");
     CUtensorMap m3, m1;
     if (!sym_maps(a.m, C::GS, &m3, &m1)) return cudaErrorNotSupported;
-    static unsigned long long attr_set = 0;
-    cudaError_t e = ensure_smem_attr(k_spmv_symm<DOT, NW, NST>, C::SMEM, attr_set);
-    if (e != cudaSuccess) return e;
-    query_occupancy();
-    const int64_t ntiles = (a.m.nslices + NW - 1) / NW;
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, g_sms));
-    k_spmv_symm<DOT, NW, NST><<<g, C::THREADS, C::SMEM, s>>>(a, m3, m1);
-    return cudaGetLastError();
+    if (DOT && a.m.nslices < SYMM_SMALL_TIER_SLICES)
+        return launch_symm_t<DOT, NW, NST, 2, 2>(a, m3, m1, s);
+    return launch_symm_t<DOT, NW, NST, 4, 4>(a, m3, m1, s);
 }
 
 // SYM tile shape (B200, 300^3: 16 consumer warps x 2 stages 0.90 ms/launch, 12 x 3 0.95 ms,
