@@ -1561,6 +1561,7 @@ __device__ __forceinline__ int p_prologue(const UpdArgs &a, double rr_new, int k
 struct PreScalars {
     double rr_old, stop_thr, alpha;
 };
+static_assert(UPD_THREADS >= ACC_WORDS, "upd_entry loads one accumulator word per thread");
 __device__ __forceinline__ bool upd_entry(const UpdArgs &a, int k, int which,
                                           unsigned long long *s_in, PreScalars &ps) {
     const bool local = a.dc.local == nullptr;
