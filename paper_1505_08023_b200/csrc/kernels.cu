@@ -1604,13 +1604,6 @@ __global__ void __launch_bounds__(UPD_THREADS, 3) k_update_xr(UpdArgs a, int k) 
     K6_STAMP(2);
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
     K6_STAMP(7);
-#ifdef SYMM_TRACE
-    {   // the same rounding again: warm instruction cache
-        const double f2 = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;
-        if (threadIdx.x == 0 && f2 != fin) a.st->status = 99;
-        K6_STAMP(8);
-    }
-#endif
     if (threadIdx.x == 0) {
         double alpha;
         s_stop = xr_prologue_v(a, fin, k, ps.rr_old, alpha);

@@ -60,7 +60,7 @@ u = u[u[:, 0] >= u[:, 0].max() - 10**7]
 u0 = u[:, 0].min()
 k6ph = {}
 for j, nm in enumerate(["entry", "done_read", "acc_in", "prologue", "loop", "flush", "merge",
-                        "finalized", "finalized_again", "loop_all"]):
+                        "finalized", "unused", "loop_all"]):
     k6ph[nm] = [int(np.median(u[:, j] - u0)), int((u[:, j] - u0).max())]
 print(json.dumps({"n": n, "options": opts, "solve_ms": r.seconds * 1e3, "ctas": len(t),
                   "iters": rows, "symm_last_launch": ph, "k6_ctas": len(u),
