@@ -197,8 +197,16 @@ __device__ __forceinline__ void expansion_flush_digits(const Expansion &ex, int 
 // goes to a second one (N2 terms), then a third (N3, optional), and only what none holds
 // reaches the shared-memory atomics (64-bit CAS loops).  Exact like Expansion; costs nothing
 // while the first tier absorbs every term.
+#ifdef EXP_STATS
+// Diagnostic builds only: how many additions reach the second tier / the shared atomics
+static __device__ unsigned long long g_exp_stats[4];
+extern "C" int minife_dbg_exp_stats(unsigned long long *out, int reset);
+#endif
 template <int N1, int N2, int N3 = 0> struct ExpansionT {
     double a[N1], b[N2], c[N3 > 0 ? N3 : 1];
+#ifdef EXP_STATS
+    unsigned n_add = 0, n_t2 = 0, n_spill = 0;
+#endif
     __device__ __forceinline__ void init() {
 #pragma unroll
         for (int j = 0; j < N1; ++j) a[j] = 0.0;
@@ -208,9 +216,15 @@ template <int N1, int N2, int N3 = 0> struct ExpansionT {
         for (int j = 0; j < N3; ++j) c[j] = 0.0;
     }
     __device__ __forceinline__ void add(double x, unsigned long long *spill) {
+#ifdef EXP_STATS
+        ++n_add;
+#endif
 #pragma unroll
         for (int j = 0; j < N1; ++j) two_sum(a[j], x, a[j], x);
         if (x != 0.0) {
+#ifdef EXP_STATS
+            ++n_t2;
+#endif
 #pragma unroll
             for (int j = 0; j < N2; ++j) two_sum(b[j], x, b[j], x);
 
@@ -218,6 +232,9 @@ template <int N1, int N2, int N3 = 0> struct ExpansionT {
 #pragma unroll
                 for (int j = 0; j < N3; ++j) two_sum(c[j], x, c[j], x);
             }
+#ifdef EXP_STATS
+            if (x != 0.0) ++n_spill;
+#endif
             if (x != 0.0) acc_add(spill, x);  // also routes NaN to the flag word
         }
     }
@@ -227,6 +244,15 @@ using Expansion2 = ExpansionT<NEXP, NEXP>;
 template <int N1, int N2, int N3>
 __device__ __forceinline__ void expansion_flush_digits(const ExpansionT<N1, N2, N3> &ex, int *dig,
                                                        unsigned long long *acc) {
+#ifdef EXP_STATS
+    {
+        const unsigned v[3] = {ex.n_add, ex.n_t2, ex.n_spill};
+        for (int q = 0; q < 3; ++q) {
+            const unsigned t = __reduce_add_sync(0xffffffffu, v[q]);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&g_exp_stats[q], (unsigned long long)t);
+        }
+    }
+#endif
 #pragma unroll
     for (int j = 0; j < N1; ++j) flush_value_digits(ex.a[j], dig, acc);
 #pragma unroll

@@ -99,6 +99,15 @@ extern "C" int minife_dbg_kt(unsigned long long *out, int reset) {
 #define KT_SCOPE(kind, k) ((void)0)
 #define K6_STAMP(i) ((void)0)
 #endif
+#ifdef EXP_STATS
+extern "C" int minife_dbg_exp_stats(unsigned long long *out, int reset) {
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        return (int)cudaMemcpyToSymbol(g_exp_stats, z, sizeof z);
+    }
+    return (int)cudaMemcpyFromSymbol(out, g_exp_stats, sizeof(unsigned long long) * 4);
+}
+#endif
 
 // Streaming (read-once) loads of the matrix: skip L1, evict-first in L2 so the re-used
 
