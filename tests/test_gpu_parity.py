@@ -510,6 +510,20 @@ def test_100cubed_full_parity(fmt):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("parts,transport", [(2, None), (4, "device")])
+def test_100cubed_partitioned_snake_order(parts, transport):
+    """configs[1] in RCB parts of 40-80 MB of matrix each, where the SYM SpMV alternates its
+    tile order every iteration (snake order, automatic for 48-400 MB): bitwise the oracle,
+    through the default and the device-initiated transports."""
+    n = (100, 100, 100)
+    with M.Minife(*n, virtual=parts) as g:
+        if transport == "device":
+            g.set_transport(M.TRANSPORT_DEVICE)
+        g.assemble()
+        check_cg(g, n, 200, 0.0)
+
+
+@pytest.mark.slow
 def test_300cubed_sampled_parity():
     """configs[2] at full size, in the bench's launch configuration: sampled rows of A and y
     against the oracle's per-row routine, and p-independence of the whole CG (P10)."""
