@@ -1805,9 +1805,16 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs
             ex.add(__dmul_rn(b, b), sacc);
         }
     }
+    // thread 0 keeps rr_(k-1) and the stop threshold (the values cg_state_init records) in
+    // registers: no global round trip in the decisions
+    double rr_prev = 0.0, stop_thr = 0.0;
     {
         const double rr0 = small_block_dot(ex, dig, sacc);
-        if (tid == 0) cg_state_init(a, rr0, tol);
+        if (tid == 0) {
+            cg_state_init(a, rr0, tol);
+            rr_prev = rr0;
+            stop_thr = __dmul_rn(tol, __dsqrt_rn(rr0));
+        }
     }
     __syncthreads();
     for (int k = 1; k <= K; ++k) {
@@ -1825,7 +1832,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs
             const double pAp = small_block_dot(ex, dig, sacc);
             if (tid == 0) {
                 double alpha;
-                s_stop = xr_prologue(a, pAp, k, alpha);
+                s_stop = xr_prologue_v(a, pAp, k, rr_prev, alpha);
                 s_coef = alpha;
             }
         }
@@ -1843,8 +1850,9 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_cg_small(Matrix m, UpdArgs
             const double rrn = small_block_dot(ex, dig, sacc);
             if (tid == 0) {
                 double beta;
-                s_stop = rr_decision(rrn, k, a.hist, a.rr, a.st, beta);
+                s_stop = rr_decision_v(rrn, k, rr_prev, stop_thr, a.hist, a.rr, a.st, beta);
                 s_coef = beta;
+                rr_prev = rrn;
             }
         }
         __syncthreads();
@@ -2058,10 +2066,17 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
     }
     cl.sync();                                     // matrix, counters and p in place everywhere
     int par = 0;
+    // thread 0 of every CTA keeps rr_(k-1) and the stop threshold (the values CTA 0's
+    // cg_state_init records) in registers: no global round trip in the decisions
+    double rr_prev = 0.0, stop_thr = 0.0;
     {
         const double rr0 = cluster_dot<DD>(ex, S, cl, par);
         par ^= 1;
         if (q == 0 && tid == 0) cg_state_init(a, rr0, tol);
+        if (tid == 0) {
+            rr_prev = rr0;
+            stop_thr = __dmul_rn(tol, __dsqrt_rn(rr0));
+        }
     }
     for (int k = 1; k <= K; ++k) {
         // a2 + a3: Ap = A p (own rows), exact pAp, alpha
@@ -2088,7 +2103,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
             par ^= 1;
             if (tid == 0) {
                 double alpha;
-                S.stop = xr_prologue(a, pAp, k, alpha);   // CTA 0 records (blockIdx.x == 0)
+                S.stop = xr_prologue_v(a, pAp, k, rr_prev, alpha);   // CTA 0 records
                 S.coef = alpha;
             }
         }
@@ -2116,8 +2131,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
             par ^= 1;
             if (tid == 0) {
                 double beta;
-                S.stop = rr_decision(rrn, k, a.hist, a.rr, a.st, beta);
+                S.stop = rr_decision_v(rrn, k, rr_prev, stop_thr, a.hist, a.rr, a.st, beta);
                 S.coef = beta;
+                rr_prev = rrn;
             }
         }
         __syncthreads();

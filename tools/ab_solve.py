@@ -27,7 +27,10 @@ for k0 in (51, 181):
     for _ in range(2):
         g.cg_solve(200, 0.0)
     t = [g.cg_solve(200, 0.0).seconds * 1e3 for _ in range(reps)]
-    s, it = g.timing_window()
+    try:
+        s, it = g.timing_window()
+    except M.MinifeError:                  # single-launch solvers: no window inside
+        s = it = 0.0
     out[f"w{k0}"] = {"spmv_ms": s, "iter_ms": it}
     out.setdefault("solve_ms", []).extend(t)
 out["median_ms"] = statistics.median(out["solve_ms"])
