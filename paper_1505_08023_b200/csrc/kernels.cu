@@ -1934,6 +1934,7 @@ __device__ __forceinline__ void dig_add(double v, int *dig) {
         if (ch[q]) atomicAdd(&dig[d16 + q], neg ? -ch[q] : ch[q]);
 }
 
+
 // Exact cluster-wide dot of the CTAs' expansions (all threads of every CTA call it); the
 // rounded value is returned to warp 0 of every CTA.  Each CTA reduces into its own digit
 // counters and adds the nonzero ones into EVERY CTA's receive counters (DSMEM atomics);
@@ -2058,10 +2059,14 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
         const int sl = warp + CL_WARPS * j;
         const int64_t row = (s_lo + sl) * 32 + lane;
         xv[j] = rv[j] = apv[j] = 0.0;
-        if (sl < nsl && row < rows) {
-            rv[j] = a.b[row];
-            if (DD) dig_add(__dmul_rn(rv[j], rv[j]), S.dig);
-            else ex.add(__dmul_rn(rv[j], rv[j]), S.sacc);
+        if (sl < nsl) {                                // warp-uniform
+            double v = 0.0;
+            if (row < rows) {
+                rv[j] = a.b[row];
+                v = __dmul_rn(rv[j], rv[j]);
+                if (!DD) ex.add(v, S.sacc);
+            }
+            if (DD) dig_add(v, S.dig);            // v = 0: nothing
         }
     }
     cl.sync();                                     // matrix, counters and p in place everywhere
@@ -2085,17 +2090,21 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
         for (int j = 0; j < CL_RPT; ++j) {
             const int sl = warp + CL_WARPS * j;
             const int64_t row = (s_lo + sl) * 32 + lane;
-            if (sl < nsl && row < rows) {
-                const unsigned msk = S.mask[sl][lane];
-                double sum = 0.0;
+            if (sl < nsl) {                            // warp-uniform
+                double v = 0.0;
+                if (row < rows) {
+                    const unsigned msk = S.mask[sl][lane];
+                    double sum = 0.0;
 #pragma unroll
-                for (int t = 0; t < 27; ++t)
-                    if ((msk >> t) & 1u)
-                        sum = __dadd_rn(sum, __dmul_rn(S.val[sl][t][lane],
-                                                       S.pfull[S.seg[sl][t / 3][lane] + t % 3]));
-                apv[j] = sum;
-                if (DD) dig_add(__dmul_rn(S.pfull[row], sum), S.dig);
-                else ex.add(__dmul_rn(S.pfull[row], sum), S.sacc);
+                    for (int t = 0; t < 27; ++t)
+                        if ((msk >> t) & 1u)
+                            sum = __dadd_rn(sum, __dmul_rn(S.val[sl][t][lane],
+                                                           S.pfull[S.seg[sl][t / 3][lane] + t % 3]));
+                    apv[j] = sum;
+                    v = __dmul_rn(S.pfull[row], sum);
+                    if (!DD) ex.add(v, S.sacc);
+                }
+                if (DD) dig_add(v, S.dig);            // v = 0: nothing
             }
         }
         {
@@ -2116,14 +2125,18 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(Matrix m, UpdArgs 
         for (int j = 0; j < CL_RPT; ++j) {
             const int sl = warp + CL_WARPS * j;
             const int64_t row = (s_lo + sl) * 32 + lane;
-            if (sl < nsl && row < rows) {
-                if (DD) {
-                    xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha, S.pfull[row]));
-                    rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha, apv[j]));
-                    dig_add(__dmul_rn(rv[j], rv[j]), S.dig);
-                } else {
-                    xr_step(xv[j], rv[j], S.pfull[row], apv[j], alpha, ex, S.sacc);
+            if (sl < nsl) {                            // warp-uniform
+                double v = 0.0;
+                if (row < rows) {
+                    if (DD) {
+                        xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha, S.pfull[row]));
+                        rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha, apv[j]));
+                        v = __dmul_rn(rv[j], rv[j]);
+                    } else {
+                        xr_step(xv[j], rv[j], S.pfull[row], apv[j], alpha, ex, S.sacc);
+                    }
                 }
+                if (DD) dig_add(v, S.dig);            // v = 0: nothing
             }
         }
         {
