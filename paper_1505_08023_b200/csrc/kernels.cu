@@ -1218,21 +1218,6 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
         mbar_expect_tx(&full_bar[st], bs + bm);
         bulk_g2s(buf + C::VAL_B, m.seg + s0 * 9 * 32, bs, &full_bar[st], pol);
         bulk_g2s(buf + C::VAL_B + C::SEG_B, m.mask + s0 * 32, bm, &full_bar[st], pol);
-        if (a.x_prefetch) {
-            // the run starts and masks of the tile this stage takes next: into L2 now, so
-            // that stage's first barrier completes at L2 latency (large problems; 300^3
-            // -0.7 % per iteration, 100^3 +0.7 %)
-            const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
-            const int64_t s2 = tau2 < ntiles ? symm_tile_at(a, tau2, ntiles) * NW : m.nslices;
-            if (tau2 < ntiles && s2 < m.nslices) {
-                const int64_t r2 = m.nslices - s2;
-                const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             ::"l"(m.seg + s2 * 9 * 32), "r"(n2 * 9 * 32 * 4) : "memory");
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             ::"l"(m.mask + s2 * 32), "r"(n2 * 32 * 4) : "memory");
-            }
-        }
         mbar_expect_tx(&val_bar[st], bv + 4 * C::MIR3_B + C::MIR1_B);
         bulk_g2s(buf, m.val + s0 * 14 * 32, bv, &val_bar[st], pol_keep);
         if (a.x_prefetch) {
@@ -1252,6 +1237,22 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
                      11 - 3 * g, &val_bar[st]);
         tma_box3(buf + C::MIR0 + 4 * C::MIR3_B, &tm1, 0, symm_box_slice(r0, 4, N0, P), 1,
                  &val_bar[st]);
+        if (a.x_prefetch) {
+            // the run starts and masks of the tile this stage takes next: into L2 now, so
+            // that stage's first barrier completes at L2 latency (large problems; 300^3
+            // -0.7 % per iteration, 100^3 +0.7 %).  After this stage's copies: with a tile
+            // order the next tile's index is a global load the copies must not wait for.
+            const int64_t tau2 = tau + (int64_t)NST * gridDim.x;
+            const int64_t s2 = tau2 < ntiles ? symm_tile_at(a, tau2, ntiles) * NW : m.nslices;
+            if (tau2 < ntiles && s2 < m.nslices) {
+                const int64_t r2 = m.nslices - s2;
+                const uint32_t n2 = r2 < NW ? (uint32_t)r2 : (uint32_t)NW;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             ::"l"(m.seg + s2 * 9 * 32), "r"(n2 * 9 * 32 * 4) : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             ::"l"(m.mask + s2 * 32), "r"(n2 * 32 * 4) : "memory");
+            }
+        }
     };
     if (producer) {
         SYMM_STAMP(1);
@@ -1303,8 +1304,13 @@ __global__ void __launch_bounds__(SymmCfg<NW, NST>::THREADS, 1)
         for (int g = 0; g < 5; ++g)
             madj[g] = g * (C::MIR3_B / 8) - 32 * symm_box_slice(0, g, N0, P);
         int64_t i = 0;
+        // with a tile order the tile index is a global load: fetch the next one a tile ahead,
+        // so it is not a dependent L2 round trip at the head of every tile (300^3 banded: the
+        // stall on its first use took ~10 % of the kernel's warp samples)
+        int64_t tile_next = blockIdx.x < ntiles ? symm_tile_at(a, blockIdx.x, ntiles) : 0;
         for (int64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++i) {
-            const int64_t tile = symm_tile_at(a, tau, ntiles);
+            const int64_t tile = tile_next;
+            if (tau + gridDim.x < ntiles) tile_next = symm_tile_at(a, tau + gridDim.x, ntiles);
             const int st = (int)(i % NST);
             mbar_wait(&full_bar[st], (uint32_t)((i / NST) & 1));
             if (i == 0 && threadIdx.x == 0) SYMM_STAMP(2);
