@@ -137,6 +137,11 @@ struct Expansion {
 // and 32-bit shared atomics are native (the 64-bit ones are CAS loops).
 constexpr int ACC_DIG16 = 2 * ACC_DIGITS;
 
+#ifdef FLUSH_STATS
+// Diagnostic builds only (tools/flush_stats.py): [kernel: 0 SpMV, 1 K6 (256 threads)][calls
+// with a nonzero value, lanes on the slow path, sum of warp sums, calls]
+static __device__ unsigned long long g_flush_stats[2][4];
+#endif
 // One value per lane into the 16-bit digit counters, warp-aggregated (all lanes, converged)
 __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned long long *acc) {
     const unsigned FULL = 0xffffffffu;
@@ -149,6 +154,9 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
     const int pos = e ? e - 1 : 0;
     const int d16 = pos >> 4, s16 = pos & 15;
     const unsigned dmax1 = __reduce_max_sync(FULL, nz ? (unsigned)d16 + 1u : 0u);
+#ifdef FLUSH_STATS
+    if (lane == 0) atomicAdd(&g_flush_stats[blockDim.x == 256 ? 1 : 0][3], 1ull);
+#endif
     if (e == 0x7ff) acc_add(acc, v);                          // flag word
     if (dmax1 == 0u) return;                                  // warp-uniform
     const bool inwin = nz && d16 >= (int)dmax1 - 1 - 8;
@@ -157,6 +165,17 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
     // need ~6 warp sums instead of 13
     const int lo = (int)__reduce_min_sync(FULL, inwin ? (unsigned)d16 : 0xffffffffu);
     const int nsum = (int)dmax1 + 4 - lo;
+#ifdef FLUSH_STATS
+    {
+        const unsigned slow = __popc(__ballot_sync(FULL, nz && !inwin));
+        if (lane == 0) {
+            const int kk = blockDim.x == 256 ? 1 : 0;
+            atomicAdd(&g_flush_stats[kk][0], 1ull);
+            atomicAdd(&g_flush_stats[kk][1], (unsigned long long)slow);
+            atomicAdd(&g_flush_stats[kk][2], (unsigned long long)nsum);
+        }
+    }
+#endif
     const unsigned long long mlo = m << s16;
     const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
     int ch[5];

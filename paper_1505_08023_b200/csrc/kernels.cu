@@ -99,6 +99,15 @@ extern "C" int minife_dbg_kt(unsigned long long *out, int reset) {
 #define KT_SCOPE(kind, k) ((void)0)
 #define K6_STAMP(i) ((void)0)
 #endif
+#ifdef FLUSH_STATS
+extern "C" int minife_dbg_flush_stats(unsigned long long *out, int reset) {
+    if (reset) {
+        unsigned long long z[8] = {0};
+        return (int)cudaMemcpyToSymbol(g_flush_stats, z, sizeof z);
+    }
+    return (int)cudaMemcpyFromSymbol(out, g_flush_stats, sizeof(unsigned long long) * 8);
+}
+#endif
 #ifdef EXP_STATS
 extern "C" int minife_dbg_exp_stats(unsigned long long *out, int reset) {
     if (reset) {
