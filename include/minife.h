@@ -227,6 +227,10 @@ int minife_set_stream(minife_ctx *ctx, void *stream);
  *   "comm_fault_part" fault injection for tests: the part / rank with this id never pushes
  *                     its accumulators or halo (device comm), so its peers time out into
  *                     MINIFE_ECOMM; -1 (default) off
+ *   "symm_nw"         SYM SpMV tile width (consumer warps = 32-row slices per tile), applied
+ *                     at the next minife_assemble: -1 (default) 11 where N_x >= 352 (a tile's
+ *                     x lines then need the larger L1 of the narrower ring), 13 otherwise;
+ *                     11 or 13 force it
  * A changed option drops the captured graph.  Errors: MINIFE_EINVAL (NULL, unknown name,
  * value out of range). */
 int minife_set_option(minife_ctx *ctx, const char *name, int64_t value);

@@ -106,6 +106,7 @@ struct Part {
     double *d_xin = nullptr, *d_yout = nullptr;   // minife_spmv buffers (lazy)
     // exact accumulators, parity double-buffered: [pAp_0, rr_0, pAp_1, rr_1] x ACC_WORDS
     unsigned long long *d_acc = nullptr;
+    int symm_nw = SYMM_NW;                        // SYM SpMV tile width, fixed at assembly
     CgState *d_st = nullptr;
     double *d_hist = nullptr, *d_rr = nullptr;
     double *d_alpha = nullptr;                    // alpha_k history (x every second iteration)
@@ -212,6 +213,7 @@ struct minife_ctx {
         int snake = -1;            // SYM SpMV: odd iterations visit the tiles last to first
         int comm_timeout_ms = 60000;   // device comm: spin limit before MINIFE_ECOMM
         int comm_fault_part = -1;  // fault injection (tests): this rank / part never signals
+        int symm_nw = -1;          // SYM SpMV tile width: -1 auto (by N_x), 11 or 13
     } opt;
     bool devcomm_ready = false;                  // regions + peer tables built
     int cur_max_iters = 0;                       // max_iters of the solve being enqueued
@@ -965,10 +967,13 @@ extern "C" int minife_set_option(minife_ctx *c, const char *name, int64_t value)
         {"snake", &c->opt.snake, -1, 1},
         {"comm_timeout_ms", &c->opt.comm_timeout_ms, 1, 3600000},
         {"comm_fault_part", &c->opt.comm_fault_part, -1, 1 << 20},
+        {"symm_nw", &c->opt.symm_nw, -1, SYMM_NW},
     };
     for (auto &t : table) {
         if (strcmp(t.name, name) != 0) continue;
-        if (value < t.lo || value > t.hi) {
+        if (value < t.lo || value > t.hi ||
+            (t.field == &c->opt.symm_nw && value != -1 && value != SYMM_NW &&
+             value != SYMM_NW_WIDE)) {
             set_err(c, "option %s: value %lld outside [%d, %d]", name, (long long)value, t.lo, t.hi);
             return MINIFE_EINVAL;
         }
@@ -1148,11 +1153,17 @@ static int build_tile_order(minife_ctx *c, Part &p) {
         p.tile_order_n = 0;
         drop_graph(c);
     };
+    const int64_t N0 = p.plan.ext_n[0], N1 = p.plan.ext_n[1];
+    // the tile width the SpMV runs with: the order is in its tiles, so both change together
+    const int nw = c->opt.symm_nw > 0 ? c->opt.symm_nw : symm_nw_auto(N0);
+    if (nw != p.symm_nw) {
+        p.symm_nw = nw;
+        drop_graph(c);
+    }
     if (c->fmt != MINIFE_FMT_SYM) {
         drop_order();
         return MINIFE_OK;
     }
-    const int64_t N0 = p.plan.ext_n[0], N1 = p.plan.ext_n[1];
     const int64_t P = N0 * N1;
     const int64_t target = c->opt.band_rows < 0 ? BAND_ROWS_AUTO : c->opt.band_rows;
     if (target == 0 || (c->opt.band_rows < 0 && P <= BAND_MIN_PLANE) || P <= target) {
@@ -1161,10 +1172,10 @@ static int build_tile_order(minife_ctx *c, Part &p) {
     }
     const int64_t B = std::max<int64_t>(8, target / N0);               // lines per band
     const int64_t nslices = (p.ncols + 31) / 32;
-    const int64_t ntiles = (nslices + SYMM_NW - 1) / SYMM_NW;
+    const int64_t ntiles = (nslices + nw - 1) / nw;
     std::vector<std::pair<int64_t, int32_t>> key(ntiles);
     for (int64_t t = 0; t < ntiles; ++t) {
-        const int64_t r = t * SYMM_NW * 32;
+        const int64_t r = t * nw * 32;
         const int64_t ey = (r / N0) % N1, ez = r / P;
         key[t] = {(ey / B) * (int64_t)1e12 + ez * (int64_t)1e6 + 0, (int32_t)t};
     }
@@ -1467,6 +1478,7 @@ static SpmvArgs spmv_args(const minife_ctx *c, Part &p, const double *x, double 
     const int xpf = c->opt.x_prefetch;
     a.x_prefetch = xpf >= 0 ? xpf : (8.0 * (double)p.ncols > 64e6 ? 1 : 0);
     a.sym_kernel = c->opt.sym_kernel;
+    a.symm_nw = p.symm_nw;
     a.impl = c->opt.spmv_impl;
     a.tile_order = c->fmt == MINIFE_FMT_SYM ? p.d_tile_order : nullptr;
     // L2 reuse of the matrix across the solve's SpMVs (snake_of): the visiting order does not

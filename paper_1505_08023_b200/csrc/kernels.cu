@@ -3015,7 +3015,8 @@ static cudaError_t launch_sym(const SpmvArgs &a, cudaStream_t s) {
     // 300^3: 1.196 ms per CG iteration vs 1.243 with L1 mirror gathers, profiles/r01/session2);
     // the ctx option "sym_kernel" = 0 (or no tensor-map support) selects the L1-gather kernel
     if (a.sym_kernel != 0) {
-        const cudaError_t e = launch_symm<DOT, SYMM_NW, 2>(a, s);
+        const cudaError_t e = a.symm_nw == SYMM_NW_WIDE ? launch_symm<DOT, SYMM_NW_WIDE, 2>(a, s)
+                                                        : launch_symm<DOT, SYMM_NW, 2>(a, s);
         if (e != cudaErrorNotSupported) return e;
         // (no tensor-map support: the L1-gather kernel below, same results; the library
         // never prints)

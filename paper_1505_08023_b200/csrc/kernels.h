@@ -130,6 +130,7 @@ struct SpmvArgs {
     int val_evict_first;                // SYMM: stream the values evict-first in L2
     int x_prefetch;                     // SYMM: warm L2 with each tile's plane-ahead x
     int sym_kernel;                     // SYM: 1 tensor-map mirror kernel, 0 L1-gather kernel
+    int symm_nw;                        // SYM tensor-map kernel tile width: SYMM_NW(_WIDE)
     const int32_t *tile_order;          // SYMM: tile visited at position tau (null: tau itself)
     int reverse;                        // SYMM: visit the positions last to first
     int impl;                           // SEG/CRS: -1 default, 1 TMA pipeline, 0 registers
@@ -277,8 +278,15 @@ cudaError_t probe_bandwidth(int64_t bytes, int reps, double *read_gbs, double *c
 int spmv_grid(int64_t nslices, int fmt);
 int stream_grid(int64_t rows);
 
-// SYMM kernel tile: SYMM_NW slices of 32 rows (the unit of SpmvArgs::tile_order)
-constexpr int SYMM_NW = 13;
+// SYMM kernel tile: NW slices of 32 rows, one consumer warp each (the unit of
+// SpmvArgs::tile_order).  13 by default; 11 where a tile's nine x lines (9 N_x doubles) exceed
+// the ~28 KB of L1 left beside the 13-wide ring (226 KB of shared memory): the 11-wide ring
+// (189 KB) fits the 196 KB carveout and leaves ~60 KB of L1 (B200, per solve: 400^3 -2.1 %;
+// 300^3 +2 %, 100^3 +1.5 % -- there the x lines fit anyway and 13 warps hide more latency;
+// profiles/r02/ab/symm_nw_wide.jsonl)
+constexpr int SYMM_NW = 13, SYMM_NW_WIDE = 11;
+constexpr int64_t SYMM_WIDE_N0 = 352;
+static inline int symm_nw_auto(int64_t n0) { return n0 >= SYMM_WIDE_N0 ? SYMM_NW_WIDE : SYMM_NW; }
 
 constexpr int SPMV_THREADS = 256;
 constexpr int UPD_THREADS = 256;

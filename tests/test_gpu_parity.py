@@ -198,7 +198,10 @@ def test_sym_fallback_kernel_bit_identical(n):
                                   {"graph": 0}, {"spmv_impl": 0}, {"val_evict_first": 1},
                                   {"x_prefetch": 1, "small_solver": 0},
                                   {"snake": 1, "small_solver": 0},
-                                  {"snake": 1, "band_rows": 1000, "small_solver": 0}])
+                                  {"snake": 1, "band_rows": 1000, "small_solver": 0},
+                                  {"symm_nw": 11, "small_solver": 0},
+                                  {"symm_nw": 11, "band_rows": 1000, "small_solver": 0},
+                                  {"symm_nw": 11, "snake": 1, "small_solver": 0}])
 def test_other_options_bit_identical(opts):
     fmt = M.FMT_SEG if "spmv_impl" in opts else M.FMT_SYM
     _solver_variant((10, 10, 10), fmt, opts)
@@ -241,11 +244,16 @@ def test_band_order_bit_identical_across_reassembly(band):
         g.set_option("band_rows", band)
         g.assemble()
         check_cg(g, n, 100, 1e-10)
+        g.set_option("symm_nw", 11)              # narrower tiles: a new order, a new graph
+        g.assemble()
+        check_cg(g, n, 200, 0.0)
+        check_spmv(g, s, 2)
 
 
 def test_option_errors():
     with M.Minife(3, 3, 3) as g:
-        for name, v in (("no_such_option", 1), ("x_defer", 9), ("graph", 2), ("small_solver", -2)):
+        for name, v in (("no_such_option", 1), ("x_defer", 9), ("graph", 2), ("small_solver", -2),
+                        ("symm_nw", 12), ("symm_nw", 0)):
             with pytest.raises(M.MinifeError) as e:
                 g.set_option(name, v)
             assert e.value.status == M.MINIFE_EINVAL
