@@ -159,6 +159,38 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
 #endif
     if (e == 0x7ff) acc_add(acc, v);                          // flag word
     if (dmax1 == 0u) return;                                  // warp-uniform
+    const unsigned long long mlo = m << s16;
+    const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
+    int ch[5];
+    ch[0] = (int)(mlo & 0xffff);
+    ch[1] = (int)((mlo >> 16) & 0xffff);
+    ch[2] = (int)((mlo >> 32) & 0xffff);
+    ch[3] = (int)(mlo >> 48);
+    ch[4] = (int)mhi;
+    if (bits >> 63) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
+    }
+    if (__all_sync(FULL, !nz || d16 == (int)dmax1 - 1)) {
+        // every nonzero lane has the same top digit (the usual case): the window is that
+        // digit's five chunks, summed straight across the warp
+        int mine = 0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            const int sum = __reduce_add_sync(FULL, nz ? ch[t] : 0);
+            mine = lane == (unsigned)t ? sum : mine;
+        }
+        const int D = (int)dmax1 - 1 + (int)lane;
+        if (lane < 5u && mine != 0 && D < ACC_DIG16) atomicAdd(&dig[D], mine);
+#ifdef FLUSH_STATS
+        if (lane == 0) {
+            const int kk = blockDim.x == 256 ? 1 : 0;
+            atomicAdd(&g_flush_stats[kk][0], 1ull);
+            atomicAdd(&g_flush_stats[kk][2], 5ull);
+        }
+#endif
+        return;
+    }
     const bool inwin = nz && d16 >= (int)dmax1 - 1 - 8;
     if (nz && !inwin) acc_add(acc, v);                        // far below: slow path
     // window [lo, dmax + 4]: from the lowest in-window digit, so lanes of similar magnitude
@@ -176,18 +208,6 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
         }
     }
 #endif
-    const unsigned long long mlo = m << s16;
-    const unsigned long long mhi = s16 ? (m >> (64 - s16)) : 0ull;
-    int ch[5];
-    ch[0] = (int)(mlo & 0xffff);
-    ch[1] = (int)((mlo >> 16) & 0xffff);
-    ch[2] = (int)((mlo >> 32) & 0xffff);
-    ch[3] = (int)(mlo >> 48);
-    ch[4] = (int)mhi;
-    if (bits >> 63) {
-#pragma unroll
-        for (int q = 0; q < 5; ++q) ch[q] = -ch[q];
-    }
     // the nsum (<= 13) warp sums back to back, then lane t adds sum t
     int mine = 0;
 #pragma unroll
