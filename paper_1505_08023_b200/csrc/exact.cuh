@@ -191,6 +191,28 @@ __device__ __forceinline__ void flush_value_digits(double v, int *dig, unsigned 
 #endif
         return;
     }
+    if (__all_sync(FULL, !nz || d16 >= (int)dmax1 - 2)) {
+        // top digits one apart: a 6-digit window from dmax - 1; a lane whose top digit is
+        // dmax contributes its chunk t - 1 to window digit t
+        const bool up = nz && d16 == (int)dmax1 - 1;
+        int mine = 0;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+            const int c = !nz ? 0 : (up ? (t >= 1 ? ch[t - 1] : 0) : (t <= 4 ? ch[t] : 0));
+            const int sum = __reduce_add_sync(FULL, c);
+            mine = lane == (unsigned)t ? sum : mine;
+        }
+        const int D = (int)dmax1 - 2 + (int)lane;
+        if (lane < 6u && mine != 0 && D >= 0 && D < ACC_DIG16) atomicAdd(&dig[D], mine);
+#ifdef FLUSH_STATS
+        if (lane == 0) {
+            const int kk = blockDim.x == 256 ? 1 : 0;
+            atomicAdd(&g_flush_stats[kk][0], 1ull);
+            atomicAdd(&g_flush_stats[kk][2], 6ull);
+        }
+#endif
+        return;
+    }
     const bool inwin = nz && d16 >= (int)dmax1 - 1 - 8;
     if (nz && !inwin) acc_add(acc, v);                        // far below: slow path
     // window [lo, dmax + 4]: from the lowest in-window digit, so lanes of similar magnitude
