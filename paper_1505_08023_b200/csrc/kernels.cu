@@ -2202,6 +2202,16 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     __shared__ double s_beta, s_alpha;
     __shared__ int s_stop;
     PreScalars ps;                       // K6 stopped (pAp test): no x update for this k
+    // the thread's first pair of p, r (and x) is loaded ahead of the entry and the rounding:
+    // none of it depends on beta, and at mid-size the entry is most of K7
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool pre = IDENT && tid < (a.g.rows >> 1);
+    double2 e_p = make_double2(0.0, 0.0), e_r = e_p, e_x = e_p;
+    if (pre) {
+        e_p = reinterpret_cast<const double2 *>(a.p)[tid];
+        e_r = reinterpret_cast<const double2 *>(a.r)[tid];
+        if (XL) e_x = reinterpret_cast<const double2 *>(a.x)[tid];
+    }
     if (!upd_entry(a, k, 1, s_in, ps)) return;
     __syncthreads();
     const double fin = threadIdx.x < 32 ? acc_finalize_warp(s_in) : 0.0;   // warp 0
@@ -2217,7 +2227,6 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
     if (!stop && blockIdx.x == 0 && a.acc_zero)
         for (int i = threadIdx.x; i < ACC_WORDS; i += blockDim.x) a.acc_zero[i] = 0ull;
     const double beta = s_beta, alpha = XL ? s_alpha : 0.0;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t rows = a.g.rows;
     if (IDENT) {
@@ -2225,7 +2234,19 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update_p(UpdArgs a, int k) {
         double2 *p2 = reinterpret_cast<double2 *>(a.p);
         double2 *x2 = reinterpret_cast<double2 *>(a.x);
         const double2 *r2 = reinterpret_cast<const double2 *>(a.r);
-        int64_t i = tid;
+        if (pre) {
+            if (XL) {
+                e_x.x = __dadd_rn(e_x.x, __dmul_rn(alpha, e_p.x));
+                e_x.y = __dadd_rn(e_x.y, __dmul_rn(alpha, e_p.y));
+                x2[tid] = e_x;
+            }
+            if (!stop) {
+                e_p.x = __dadd_rn(e_r.x, __dmul_rn(beta, e_p.x));
+                e_p.y = __dadd_rn(e_r.y, __dmul_rn(beta, e_p.y));
+                p2[tid] = e_p;
+            }
+        }
+        int64_t i = tid + stride;
         for (; i + stride < n2; i += 2 * stride) {
             double2 pa = p2[i], pb = p2[i + stride];
             if (XL) {
